@@ -1,0 +1,458 @@
+// C ABI: search, single-arm GA, result accessors and the config-5 sweep.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+
+#include "engine.hpp"
+#include "eval_launch.hpp"
+#include "search.hpp"
+#include "sweep.hpp"
+
+using namespace hpg;
+
+struct hpg_ctx {
+  Ctx* impl;
+};
+
+struct hpg_search_result {
+  SearchOut out;
+  // chosen plan as a one-plan table
+  int32_t n_groups = 0;
+  std::vector<int32_t> task_group, gpu_counts, dp, pp, tp, stage_layers, devices, groups_flat;
+  std::vector<int64_t> sl_off, w_off, dev_off;
+  std::vector<double> weights;
+};
+
+namespace {
+
+void set_err(char* err, size_t errlen, const std::string& msg) {
+  if (err && errlen > 0) std::snprintf(err, errlen, "%s", msg.c_str());
+}
+
+template <typename F>
+int guarded(char* err, size_t errlen, F&& f) {
+  try {
+    f();
+    set_err(err, errlen, "");
+    return HPG_OK;
+  } catch (const UsageError& e) {
+    set_err(err, errlen, e.what());
+    return HPG_USAGE;
+  } catch (const InputError& e) {
+    set_err(err, errlen, e.what());
+    return HPG_INPUT;
+  } catch (const InfeasibleError& e) {
+    set_err(err, errlen, e.what());
+    return HPG_INFEASIBLE;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return HPG_INTERNAL;
+  } catch (...) {
+    set_err(err, errlen, "unknown engine failure");
+    return HPG_INTERNAL;
+  }
+}
+
+hpg_search_result* wrap(SearchOut&& s, const Problem& P) {
+  auto* r = new hpg_search_result();
+  r->out = std::move(s);
+  if (r->out.has_plan) {
+    const SearchOut& o = r->out;
+    const int T = P.T;
+    r->n_groups = static_cast<int32_t>(o.plan_groups.size());
+    r->task_group.assign(T, 0);
+    for (size_t g = 0; g < o.plan_groups.size(); ++g)
+      for (int sl : o.plan_groups[g]) {
+        r->task_group[sl] = static_cast<int32_t>(g);
+        r->groups_flat.push_back(sl);
+      }
+    r->gpu_counts.assign(T, 0);
+    for (size_t g = 0; g < o.plan_counts.size(); ++g) r->gpu_counts[g] = o.plan_counts[g];
+    const Cand& c = o.plan;
+    for (int t = 0; t < T; ++t) {
+      r->dp.push_back(c.hdr().dp[t]);
+      r->pp.push_back(c.hdr().pp[t]);
+      r->tp.push_back(c.hdr().tp[t]);
+      r->sl_off.push_back(c.o.sl[t]);
+      r->w_off.push_back(c.o.w[t]);
+      r->dev_off.push_back(c.o.dev[t]);
+    }
+    r->stage_layers.assign(c.sl(), c.sl() + c.o.sl[T]);
+    r->weights.assign(c.w(), c.w() + c.o.w[T]);
+    for (int i = 0; i < c.o.dev[T]; ++i) r->devices.push_back(c.dev()[i]);
+  }
+  return r;
+}
+
+// ---- sweep tables ----
+
+struct SweepHost {
+  SweepTablesDev tb{};
+  void* blob = nullptr;
+};
+
+std::map<Ctx*, SweepHost> g_sweep;
+
+SweepTablesDev& sweep_tables(Ctx& C) {
+  auto it = g_sweep.find(&C);
+  if (it != g_sweep.end()) return it->second.tb;
+  const Problem& P = C.prob;
+  if (P.N < P.T) throw InputError("sweep needs at least as many devices as workflow tasks");
+  const auto tgs = enumerate_task_groupings(P, false);
+  std::vector<int8_t> grp(tgs.size() * kMaxTasks, -1), ng(tgs.size());
+  for (size_t i = 0; i < tgs.size(); ++i) {
+    ng[i] = static_cast<int8_t>(tgs[i].size());
+    for (size_t g = 0; g < tgs[i].size(); ++g)
+      for (int s : tgs[i][g]) grp[i * kMaxTasks + s] = static_cast<int8_t>(g);
+  }
+  const int N = P.N, T = P.T;
+  std::vector<int32_t> off(T * (N + 1) + 1, 0);
+  std::vector<int16_t> opt;
+  int idx = 0;
+  for (int s = 0; s < T; ++s) {
+    for (int c = 0; c <= N; ++c) {
+      off[s * (N + 1) + c] = idx;
+      if (c == 0) continue;
+      for (int dp = 1; dp <= c; ++dp) {
+        if (c % dp) continue;
+        const int rest = c / dp;
+        for (int pp = 1; pp <= rest; ++pp) {
+          if (rest % pp) continue;
+          const int tp = rest / pp;
+          if (pp > P.tasks[s].nl || tp > P.max_node_size) continue;
+          opt.push_back(static_cast<int16_t>(dp));
+          opt.push_back(static_cast<int16_t>(pp));
+          opt.push_back(static_cast<int16_t>(tp));
+          ++idx;
+        }
+      }
+    }
+  }
+  off[T * (N + 1)] = idx;
+  const size_t b_grp = grp.size(), b_ng = ng.size(), b_off = 4 * off.size(), b_opt = 2 * opt.size();
+  const size_t o_ng = (b_grp + 15) & ~size_t(15);
+  const size_t o_off = (o_ng + b_ng + 15) & ~size_t(15);
+  const size_t o_opt = (o_off + b_off + 15) & ~size_t(15);
+  const size_t total = o_opt + b_opt + 16;
+  std::vector<uint8_t> blob(total, 0);
+  std::memcpy(blob.data(), grp.data(), b_grp);
+  std::memcpy(blob.data() + o_ng, ng.data(), b_ng);
+  std::memcpy(blob.data() + o_off, off.data(), b_off);
+  std::memcpy(blob.data() + o_opt, opt.data(), b_opt);
+  SweepHost h;
+  cuda_check(cudaMalloc(&h.blob, total), "cudaMalloc sweep tables");
+  cuda_check(cudaMemcpy(h.blob, blob.data(), total, cudaMemcpyHostToDevice), "H2D sweep tables");
+  uint8_t* b = static_cast<uint8_t*>(h.blob);
+  h.tb.n_dev = N;
+  h.tb.n_tasks = T;
+  h.tb.n_tgs = static_cast<int32_t>(tgs.size());
+  h.tb.tg_group = reinterpret_cast<const int8_t*>(b);
+  h.tb.tg_ng = reinterpret_cast<const int8_t*>(b + o_ng);
+  h.tb.opt_off = reinterpret_cast<const int32_t*>(b + o_off);
+  h.tb.opt = reinterpret_cast<const int16_t*>(b + o_opt);
+  return g_sweep.emplace(&C, h).first->second.tb;
+}
+
+struct SweepAcc {
+  double best = kInf;
+  uint64_t best_k = ~0ull, nf = 0, x = 0, bytes = 0;
+  float gen_ms = 0, eval_ms = 0, total_ms = 0;
+  int64_t launches = 0;
+};
+
+void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs,
+               uint8_t* feasible, SweepAcc& acc) {
+  const Problem& P = C.prob;
+  SweepTablesDev& tb = sweep_tables(C);
+  const int64_t stride = (80 + P.T * P.N + 7) & ~int64_t(7);
+  const int64_t chunk = static_cast<int64_t>(std::min<uint64_t>(count, 1ull << 20));
+  C.d_recs.reserve(static_cast<size_t>(chunk) * stride);
+  C.d_res.reserve(chunk);
+  C.d_best.reserve(2);
+  const int red_blocks = 4 * C.n_sm;
+  DevBuf<SweepPartial> partial;
+  partial.reserve(red_blocks);
+  std::vector<SweepPartial> hp(red_blocks);
+  Carve cv{};
+  cv.n_dev = P.N;
+  cv.n_tasks = P.T;
+  cv.max_w = cv.max_sl = cv.max_slots = cv.max_cells = cv.max_dpk = P.T * P.N;
+  const DevCostConfig cfg = to_dev_cfg(default_cost_config());
+  cudaStream_t st = C.stream;
+  cudaEvent_t e0, e1, e2, e3;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventCreate(&e3);
+  cuda_check(cudaMemsetAsync(C.d_best.p, 0, 16, st), "memset");
+  for (uint64_t done = 0; done < count;) {
+    const int64_t n = static_cast<int64_t>(std::min<uint64_t>(chunk, count - done));
+    const uint64_t kk = k0 + done;
+    cudaEventRecord(e0, st);
+    cuda_check(launch_gen(tb, seed, kk, n, C.d_recs.p, stride, C.d_best.p, st), "gen_kernel");
+    cudaEventRecord(e1, st);
+    cuda_check(launch_eval(C.dprob, cfg, cv, 0, C.d_recs.p, nullptr, nullptr, kModeE2E,
+                           static_cast<int>(n), stride, nullptr, C.d_res.p, nullptr, nullptr,
+                           C.n_sm, st),
+               "eval_kernel");
+    cudaEventRecord(e2, st);
+    cuda_check(launch_reduce(C.d_res.p, n, kk, partial.p, red_blocks, st), "reduce_kernel");
+    cudaEventRecord(e3, st);
+    acc.launches += 3;
+    C.launches += 3;
+    C.plans_evaluated += n;
+    cuda_check(cudaMemcpyAsync(hp.data(), partial.p, sizeof(SweepPartial) * red_blocks,
+                               cudaMemcpyDeviceToHost, st), "D2H partial");
+    if (costs || feasible) {
+      std::vector<EvalResult> r(n);
+      cuda_check(cudaMemcpyAsync(r.data(), C.d_res.p, sizeof(EvalResult) * n,
+                                 cudaMemcpyDeviceToHost, st), "D2H results");
+      cuda_check(cudaStreamSynchronize(st), "sweep");
+      for (int64_t i = 0; i < n; ++i) {
+        if (costs) costs[done + i] = r[i].cost;
+        if (feasible) feasible[done + i] = (r[i].flags & kResFeasOut) ? 1 : 0;
+      }
+    }
+    cuda_check(cudaStreamSynchronize(st), "sweep");
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, e0, e1);
+    cudaEventElapsedTime(&b, e1, e2);
+    cudaEventElapsedTime(&c, e2, e3);
+    acc.gen_ms += a;
+    acc.eval_ms += b;
+    acc.total_ms += a + b + c;
+    for (const SweepPartial& p : hp) {
+      acc.nf += p.n_feasible;
+      acc.x ^= p.xor_bits;
+      if (p.best < acc.best || (p.best == acc.best && p.best_k < acc.best_k)) {
+        acc.best = p.best;
+        acc.best_k = p.best_k;
+      }
+    }
+    done += n;
+  }
+  unsigned long long bytes = 0;
+  cuda_check(cudaMemcpy(&bytes, C.d_best.p, 8, cudaMemcpyDeviceToHost), "D2H bytes");
+  acc.bytes = bytes;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  cudaEventDestroy(e3);
+}
+
+}  // namespace
+
+extern "C" {
+
+int hpg_search(hpg_ctx* ctx, const hpg_knobs* knobs, hpg_search_result** out, char* err,
+               size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl || !knobs || !out) throw UsageError("hpg_search: null argument");
+    *out = nullptr;
+    Ctx& C = *ctx->impl;
+    const Knobs K = knobs_from_c(C.prob, *knobs);
+    if (K.budget < 1) throw UsageError("search budget must be >= 1");
+    *out = wrap(nested_sha_search(C, K, nullptr), C.prob);
+  });
+}
+
+int hpg_nccl_unique_id(uint8_t id_out[128], char* err, size_t errlen) {
+  return guarded(err, errlen, [&] { dist_unique_id(id_out); });
+}
+
+int hpg_search_dist(hpg_ctx* ctx, const hpg_knobs* knobs, int rank, int world,
+                    const uint8_t nccl_id[128], hpg_search_result** out, char* err,
+                    size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl || !knobs || !out) throw UsageError("hpg_search_dist: null argument");
+    *out = nullptr;
+    Ctx& C = *ctx->impl;
+    const Knobs K = knobs_from_c(C.prob, *knobs);
+    if (K.budget < 1) throw UsageError("search budget must be >= 1");
+    if (world <= 1) {
+      *out = wrap(nested_sha_search(C, K, nullptr), C.prob);
+      return;
+    }
+    Dist d;
+    dist_init(d, rank, world, nccl_id, C.device);
+    try {
+      *out = wrap(nested_sha_search(C, K, &d), C.prob);
+    } catch (...) {
+      dist_destroy(d);
+      throw;
+    }
+    dist_destroy(d);
+  });
+}
+
+int hpg_ga_search(hpg_ctx* ctx, const int32_t* task_group, int32_t n_groups,
+                  const int32_t* gpu_counts, int64_t budget_slice, uint64_t rng_seed,
+                  const hpg_knobs* knobs, hpg_search_result** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl || !knobs || !out || !task_group || !gpu_counts)
+      throw UsageError("hpg_ga_search: null argument");
+    *out = nullptr;
+    Ctx& C = *ctx->impl;
+    const Knobs K = knobs_from_c(C.prob, *knobs);
+    Grouping tg(n_groups);
+    for (int s = 0; s < C.prob.T; ++s) {
+      if (task_group[s] < 0 || task_group[s] >= n_groups)
+        throw InputError("task grouping must cover every workflow task");
+      tg[task_group[s]].push_back(s);
+    }
+    std::vector<int> counts(gpu_counts, gpu_counts + n_groups);
+    *out = wrap(ga_search(C, tg, counts, budget_slice, rng_seed, K), C.prob);
+  });
+}
+
+int hpg_result_info(const hpg_search_result* r, hpg_search_info* info) {
+  if (!r || !info) return HPG_USAGE;
+  const SearchOut& o = r->out;
+  info->budget = o.budget;
+  info->consumed = o.consumed;
+  info->seed = o.seed;
+  info->has_plan = o.has_plan ? 1 : 0;
+  info->n_b_m = static_cast<int32_t>(o.b_m.size());
+  info->n_trace = static_cast<int32_t>(o.trace.size());
+  info->n_arms = static_cast<int32_t>(o.arms.size());
+  info->n_halvings = static_cast<int32_t>(o.halvings.size());
+  info->n_survivor_sets = static_cast<int32_t>(o.survivors.size());
+  info->task_groupings = o.task_groupings;
+  info->wall_s = o.wall_s;
+  info->time_to_best_s = o.time_to_best_s;
+  info->gpu_launches = o.launches;
+  info->waves = o.waves;
+  info->plans_evaluated_gpu = o.plans_gpu;
+  return HPG_OK;
+}
+
+int hpg_result_b_m(const hpg_search_result* r, int64_t* b_m) {
+  if (!r || !b_m) return HPG_USAGE;
+  std::copy(r->out.b_m.begin(), r->out.b_m.end(), b_m);
+  return HPG_OK;
+}
+
+int hpg_result_trace(const hpg_search_result* r, int64_t* consumed, double* cost) {
+  if (!r) return HPG_USAGE;
+  for (size_t i = 0; i < r->out.trace.size(); ++i) {
+    if (consumed) consumed[i] = r->out.trace[i].first;
+    if (cost) cost[i] = r->out.trace[i].second;
+  }
+  return HPG_OK;
+}
+
+int hpg_result_arms(const hpg_search_result* r, int64_t* tg_index, int64_t* gg_index,
+                    double* best_cost, int64_t* evals) {
+  if (!r) return HPG_USAGE;
+  for (size_t i = 0; i < r->out.arms.size(); ++i) {
+    const ArmRec& a = r->out.arms[i];
+    if (tg_index) tg_index[i] = a.tg;
+    if (gg_index) gg_index[i] = a.gg;
+    if (best_cost) best_cost[i] = a.best;
+    if (evals) evals[i] = a.evals;
+  }
+  return HPG_OK;
+}
+
+int hpg_result_halvings(const hpg_search_result* r, int32_t* level, int64_t* before,
+                        int64_t* after, double* survivor_worst, double* eliminated_best) {
+  if (!r) return HPG_USAGE;
+  for (size_t i = 0; i < r->out.halvings.size(); ++i) {
+    const Halving& h = r->out.halvings[i];
+    if (level) level[i] = h.level;
+    if (before) before[i] = h.before;
+    if (after) after[i] = h.after;
+    if (survivor_worst) survivor_worst[i] = h.survivor_worst;
+    if (eliminated_best) eliminated_best[i] = h.eliminated_best;
+  }
+  return HPG_OK;
+}
+
+int hpg_result_survivor_sizes(const hpg_search_result* r, int32_t* sizes) {
+  if (!r || !sizes) return HPG_USAGE;
+  for (size_t i = 0; i < r->out.survivors.size(); ++i)
+    sizes[i] = static_cast<int32_t>(r->out.survivors[i].size());
+  return HPG_OK;
+}
+
+int hpg_result_survivors(const hpg_search_result* r, int64_t* idx) {
+  if (!r || !idx) return HPG_USAGE;
+  size_t k = 0;
+  for (const auto& s : r->out.survivors)
+    for (int64_t v : s) idx[k++] = v;
+  return HPG_OK;
+}
+
+int hpg_result_plan(const hpg_search_result* r, hpg_plan_table* plan, int32_t* groups_flat,
+                    double* estimated_cost_s, uint64_t* prov_seed, int64_t* prov_budget) {
+  if (!r) return HPG_USAGE;
+  if (!r->out.has_plan) return HPG_INFEASIBLE;
+  if (plan) {
+    plan->n_plans = 1;
+    plan->n_groups = &r->n_groups;
+    plan->task_group = r->task_group.data();
+    plan->gpu_counts = r->gpu_counts.data();
+    plan->dp = r->dp.data();
+    plan->pp = r->pp.data();
+    plan->tp = r->tp.data();
+    plan->sl_off = r->sl_off.data();
+    plan->stage_layers = r->stage_layers.data();
+    plan->w_off = r->w_off.data();
+    plan->weights = r->weights.data();
+    plan->dev_off = r->dev_off.data();
+    plan->devices = r->devices.data();
+  }
+  if (groups_flat) std::copy(r->groups_flat.begin(), r->groups_flat.end(), groups_flat);
+  if (estimated_cost_s) *estimated_cost_s = r->out.est_cost;
+  if (prov_seed) *prov_seed = r->out.seed;
+  if (prov_budget) *prov_budget = r->out.consumed;
+  return HPG_OK;
+}
+
+int hpg_result_breakdown(const hpg_search_result* r, double* per_task, double* reshard_s,
+                         double* sync_s, double* end_to_end_s, uint8_t* memory_feasible) {
+  if (!r) return HPG_USAGE;
+  if (!r->out.has_plan) return HPG_INFEASIBLE;
+  if (per_task) std::copy(r->out.per_task.begin(), r->out.per_task.end(), per_task);
+  if (reshard_s) *reshard_s = r->out.reshard_s;
+  if (sync_s) *sync_s = r->out.sync_s;
+  if (end_to_end_s) *end_to_end_s = r->out.e2e;
+  if (memory_feasible) *memory_feasible = r->out.feasible ? 1 : 0;
+  return HPG_OK;
+}
+
+void hpg_result_free(hpg_search_result* r) { delete r; }
+
+int hpg_sweep(hpg_ctx* ctx, uint64_t seed, uint64_t k0, uint64_t count, double* costs,
+              uint8_t* feasible, double* best_cost, uint64_t* best_k, uint64_t* n_feasible,
+              char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl) throw UsageError("hpg_sweep: null context");
+    SweepAcc acc;
+    run_sweep(*ctx->impl, seed, k0, count, costs, feasible, acc);
+    if (best_cost) *best_cost = acc.best;
+    if (best_k) *best_k = acc.best_k;
+    if (n_feasible) *n_feasible = acc.nf;
+  });
+}
+
+int hpg_sweep_resident(hpg_ctx* ctx, uint64_t seed, uint64_t k0, uint64_t count,
+                       hpg_sweep_stats* stats, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl || !stats) throw UsageError("hpg_sweep_resident: null argument");
+    SweepAcc acc;
+    run_sweep(*ctx->impl, seed, k0, count, nullptr, nullptr, acc);
+    stats->best_cost = acc.best;
+    stats->best_k = acc.best_k;
+    stats->n_feasible = acc.nf;
+    stats->xor_bits = acc.x;
+    stats->canonical_bytes = acc.bytes;
+    stats->total_ms = acc.total_ms;
+    stats->eval_ms = acc.eval_ms;
+    stats->gen_ms = acc.gen_ms;
+    stats->launches = acc.launches;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,177 @@
+// Shared host/device definitions of the B200 plan-search engine.
+//
+// The reference planner (hetplan, C++20, single-threaded) keeps plans as
+// std::map<int, ...> keyed by task id with device-id strings
+// (proj/include/hetplan/plan.hpp:59-70). The engine keeps them as packed
+// byte records (PlanRec below): integer device indices, per-task layout
+// triples, stage splits and replica weights, laid out so one warp can stage a
+// whole plan into shared memory with coalesced loads.
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define HPG_HD __host__ __device__ __forceinline__
+#else
+#define HPG_HD inline
+#endif
+
+namespace hpg {
+
+constexpr int kMaxTasks = 6;        // PPO: tasks 1..6 (workflow.cpp:64-69)
+constexpr int kMaxDevices = 256;    // device slots are u8 indices
+constexpr int kMaxClasses = 64;     // distinct (latency, bandwidth) link classes
+constexpr double kInf = __builtin_inf();
+
+enum TaskKind : int32_t { kGeneration = 0, kInference = 1, kTraining = 2 };
+
+// Task constants, workflow order (== task-id order, workflow.cpp:111-125).
+struct DevTask {
+  int32_t id;
+  int32_t kind;
+  int32_t precision_bytes;
+  int32_t include_embedding;
+  int64_t h1, h2, nl, vocab;
+  int64_t layer_params;  // ModelSpec::layer_params (workflow.hpp:27-30), int64
+  int64_t param_count;   // ModelSpec::param_count (workflow.hpp:34-36), int64
+};
+
+// Cost-model configuration (cost_model.hpp:13-28 + plan.hpp:83-89).
+struct DevCostConfig {
+  int32_t recompute;
+  int32_t dbs_cap;
+  double reshard_override;
+  double sync_override;
+  double dbs_override;
+  double train_bytes_per_param;
+  double infer_bytes_per_param;
+  double kv_bytes_per_elem;
+  double act_factor;
+};
+
+// Problem header, passed by value to every kernel. Arrays live in one device
+// allocation owned by the context.
+struct DevProblem {
+  int32_t n_dev;
+  int32_t n_tasks;
+  int32_t n_classes;
+  int32_t mode;       // 0 sync, 1 async
+  int32_t algorithm;  // 0 ppo, 1 grpo
+  int32_t gen_slot;   // slot of task id 1 or -1
+  int32_t train6_slot;  // slot of task id 6 or -1
+  int32_t max_tp;     // DeviceTopology::max_devices_per_node
+  double eta;
+  int64_t global_batch, rpp, seq_in, seq_out, mbs, total_seq;
+  DevTask task[kMaxTasks];
+  const double* comp;  // [n_dev] FLOP/s   (Device::comp, topology.hpp:33)
+  const double* mem;   // [n_dev] bytes    (Device::mem)
+  const double* hbm;   // [n_dev] bytes/s  (Device::hbm)
+  const uint8_t* cls;  // [n_dev * n_dev] link class of (a, b)
+  const double* lat;   // [n_classes] seconds
+  const double* bw;    // [n_classes] bytes/s (inf for self)
+};
+
+// ---- packed plan record ----
+//
+//   int32 bytes, int32 n_tasks, int32 dp[6], pp[6], tp[6]     (80 bytes)
+//   double  weights[sum dp]       replica_batch_weights per task
+//   int32   stage_layers[sum pp]
+//   uint8   devices[sum dp*pp*tp] flat (replica, stage, shard) order
+//   padding to 8 bytes
+struct RecHeader {
+  int32_t bytes;
+  int32_t n_tasks;
+  int32_t dp[kMaxTasks];
+  int32_t pp[kMaxTasks];
+  int32_t tp[kMaxTasks];
+};
+static_assert(sizeof(RecHeader) == 80, "record header layout");
+
+struct RecOffsets {
+  int32_t w[kMaxTasks + 1];    // index into weights (doubles)
+  int32_t sl[kMaxTasks + 1];   // index into stage layers (int32)
+  int32_t dev[kMaxTasks + 1];  // index into devices (bytes)
+  int32_t cell[kMaxTasks + 1];  // prefix of dp*pp
+  int32_t dpk[kMaxTasks + 1];   // prefix of pp*tp (dp-ring slots)
+  int32_t w_byte, sl_byte, dev_byte, bytes;
+};
+
+// n_tasks bit 16: compact record (no weight / stage-layer sections; unit
+// weights and make_layout's uniform split are implied, plan.cpp:89-100).
+constexpr int32_t kRecCompact = 1 << 16;
+
+HPG_HD void rec_offsets(const RecHeader& h, RecOffsets& o) {
+  o.w[0] = o.sl[0] = o.dev[0] = o.cell[0] = o.dpk[0] = 0;
+  const int nt = h.n_tasks & 0xffff;
+  for (int t = 0; t < nt; ++t) {
+    o.w[t + 1] = o.w[t] + h.dp[t];
+    o.sl[t + 1] = o.sl[t] + h.pp[t];
+    o.dev[t + 1] = o.dev[t] + h.dp[t] * h.pp[t] * h.tp[t];
+    o.cell[t + 1] = o.cell[t] + h.dp[t] * h.pp[t];
+    o.dpk[t + 1] = o.dpk[t] + h.pp[t] * h.tp[t];
+  }
+  const bool compact = (h.n_tasks & kRecCompact) != 0;
+  o.w_byte = static_cast<int32_t>(sizeof(RecHeader));
+  o.sl_byte = o.w_byte + (compact ? 0 : 8 * o.w[nt]);
+  o.dev_byte = o.sl_byte + (compact ? 0 : 4 * o.sl[nt]);
+  o.bytes = (o.dev_byte + o.dev[nt] + 7) & ~7;
+}
+
+// Per-plan request modes of the evaluation kernel.
+enum EvalMode : int32_t {
+  kModeMemcheck = 0,     // check_memory only (plan.cpp:351-380)
+  kModeE2E = 1,          // end_to_end_cost (cost_model.cpp:431-487), no balancing
+  kModeEvaluate = 2,     // EvalContext::evaluate (search.cpp:259-279) if memory-feasible
+  kModeBalanceData = 3,  // balance_data (balance.cpp:37-56) only
+  kModeBalanceLayers = 4,  // balance_layers (balance.cpp:81-167) only
+  kModeChain = 5,        // balance_data -> balance_layers -> e2e, no C3 gate
+};
+
+// Per-plan result slot.
+struct EvalResult {
+  double cost;       // end_to_end_s of the (balanced) plan, or -1 when not evaluated
+  double reshard_s;
+  double sync_s;
+  int32_t flags;     // bit0: input memory-feasible; bit1: output memory-feasible;
+                     // bit2: weights changed; bit3: stage layers changed
+  int32_t pad;
+};
+static_assert(sizeof(EvalResult) == 32, "result layout");
+
+constexpr int kResFeasIn = 1;
+constexpr int kResFeasOut = 2;
+constexpr int kResWeights = 4;
+constexpr int kResLayers = 8;
+
+// Per-batch shared-memory carve sizes of the evaluation kernel (the host
+// computes the batch maxima while packing).
+struct Carve {
+  int32_t n_dev;      // N
+  int32_t n_tasks;    // T
+  int32_t max_w;      // max over plans of sum dp
+  int32_t max_sl;     // max sum pp
+  int32_t max_slots;  // max sum dp*pp*tp
+  int32_t max_cells;  // max sum dp*pp
+  int32_t max_dpk;    // max sum pp*tp
+  int32_t bytes;      // total dynamic smem per CTA
+};
+
+HPG_HD int carve_round(int b) { return (b + 15) & ~15; }
+
+HPG_HD int carve_bytes(const Carve& c) {
+  const int N = c.n_dev, T = c.n_tasks;
+  int b = 0;
+  b += 2 * carve_round(8 * c.max_w) + 2 * carve_round(8 * c.max_cells) + carve_round(8 * c.max_dpk);
+  b += 7 * carve_round(8 * N) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
+       carve_round(8 * T * 7);
+  b += 2 * carve_round(4 * c.max_sl) + carve_round(4 * c.max_dpk) + 2 * carve_round(4 * N);
+  b += carve_round(c.max_slots) + carve_round(T * N) + 2 * carve_round(N);
+  return b;
+}
+
+HPG_HD int carve2_bytes(const Carve& c) {
+  return carve_bytes(c) + carve_round(8 * c.n_dev) + carve_round(4 * c.max_sl) +
+         2 * carve_round(4 * c.n_dev);
+}
+
+}  // namespace hpg

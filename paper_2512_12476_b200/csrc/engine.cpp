@@ -1,0 +1,498 @@
+// Problem staging, plan validation/packing and the batched device call.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <numeric>
+
+#include "eval_launch.hpp"
+
+namespace hpg {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw InternalError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+
+namespace {
+
+std::string str_or_empty(const char* s) { return s ? std::string(s) : std::string(); }
+
+int task_kind_of(int id) { return id == 1 ? kGeneration : (id <= 4 ? kInference : kTraining); }
+
+}  // namespace
+
+Problem build_problem(const hpg_problem& p) {
+  Problem P;
+  // ---- workflow (build_workflow, workflow.cpp:97-146; validators :16-33) ----
+  if (p.eta < 0.0 || p.eta > 1.0) throw InputError("eta must be within [0, 1]");
+  if (p.global_batch < 1 || p.responses_per_prompt < 1 || p.micro_batch_size < 1)
+    throw InputError("batch sizes must be >= 1");
+  if (p.seq_in < 1 || p.seq_out < 0) throw InputError("seq_in must be >= 1 and seq_out >= 0");
+  if (p.n_tasks < 1 || p.n_tasks > kMaxTasks || p.tasks == nullptr)
+    throw InputError("workflow must list 1..6 tasks");
+  P.algorithm = p.algorithm;
+  P.mode = p.mode;
+  P.eta = p.eta;
+  P.global_batch = p.global_batch;
+  P.rpp = p.responses_per_prompt;
+  P.seq_in = p.seq_in;
+  P.seq_out = p.seq_out;
+  P.mbs = p.micro_batch_size;
+  std::fill(std::begin(P.slot_of_id), std::end(P.slot_of_id), -1);
+  int prev = 0;
+  for (int t = 0; t < p.n_tasks; ++t) {
+    const hpg_task& in = p.tasks[t];
+    if (in.id < 1 || in.id > 6) throw InputError("unknown task id " + std::to_string(in.id));
+    if (in.id <= prev) throw InputError("workflow tasks must be ordered by id");
+    prev = in.id;
+    if (in.kind < 0 || in.kind > 2) throw InputError("unknown task kind");
+    if (in.hidden_size < 1 || in.intermediate_size < 1 || in.num_layers < 1)
+      throw InputError(
+          "model spec requires hidden_size, intermediate_size and num_layers >= 1");
+    if (in.include_embedding && in.vocab_size < 1)
+      throw InputError("include_embedding requires vocab_size >= 1");
+    HostTask h;
+    h.id = in.id;
+    h.kind = in.kind;
+    h.h1 = in.hidden_size;
+    h.h2 = in.intermediate_size;
+    h.nl = in.num_layers;
+    h.emb = in.include_embedding != 0;
+    h.vocab = in.vocab_size;
+    h.prec = in.precision_bytes;
+    h.layer_params = 4 * h.h1 * h.h1 + 3 * h.h1 * h.h2;
+    h.param_count = h.nl * h.layer_params + (h.emb ? 2 * h.vocab * h.h1 : 0);
+    P.slot_of_id[in.id] = t;
+    P.tasks.push_back(h);
+  }
+  (void)task_kind_of;
+  P.T = p.n_tasks;
+  for (int e = 0; e < p.n_dep_edges; ++e) {
+    P.dep_edges.emplace(p.dep_edges[2 * e], p.dep_edges[2 * e + 1]);
+  }
+
+  // ---- topology (DeviceTopology::make, topology.cpp:44-113) ----
+  if (p.n_devices < 1 || p.devices == nullptr)
+    throw InputError("topology must list at least one device");
+  if (p.n_devices > kMaxDevices)
+    throw InputError("engine limit: at most 256 devices per topology");
+  if (p.intra_region_latency_ms < 0 || p.intra_region_bandwidth_gbps <= 0)
+    throw InputError(
+        "intra-region defaults must be non-negative latency and positive bandwidth");
+  P.def_lat_ms = p.intra_region_latency_ms;
+  P.def_bw_gbps = p.intra_region_bandwidth_gbps;
+  const int N = p.n_devices;
+  P.N = N;
+  std::map<std::string, int> index;
+  std::map<std::string, int> node_sizes;
+  for (int i = 0; i < N; ++i) {
+    const hpg_device& d = p.devices[i];
+    const std::string id = str_or_empty(d.id);
+    if (id.empty()) throw InputError("device id must be non-empty");
+    if (d.comp_tflops <= 0 || d.mem_gb <= 0 || d.hbm_gbps <= 0 || d.intra_node_gbps <= 0)
+      throw InputError("device '" + id + "' has a non-positive attribute (comp/mem/hbm/intra)");
+    const std::string node = str_or_empty(d.node), region = str_or_empty(d.region);
+    if (node.empty() || region.empty())
+      throw InputError("device '" + id + "' needs node and region labels");
+    if (!index.emplace(id, i).second) throw InputError("duplicate device id '" + id + "'");
+    P.max_node_size = std::max(P.max_node_size, ++node_sizes[node]);
+    P.dev_id.push_back(id);
+    P.dev_node.push_back(node);
+    P.dev_region.push_back(region);
+    P.dev_model.push_back(str_or_empty(d.gpu_model));
+    P.comp_tflops.push_back(d.comp_tflops);
+    P.mem_gb.push_back(d.mem_gb);
+    P.hbm_gbps.push_back(d.hbm_gbps);
+    P.intra_gbps.push_back(d.intra_node_gbps);
+    P.comp.push_back(d.comp_tflops * 1e12);  // kTflops
+    P.mem.push_back(d.mem_gb * 1e9);         // kGigabyte
+    P.hbm.push_back(d.hbm_gbps * 1e9);
+  }
+  auto ordered = [](const std::string& a, const std::string& b) {
+    return a <= b ? std::make_pair(a, b) : std::make_pair(b, a);
+  };
+  std::map<std::pair<std::string, std::string>, std::pair<double, double>> region_matrix;
+  for (int e = 0; e < p.n_region_links; ++e) {
+    const hpg_region_link& rl = p.region_links[e];
+    const std::string src = str_or_empty(rl.src), dst = str_or_empty(rl.dst);
+    if (rl.latency_ms < 0 || rl.bandwidth_gbps <= 0)
+      throw InputError("region link " + src + "<->" + dst +
+                       " must have latency >= 0 and bandwidth > 0");
+    if (!region_matrix
+             .emplace(ordered(src, dst), std::make_pair(rl.latency_ms * 1e-3,
+                                                        rl.bandwidth_gbps * 1.25e8))
+             .second)
+      throw InputError("duplicate region link " + src + "<->" + dst);
+    P.rl_src.push_back(src);
+    P.rl_dst.push_back(dst);
+    P.rl_lat_ms.push_back(rl.latency_ms);
+    P.rl_bw_gbps.push_back(rl.bandwidth_gbps);
+  }
+  // link classes: distinct (latency, bandwidth) bit patterns; class 0 = self
+  std::map<std::pair<uint64_t, uint64_t>, int> cls_of;
+  auto class_id = [&](double lat, double bw) {
+    uint64_t a, b;
+    std::memcpy(&a, &lat, 8);
+    std::memcpy(&b, &bw, 8);
+    auto it = cls_of.find({a, b});
+    if (it != cls_of.end()) return it->second;
+    const int id = static_cast<int>(P.lat.size());
+    if (id >= kMaxClasses) throw InputError("engine limit: more than 64 distinct link classes");
+    cls_of.emplace(std::make_pair(a, b), id);
+    P.lat.push_back(lat);
+    P.bw.push_back(bw);
+    return id;
+  };
+  class_id(0.0, std::numeric_limits<double>::infinity());
+  P.cls.assign(static_cast<size_t>(N) * N, 0);
+  for (int a = 0; a < N; ++a) {
+    for (int b = 0; b < N; ++b) {
+      double lat, bw;
+      if (a == b) {
+        lat = 0.0;
+        bw = std::numeric_limits<double>::infinity();
+      } else if (P.dev_node[a] == P.dev_node[b] && P.dev_region[a] == P.dev_region[b]) {
+        lat = 5e-6;  // kIntraNodeLatencyS
+        bw = std::min(P.intra_gbps[a] * 1e9, P.intra_gbps[b] * 1e9);
+      } else if (P.dev_region[a] == P.dev_region[b]) {
+        lat = p.intra_region_latency_ms * 1e-3;
+        bw = p.intra_region_bandwidth_gbps * 1.25e8;
+      } else {
+        auto it = region_matrix.find(ordered(P.dev_region[a], P.dev_region[b]));
+        if (it == region_matrix.end())
+          throw InputError("no link rule between regions '" + P.dev_region[a] + "' and '" +
+                           P.dev_region[b] + "' (devices " + P.dev_id[a] + ", " + P.dev_id[b] +
+                           ")");
+        lat = it->second.first;
+        bw = it->second.second;
+      }
+      P.cls[static_cast<size_t>(a) * N + b] = static_cast<uint8_t>(class_id(lat, bw));
+    }
+  }
+  // lexicographic orders of the std::string keys the reference iterates
+  std::vector<int> order(N);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(),
+            [&](int x, int y) { return P.dev_id[x] < P.dev_id[y]; });
+  P.id_rank.assign(N, 0);
+  for (int r = 0; r < N; ++r) P.id_rank[order[r]] = r;
+  std::map<std::string, int> node_names;
+  for (int i = 0; i < N; ++i) node_names.emplace(P.dev_node[i], 0);
+  int r = 0;
+  for (auto& kv : node_names) kv.second = r++;
+  P.node_rank.assign(N, 0);
+  for (int i = 0; i < N; ++i) P.node_rank[i] = node_names[P.dev_node[i]];
+  std::map<std::string, std::map<std::string, std::vector<int>>> by_region;
+  for (int i = 0; i < N; ++i) by_region[P.dev_region[i]][P.dev_node[i]].push_back(i);
+  for (auto& [reg, nodes] : by_region) {
+    std::vector<std::vector<int>> v;
+    for (auto& [nd, devs] : nodes) v.push_back(devs);
+    P.region_nodes.push_back(std::move(v));
+  }
+  return P;
+}
+
+DevCostConfig to_dev_cfg(const hpg_cost_config& c) {
+  DevCostConfig d;
+  d.recompute = c.recompute;
+  d.dbs_cap = c.dbs_cap;
+  d.reshard_override = c.reshard_override;
+  d.sync_override = c.sync_override;
+  d.dbs_override = c.dbs_override;
+  d.train_bytes_per_param = c.train_bytes_per_param;
+  d.infer_bytes_per_param = c.infer_bytes_per_param;
+  d.kv_bytes_per_elem = c.kv_bytes_per_elem;
+  d.act_factor = c.act_factor;
+  return d;
+}
+
+hpg_cost_config default_cost_config() {
+  hpg_cost_config c;
+  c.recompute = 1;
+  c.reshard_override = -1.0;
+  c.sync_override = -1.0;
+  c.dbs_override = -1.0;
+  c.train_bytes_per_param = 18.0;
+  c.infer_bytes_per_param = 2.0;
+  c.kv_bytes_per_elem = 2.0;
+  c.dbs_cap = 1;
+  c.act_factor = 4.0;
+  return c;
+}
+
+void init_cand(Cand& c, int T, const int* dp, const int* pp, const int* tp, const Problem& P) {
+  RecHeader h{};
+  h.n_tasks = T;
+  for (int t = 0; t < T; ++t) {
+    h.dp[t] = dp[t];
+    h.pp[t] = pp[t];
+    h.tp[t] = tp[t];
+  }
+  rec_offsets(h, c.o);
+  h.bytes = c.o.bytes;
+  c.rec.assign(c.o.bytes, 0);
+  std::memcpy(c.rec.data(), &h, sizeof(h));
+  double* w = c.w();
+  for (int i = 0; i < c.o.w[T]; ++i) w[i] = 1.0;
+  int32_t* sl = c.sl();
+  for (int t = 0; t < T; ++t) {
+    const int64_t nl = P.tasks[t].nl;
+    for (int j = 0; j < pp[t]; ++j) {
+      sl[c.o.sl[t] + j] = static_cast<int32_t>(nl / pp[t]) + (j < nl % pp[t] ? 1 : 0);
+    }
+  }
+}
+
+Ctx::~Ctx() {
+  if (d_blob) cudaFree(d_blob);
+  if (d_sweep_tables) cudaFree(d_sweep_tables);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+Ctx* create_ctx(const hpg_problem& hp, int device) {
+  Problem P = build_problem(hp);
+  int n_dev = 0;
+  cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount (no CUDA device: the engine has "
+                                         "no CPU fallback)");
+  if (device < 0 || device >= n_dev) throw InternalError("CUDA device index out of range");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major < 10) {
+    throw InternalError(std::string("engine is built for sm_100a; device is ") + prop.name);
+  }
+  auto* ctx = new Ctx();
+  try {
+    ctx->prob = std::move(P);
+    ctx->device = device;
+    ctx->n_sm = prop.multiProcessorCount;
+    cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    const Problem& Q = ctx->prob;
+    const int N = Q.N, C = static_cast<int>(Q.lat.size());
+    const size_t bytes = 8 * (3 * N + 2 * C) + static_cast<size_t>(N) * N;
+    std::vector<uint8_t> blob(bytes);
+    double* dd = reinterpret_cast<double*>(blob.data());
+    std::memcpy(dd, Q.comp.data(), 8 * N);
+    std::memcpy(dd + N, Q.mem.data(), 8 * N);
+    std::memcpy(dd + 2 * N, Q.hbm.data(), 8 * N);
+    std::memcpy(dd + 3 * N, Q.lat.data(), 8 * C);
+    std::memcpy(dd + 3 * N + C, Q.bw.data(), 8 * C);
+    std::memcpy(blob.data() + 8 * (3 * N + 2 * C), Q.cls.data(), static_cast<size_t>(N) * N);
+    cuda_check(cudaMalloc(&ctx->d_blob, bytes), "cudaMalloc problem");
+    cuda_check(cudaMemcpy(ctx->d_blob, blob.data(), bytes, cudaMemcpyHostToDevice), "H2D problem");
+    DevProblem& D = ctx->dprob;
+    const double* db = reinterpret_cast<const double*>(ctx->d_blob);
+    D.n_dev = N;
+    D.n_tasks = Q.T;
+    D.n_classes = C;
+    D.mode = Q.mode;
+    D.algorithm = Q.algorithm;
+    D.gen_slot = Q.slot_of_id[1];
+    D.train6_slot = Q.slot_of_id[6];
+    D.max_tp = Q.max_node_size;
+    D.eta = Q.eta;
+    D.global_batch = Q.global_batch;
+    D.rpp = Q.rpp;
+    D.seq_in = Q.seq_in;
+    D.seq_out = Q.seq_out;
+    D.mbs = Q.mbs;
+    D.total_seq = Q.global_batch * Q.rpp;
+    for (int t = 0; t < Q.T; ++t) {
+      const HostTask& h = Q.tasks[t];
+      DevTask& d = D.task[t];
+      d.id = h.id;
+      d.kind = h.kind;
+      d.precision_bytes = h.prec;
+      d.include_embedding = h.emb ? 1 : 0;
+      d.h1 = h.h1;
+      d.h2 = h.h2;
+      d.nl = h.nl;
+      d.vocab = h.vocab;
+      d.layer_params = h.layer_params;
+      d.param_count = h.param_count;
+    }
+    D.comp = db;
+    D.mem = db + N;
+    D.hbm = db + 2 * N;
+    D.lat = db + 3 * N;
+    D.bw = db + 3 * N + C;
+    D.cls = reinterpret_cast<const uint8_t*>(ctx->d_blob) + 8 * (3 * N + 2 * C);
+  } catch (...) {
+    delete ctx;
+    throw;
+  }
+  return ctx;
+}
+
+void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags, bool want_out,
+               bool want_per_task, bool want_required, BatchOut& out) {
+  const int n = static_cast<int>(b.cands.size());
+  out.res.resize(n);
+  out.off.resize(n);
+  if (n == 0) return;
+  const Problem& P = ctx.prob;
+  Carve cv{};
+  cv.n_dev = P.N;
+  cv.n_tasks = P.T;
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) {
+    const Cand& c = *b.cands[i];
+    out.off[i] = total;
+    total += c.o.bytes;
+    const int T = P.T;
+    cv.max_w = std::max(cv.max_w, c.o.w[T]);
+    cv.max_sl = std::max(cv.max_sl, c.o.sl[T]);
+    cv.max_slots = std::max(cv.max_slots, c.o.dev[T]);
+    cv.max_cells = std::max(cv.max_cells, c.o.cell[T]);
+    cv.max_dpk = std::max(cv.max_dpk, c.o.dpk[T]);
+  }
+  ctx.h_recs.reserve(total);
+  ctx.h_off.reserve(n);
+  ctx.h_modes.reserve(n);
+  ctx.h_res.reserve(n);
+  for (int i = 0; i < n; ++i) {
+    std::memcpy(ctx.h_recs.p + out.off[i], b.cands[i]->rec.data(), b.cands[i]->o.bytes);
+    ctx.h_off.p[i] = out.off[i];
+    ctx.h_modes.p[i] = b.modes[i];
+  }
+  ctx.d_recs.reserve(total);
+  ctx.d_off.reserve(n);
+  ctx.d_modes.reserve(n);
+  ctx.d_res.reserve(n);
+  if (want_out) ctx.d_out.reserve(total);
+  if (want_per_task) ctx.d_per_task.reserve(static_cast<size_t>(n) * P.T * 7);
+  if (want_required) ctx.d_required.reserve(static_cast<size_t>(n) * P.N);
+  cudaStream_t st = ctx.stream;
+  cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, total, cudaMemcpyHostToDevice, st), "H2D recs");
+  cuda_check(cudaMemcpyAsync(ctx.d_off.p, ctx.h_off.p, 8 * n, cudaMemcpyHostToDevice, st), "H2D off");
+  cuda_check(cudaMemcpyAsync(ctx.d_modes.p, ctx.h_modes.p, 4 * n, cudaMemcpyHostToDevice, st), "H2D modes");
+  cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, ctx.d_recs.p, ctx.d_off.p, ctx.d_modes.p, 0,
+                         n, 0, want_out ? ctx.d_out.p : nullptr, ctx.d_res.p,
+                         want_per_task ? ctx.d_per_task.p : nullptr,
+                         want_required ? ctx.d_required.p : nullptr, ctx.n_sm, st),
+             "eval_kernel launch");
+  ++ctx.launches;
+  ctx.plans_evaluated += n;
+  cuda_check(cudaMemcpyAsync(ctx.h_res.p, ctx.d_res.p, sizeof(EvalResult) * n,
+                             cudaMemcpyDeviceToHost, st), "D2H results");
+  if (want_out) {
+    ctx.h_out.reserve(total);
+    cuda_check(cudaMemcpyAsync(ctx.h_out.p, ctx.d_out.p, total, cudaMemcpyDeviceToHost, st), "D2H recs");
+    out.out_recs = &ctx.h_out;
+  }
+  if (want_per_task) out.per_task.resize(static_cast<size_t>(n) * P.T * 7);
+  if (want_required) out.required.resize(static_cast<size_t>(n) * P.N);
+  if (want_per_task)
+    cuda_check(cudaMemcpyAsync(out.per_task.data(), ctx.d_per_task.p, 8 * out.per_task.size(),
+                               cudaMemcpyDeviceToHost, st), "D2H per-task");
+  if (want_required)
+    cuda_check(cudaMemcpyAsync(out.required.data(), ctx.d_required.p, 8 * out.required.size(),
+                               cudaMemcpyDeviceToHost, st), "D2H required");
+  cuda_check(cudaStreamSynchronize(st), "eval_kernel");
+  std::memcpy(out.res.data(), ctx.h_res.p, sizeof(EvalResult) * n);
+}
+
+std::vector<TablePlan> unpack_table(const Problem& P, const hpg_plan_table& t) {
+  std::vector<TablePlan> out;
+  if (t.n_plans < 0) throw UsageError("negative plan count");
+  const int T = P.T, N = P.N;
+  out.resize(t.n_plans);
+  for (int p = 0; p < t.n_plans; ++p) {
+    TablePlan& tp = out[p];
+    const int ng = t.n_groups[p];
+    if (ng < 1) throw InputError("task grouping must contain at least one group");
+    if (ng > T) throw InputError("task groups must be non-empty");
+    tp.groups.assign(ng, {});
+    for (int s = 0; s < T; ++s) {
+      const int g = t.task_group[static_cast<int64_t>(p) * T + s];
+      if (g < 0 || g >= ng) throw InputError("task grouping must cover every workflow task");
+      tp.groups[g].push_back(s);
+    }
+    for (const auto& g : tp.groups)
+      if (g.empty()) throw InputError("task groups must be non-empty");
+    int64_t count_sum = 0;
+    for (int g = 0; g < ng; ++g) {
+      const int c = t.gpu_counts[static_cast<int64_t>(p) * T + g];
+      if (c < 1) throw InputError("gpu_counts entries must be >= 1");
+      tp.counts.push_back(c);
+      count_sum += c;
+    }
+    if (count_sum != N)
+      throw InputError("gpu_counts must sum to the device count (" + std::to_string(N) + ")");
+    int dp[kMaxTasks], pp[kMaxTasks], tpp[kMaxTasks];
+    for (int s = 0; s < T; ++s) {
+      dp[s] = t.dp[static_cast<int64_t>(p) * T + s];
+      pp[s] = t.pp[static_cast<int64_t>(p) * T + s];
+      tpp[s] = t.tp[static_cast<int64_t>(p) * T + s];
+      if (dp[s] < 1 || pp[s] < 1 || tpp[s] < 1) throw InputError("dp, pp and tp must be >= 1");
+    }
+    init_cand(tp.cand, T, dp, pp, tpp, P);
+    Cand& c = tp.cand;
+    std::vector<std::vector<int>> group_sets(ng);
+    std::vector<bool> group_set_init(ng, false);
+    for (int g = 0; g < ng; ++g) {
+      for (int s : tp.groups[g]) {
+        const HostTask& task = P.tasks[s];
+        const std::string tid = std::to_string(task.id);
+        // ParallelLayout::validate (plan.cpp:54-87)
+        if (pp[s] > task.nl) throw InputError("pp exceeds layer count");
+        const int64_t so = t.sl_off[static_cast<int64_t>(p) * T + s];
+        int64_t total = 0;
+        for (int j = 0; j < pp[s]; ++j) {
+          const int v = t.stage_layers[so + j];
+          if (v < 1) throw InputError("every pipeline stage needs at least one layer");
+          total += v;
+          c.sl()[c.o.sl[s] + j] = v;
+        }
+        if (total != task.nl) throw InputError("stage_layers must sum to the model layer count");
+        const int64_t wo = t.w_off[static_cast<int64_t>(p) * T + s];
+        double wsum = 0;
+        for (int i = 0; i < dp[s]; ++i) {
+          const double w = t.weights[wo + i];
+          if (!(w > 0)) throw InputError("replica batch weights must be positive");
+          wsum += w;
+          c.w()[c.o.w[s] + i] = w;
+        }
+        if (std::abs(wsum - dp[s]) > 1e-6 * dp[s])
+          throw InputError("replica batch weights must sum to dp");
+        const int size = dp[s] * pp[s] * tpp[s];
+        if (size != tp.counts[g])
+          throw InputError("task " + tid + ": dp*pp*tp must equal its group's GPU count");
+        const int64_t dof = t.dev_off[static_cast<int64_t>(p) * T + s];
+        std::vector<int> used;
+        for (int e = 0; e < size; ++e) {
+          const int d = t.devices[dof + e];
+          if (d < 0 || d >= N) throw InputError("unknown device index " + std::to_string(d));
+          if (std::find(used.begin(), used.end(), d) != used.end())
+            throw InputError("task " + tid + ": device '" + P.dev_id[d] +
+                             "' hosts more than one tasklet");
+          used.push_back(d);
+          c.dev()[c.o.dev[s] + e] = static_cast<uint8_t>(d);
+        }
+        std::sort(used.begin(), used.end());
+        if (!group_set_init[g]) {
+          group_sets[g] = used;
+          group_set_init[g] = true;
+        } else if (group_sets[g] != used) {
+          throw InputError("co-located tasks in group " + std::to_string(g) +
+                           " must share the same device set");
+        }
+      }
+    }
+    std::vector<int> seen(N, 0);
+    for (int g = 0; g < ng; ++g) {
+      for (int d : group_sets[g]) {
+        if (seen[d]++) throw InputError("device '" + P.dev_id[d] + "' appears in more than one GPU group");
+      }
+    }
+  }
+  return out;
+}
+
+}  // namespace hpg

@@ -1,0 +1,191 @@
+// Host side of the engine: problem staging, device buffers, plan records and
+// the batched evaluation call used by the C ABI and by the search driver.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/hpg.h"
+#include "common.hpp"
+#include "rng.hpp"
+
+namespace hpg {
+
+// Status-carrying errors, mapped to HPG_* codes at the C boundary
+// (InputError / UsageError of proj/include/hetplan/errors.hpp:11-18).
+struct InputError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct UsageError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InternalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct HostTask {
+  int id = 0;
+  int kind = 0;
+  int64_t h1 = 0, h2 = 0, nl = 0, vocab = 0;
+  bool emb = false;
+  int prec = 2;
+  int64_t layer_params = 0, param_count = 0;
+};
+
+// Workflow + topology, flattened to integers (SURVEY.md §7 step 1 "problem
+// flattener"): devices as indices, link classes, lexicographic orders of the
+// id/node/region strings that drive the reference's std::map iteration.
+struct Problem {
+  int N = 0, T = 0;
+  int algorithm = 0, mode = 0;
+  double eta = 0.5;
+  int64_t global_batch = 1, rpp = 1, seq_in = 1, seq_out = 0, mbs = 1;
+  std::vector<HostTask> tasks;  // workflow order = task-id order
+  int slot_of_id[8];            // task id -> slot, -1 absent
+  std::set<std::pair<int, int>> dep_edges;
+  // devices
+  std::vector<std::string> dev_id, dev_node, dev_region, dev_model;
+  std::vector<double> comp_tflops, mem_gb, hbm_gbps, intra_gbps;
+  std::vector<double> comp, mem, hbm;  // SI
+  int max_node_size = 0;
+  // links
+  std::vector<uint8_t> cls;  // N*N
+  std::vector<double> lat, bw;
+  // orders
+  std::vector<int> id_rank;    // lexicographic rank of the device id
+  std::vector<int> node_rank;  // lexicographic rank of the node name (global)
+  // random_medium_assignment locality structure (search.cpp:163-186):
+  // regions (lex) -> nodes (lex) -> devices (index order)
+  std::vector<std::vector<std::vector<int>>> region_nodes;
+  std::vector<int> region_node_count;
+  // region links as given (for error messages and re-serialisation)
+  std::vector<std::string> rl_src, rl_dst;
+  std::vector<double> rl_lat_ms, rl_bw_gbps;
+  double def_lat_ms = 0.1, def_bw_gbps = 100.0;
+};
+
+Problem build_problem(const hpg_problem& p);
+
+DevCostConfig to_dev_cfg(const hpg_cost_config& c);
+hpg_cost_config default_cost_config();
+
+// One candidate in record form (common.hpp PlanRec) plus its host metadata.
+struct Cand {
+  std::vector<uint8_t> rec;
+  RecOffsets o;
+  int tg = -1;  // arm task grouping (search only)
+  RecHeader& hdr() { return *reinterpret_cast<RecHeader*>(rec.data()); }
+  const RecHeader& hdr() const { return *reinterpret_cast<const RecHeader*>(rec.data()); }
+  double* w() { return reinterpret_cast<double*>(rec.data() + o.w_byte); }
+  int32_t* sl() { return reinterpret_cast<int32_t*>(rec.data() + o.sl_byte); }
+  uint8_t* dev() { return rec.data() + o.dev_byte; }
+  const double* w() const { return reinterpret_cast<const double*>(rec.data() + o.w_byte); }
+  const int32_t* sl() const { return reinterpret_cast<const int32_t*>(rec.data() + o.sl_byte); }
+  const uint8_t* dev() const { return rec.data() + o.dev_byte; }
+  int size(int t) const { return o.dev[t + 1] - o.dev[t]; }
+};
+
+// Allocates a record for the given layouts; weights 1.0, uniform stage split
+// (make_layout, plan.cpp:89-100), devices zeroed.
+void init_cand(Cand& c, int T, const int* dp, const int* pp, const int* tp, const Problem& P);
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void reserve(size_t n) {
+    if (n <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    const size_t c = n > cap * 2 ? n : cap * 2;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), c * sizeof(T)), "cudaMalloc");
+    cap = c;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+template <typename T>
+struct HostBuf {  // pinned
+  T* p = nullptr;
+  size_t cap = 0;
+  void reserve(size_t n) {
+    if (n <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    const size_t c = n > cap * 2 ? n : cap * 2;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), c * sizeof(T), cudaHostAllocDefault),
+               "cudaHostAlloc");
+    cap = c;
+  }
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+struct Batch {
+  std::vector<const Cand*> cands;
+  std::vector<int32_t> modes;
+};
+
+struct BatchOut {
+  std::vector<EvalResult> res;
+  HostBuf<uint8_t>* out_recs = nullptr;  // same offsets as packed input
+  std::vector<int64_t> off;
+  std::vector<double> per_task;          // if requested
+  std::vector<double> required;          // if requested
+};
+
+struct Ctx {
+  Problem prob;
+  int device = 0;
+  int n_sm = 0;
+  cudaStream_t stream = nullptr;
+  DevProblem dprob{};
+  void* d_blob = nullptr;
+  // batch staging
+  HostBuf<uint8_t> h_recs, h_out;
+  HostBuf<int64_t> h_off;
+  HostBuf<int32_t> h_modes;
+  HostBuf<EvalResult> h_res;
+  DevBuf<uint8_t> d_recs, d_out;
+  DevBuf<int64_t> d_off;
+  DevBuf<int32_t> d_modes;
+  DevBuf<EvalResult> d_res;
+  DevBuf<double> d_per_task, d_required;
+  // sweep
+  void* d_sweep_tables = nullptr;
+  DevBuf<double> d_costs;
+  DevBuf<uint8_t> d_feas;
+  DevBuf<unsigned long long> d_best;
+  // best-half
+  DevBuf<double> d_scores, d_events;
+  DevBuf<int32_t> d_seg_off, d_arm_idx, d_keep;
+  int64_t launches = 0;
+  int64_t plans_evaluated = 0;
+  ~Ctx();
+};
+
+Ctx* create_ctx(const hpg_problem& p, int device);
+
+// Packs `b`, runs eval_kernel, returns per-plan results (and balanced records).
+void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
+               bool want_out, bool want_per_task, bool want_required, BatchOut& out);
+
+// Plan-table validation + packing (resolve_plan semantics, plan.cpp:257-349).
+struct TablePlan {
+  std::vector<std::vector<int>> groups;  // task slots per group
+  std::vector<int> counts;
+  Cand cand;
+};
+std::vector<TablePlan> unpack_table(const Problem& P, const hpg_plan_table& t);
+
+}  // namespace hpg

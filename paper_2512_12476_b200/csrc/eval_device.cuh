@@ -1,0 +1,889 @@
+// Device side of the per-plan cost model: one warp evaluates one plan.
+//
+// Every formula restates the reference expression by expression, in the same
+// association order, compiled with -fmad=false, so
+// results are bit-identical to proj/src/cost_model.cpp and proj/src/plan.cpp.
+// Only max/min folds are tree-reduced across lanes; every sum keeps the
+// reference's sequential order.
+//
+// Geometry memo: inside one plan evaluation the tasklet->device assignment
+// never changes (balancing only moves replica weights and stage splits), so
+// TP rings, PP pairs and the gen->train bridge are computed once per plan and
+// DP rings once per (stage, shard, stage-layer count). Same doubles as
+// recomputing them, far fewer gathers.
+#pragma once
+
+#include <cstdint>
+
+#include "common.hpp"
+
+namespace hpg {
+namespace dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// std::max / std::min semantics (NaN behaviour of the reference included)
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = smax(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = smin(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+struct Ws {
+  // plan
+  RecHeader h;
+  RecOffsets o;
+  double* w;
+  int64_t* nm;
+  int32_t* sl;
+  uint8_t* dev;
+  uint8_t* dstage;   // [T*N] stage of device d inside task t, 0xff = none
+  // memo
+  double* rtp;       // [cells] TP ring bottleneck per (task, replica, stage)
+  double* ppp;       // [cells] cheapest cross-stage pair per (task, replica, stage)
+  double* dpr;       // [dpk]   DP ring per (task, stage, shard)
+  int32_t* dpr_sl;   // [dpk]   stage layers the DP memo was computed for
+  // scratch
+  double* resident;  // [N]
+  double* c_comp;    // [N] per cell of the task in flight
+  double* c_tp;
+  double* c_pp;
+  double* c_hbm;
+  double* edge;      // [N]
+  double* wnew;      // [N]
+  double* cc;        // [kMaxClasses] class costs at the volume in flight
+  double* rm;        // [64] small-ring cost matrix
+  double* agg;       // [T*7]
+  int32_t* sl_save;  // [sum pp]
+  int32_t* split_best;   // [N]
+  int32_t* split_trial;  // [N]
+  uint8_t* tour;     // [N]
+  uint8_t* peers;    // [N]
+  int64_t nm_base[kMaxTasks];
+  int32_t memo_tp_ok;   // bit t
+  int32_t memo_pp_ok;
+  double bridge;
+  int32_t bridge_ok;
+};
+
+__device__ __forceinline__ uint8_t* carve_ptr(uint8_t*& p, int bytes) {
+  uint8_t* r = p;
+  p += (bytes + 15) & ~15;
+  return r;
+}
+
+__device__ inline void carve(Ws& s, uint8_t* base, const Carve& c) {
+  uint8_t* p = base;
+  const int N = c.n_dev, T = c.n_tasks;
+  s.w = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_w));
+  s.nm = reinterpret_cast<int64_t*>(carve_ptr(p, 8 * c.max_w));
+  s.rtp = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_cells));
+  s.ppp = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_cells));
+  s.dpr = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_dpk));
+  s.resident = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.c_comp = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.c_tp = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.c_pp = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.c_hbm = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.edge = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.wnew = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.cc = reinterpret_cast<double*>(carve_ptr(p, 8 * kMaxClasses));
+  s.rm = reinterpret_cast<double*>(carve_ptr(p, 8 * 64));
+  s.agg = reinterpret_cast<double*>(carve_ptr(p, 8 * T * 7));
+  s.sl = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
+  s.sl_save = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
+  s.dpr_sl = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_dpk));
+  s.split_best = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
+  s.split_trial = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
+  s.dev = carve_ptr(p, c.max_slots);
+  s.dstage = carve_ptr(p, T * N);
+  s.tour = carve_ptr(p, N);
+  s.peers = carve_ptr(p, N);
+}
+
+// ---- memory model (plan.cpp:160-220) ----
+
+__device__ __forceinline__ double params_on_device(const DevTask& t, int sl_j, int tp,
+                                                   int stage, int pp) {
+  double p = static_cast<double>(sl_j) * static_cast<double>(t.layer_params) / tp;
+  if (t.include_embedding) {
+    const double emb = static_cast<double>(t.vocab) * static_cast<double>(t.h1) / tp;
+    if (stage == 0) p += emb;
+    if (stage == pp - 1) p += emb;
+  }
+  return p;
+}
+
+__device__ __forceinline__ double kv_bytes_per_sequence(const DevProblem& P, const DevTask& t,
+                                                        int sl_j, int tp,
+                                                        const DevCostConfig& cfg) {
+  return static_cast<double>(P.seq_in + P.seq_out) * 2.0 * static_cast<double>(t.h1) *
+         static_cast<double>(sl_j) * cfg.kv_bytes_per_elem / tp;
+}
+
+__device__ __forceinline__ double model_memory_bytes(const DevProblem& P, const DevTask& t,
+                                                     int sl_j, int tp, int stage, int pp,
+                                                     const DevCostConfig& cfg) {
+  const double params = params_on_device(t, sl_j, tp, stage, pp);
+  if (t.kind == kTraining) return params * cfg.train_bytes_per_param;
+  if (t.kind == kInference) return params * cfg.infer_bytes_per_param;
+  return params * cfg.infer_bytes_per_param +
+         static_cast<double>(P.mbs) * cfg.dbs_cap * kv_bytes_per_sequence(P, t, sl_j, tp, cfg);
+}
+
+__device__ __forceinline__ double weights_memory_bytes(const DevTask& t, int sl_j, int tp,
+                                                       int stage, int pp,
+                                                       const DevCostConfig& cfg) {
+  const double params = params_on_device(t, sl_j, tp, stage, pp);
+  return t.kind == kTraining ? params * cfg.train_bytes_per_param
+                             : params * cfg.infer_bytes_per_param;
+}
+
+__device__ __forceinline__ double working_memory_bytes(const DevProblem& P, const DevTask& t,
+                                                       int sl_j, int tp,
+                                                       const DevCostConfig& cfg) {
+  return static_cast<double>(P.mbs) * static_cast<double>(P.seq_in + P.seq_out) *
+         static_cast<double>(t.h1) * static_cast<double>(sl_j) * 2.0 * cfg.act_factor / tp;
+}
+
+// ---- formula helpers (cost_model.cpp:129-177, 220-241) ----
+
+__device__ __forceinline__ double tp_comm_volume(int prec, int64_t mbs, int64_t seq_total,
+                                                 int64_t h1, int tp) {
+  return static_cast<double>(prec) * static_cast<double>(mbs) *
+         static_cast<double>(seq_total) * static_cast<double>(h1) * (2.0 * (tp - 1) / tp);
+}
+__device__ __forceinline__ double pp_comm_volume(int prec, int64_t mbs, int64_t seq_total,
+                                                 int64_t h1) {
+  return static_cast<double>(prec) * static_cast<double>(mbs) *
+         static_cast<double>(seq_total) * static_cast<double>(h1);
+}
+__device__ __forceinline__ double dp_comm_volume(int prec, int64_t nl_j, int64_t h1, int64_t h2,
+                                                 int dp, int tp) {
+  return static_cast<double>(prec) * static_cast<double>(nl_j) *
+         (4.0 * static_cast<double>(h1) * static_cast<double>(h1) +
+          3.0 * static_cast<double>(h1) * static_cast<double>(h2)) *
+         (2.0 * (dp - 1) / (static_cast<double>(dp) * tp));
+}
+__device__ __forceinline__ double layer_flops(int64_t s, int64_t h1, int64_t h2) {
+  const double sd = static_cast<double>(s);
+  const double h1d = static_cast<double>(h1);
+  const double h2d = static_cast<double>(h2);
+  return 2.0 * 4.0 * sd * h1d * h1d + 2.0 * 2.0 * sd * sd * h1d + 2.0 * 3.0 * sd * h1d * h2d;
+}
+__device__ __forceinline__ double tp_pass_factor(int kind, bool recompute) {
+  if (kind != kTraining) return 2.0;
+  return recompute ? 6.0 : 4.0;
+}
+__device__ __forceinline__ double pp_pass_factor(int kind) { return kind == kTraining ? 2.0 : 1.0; }
+__device__ __forceinline__ double comp_pass_factor(int kind) {
+  return kind == kTraining ? 3.0 : 1.0;
+}
+__device__ __forceinline__ int64_t comp_seq(const DevProblem& P, int kind) {
+  return kind == kGeneration ? P.seq_in : P.seq_in + P.seq_out;
+}
+__device__ __forceinline__ double compute_cost(int kind, int64_t nm, int64_t mbs, int64_t nl_j,
+                                               double flops, double comp_d, int tp) {
+  return comp_pass_factor(kind) * static_cast<double>(nm) * static_cast<double>(mbs) *
+         static_cast<double>(nl_j) * flops / (comp_d * tp);
+}
+__device__ __forceinline__ double hbm_decode_cost(int64_t seq_out, int64_t nm, int64_t mbs,
+                                                  int prec, int64_t nl_j, int64_t h1,
+                                                  int64_t h2, double dbs, double hbm_d, int tp) {
+  const double weight_bytes =
+      static_cast<double>(prec) * static_cast<double>(nl_j) *
+      (4.0 * static_cast<double>(h1) * static_cast<double>(h1) +
+       3.0 * static_cast<double>(h1) * static_cast<double>(h2));
+  return static_cast<double>(seq_out) * static_cast<double>(nm) * static_cast<double>(mbs) *
+         weight_bytes / (dbs * hbm_d * tp);
+}
+
+// ---- plan staging ----
+
+__device__ __forceinline__ int flat(int i, int j, int k, int pp, int tp) {
+  return (i * pp + j) * tp + k;
+}
+
+// nm_base (workflow.cpp:148-157) and apportion_microbatches (plan.cpp:222-255)
+__device__ __noinline__ void apportion(const DevProblem& P, Ws& s, int t) {
+  const int lane = threadIdx.x & 31;
+  const int dp = s.h.dp[t];
+  const int64_t denom = static_cast<int64_t>(dp) * P.mbs;
+  const int64_t nm_base = (P.total_seq + denom - 1) / denom;
+  const double* w = s.w + s.o.w[t];
+  int64_t* out = s.nm + s.o.w[t];
+  if (lane == 0) s.nm_base[t] = nm_base;
+  const int64_t total = nm_base * dp;
+  double wsum = 0.0;  // std::accumulate, sequential (all lanes redundantly)
+  for (int i = 0; i < dp; ++i) wsum += w[i];
+  // floor of quotas + remainders
+  int64_t assigned_part = 0;
+  for (int i = lane; i < dp; i += 32) {
+    const double quota = static_cast<double>(total) * w[i] / wsum;
+    const int64_t f = static_cast<int64_t>(floor(quota));
+    out[i] = f;
+    assigned_part += f;
+  }
+  for (int o = 16; o > 0; o >>= 1) assigned_part += __shfl_xor_sync(kFull, assigned_part, o);
+  const int64_t deficit = total - assigned_part;
+  __syncwarp();
+  if (deficit > 0) {
+    // rank of replica i in (remainder desc, index asc); deficit hands out one
+    // micro-batch per rank position, cycling (plan.cpp:236-244)
+    for (int i = lane; i < dp; i += 32) {
+      const double qi = static_cast<double>(total) * w[i] / wsum;
+      const double ri = qi - static_cast<double>(out[i]);
+      int rank = 0;
+      for (int k = 0; k < dp; ++k) {
+        const double qk = static_cast<double>(total) * w[k] / wsum;
+        const double rk = qk - floor(qk);
+        if (rk > ri || (!(ri > rk) && rk == ri && k < i) ) ++rank;
+      }
+      const int64_t extra = deficit / dp + (rank < deficit % dp ? 1 : 0);
+      out[i] += extra;
+    }
+    __syncwarp();
+  }
+  // every replica processes at least one micro-batch (plan.cpp:246-253)
+  bool any_zero = false;
+  for (int i = lane; i < dp; i += 32) any_zero |= out[i] == 0;
+  if (__any_sync(kFull, any_zero)) {
+    if (lane == 0) {
+      for (int i = 0; i < dp; ++i) {
+        while (out[i] == 0) {
+          int donor = 0;
+          for (int k = 1; k < dp; ++k)
+            if (out[donor] < out[k]) donor = k;  // std::max_element: first max
+          --out[donor];
+          ++out[i];
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__device__ inline void build_dstage(const DevProblem& P, Ws& s) {
+  const int lane = threadIdx.x & 31;
+  const int N = P.n_dev;
+  for (int e = lane; e < P.n_tasks * N; e += 32) s.dstage[e] = 0xff;
+  __syncwarp();
+  for (int t = 0; t < P.n_tasks; ++t) {
+    const int pp = s.h.pp[t], tp = s.h.tp[t], size = s.h.dp[t] * pp * tp;
+    const uint8_t* dv = s.dev + s.o.dev[t];
+    for (int e = lane; e < size; e += 32) s.dstage[t * N + dv[e]] = static_cast<uint8_t>((e / tp) % pp);
+  }
+  __syncwarp();
+}
+
+// check_memory (plan.cpp:351-380): sum of model memory in task order plus the
+// max working set, per device. Returns true when every device fits.
+__device__ __noinline__ bool check_memory(const DevProblem& P, const DevCostConfig& cfg, Ws& s,
+                                    double* required_out = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const int N = P.n_dev;
+  bool viol = false;
+  for (int d = lane; d < N; d += 32) {
+    double ms = 0.0, wm = 0.0;
+    for (int t = 0; t < P.n_tasks; ++t) {
+      const int j = s.dstage[t * N + d];
+      if (j == 0xff) continue;
+      const DevTask& tk = P.task[t];
+      const int sl_j = s.sl[s.o.sl[t] + j];
+      ms += model_memory_bytes(P, tk, sl_j, s.h.tp[t], j, s.h.pp[t], cfg);
+      wm = smax(wm, working_memory_bytes(P, tk, sl_j, s.h.tp[t], cfg));
+    }
+    const double req = ms + wm;
+    if (required_out) required_out[d] = req;
+    if (req > P.mem[d]) viol = true;
+  }
+  return !__any_sync(kFull, viol);
+}
+
+// ---- communication primitives (cost_model.cpp:18-125, 179-218) ----
+
+__device__ __forceinline__ void class_costs(const DevProblem& P, Ws& s, double volume) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  for (int c = lane; c < P.n_classes; c += 32) s.cc[c] = P.lat[c] + volume / P.bw[c];
+  __syncwarp();
+}
+
+__device__ __forceinline__ double ecost(const DevProblem& P, const Ws& s, int a, int b) {
+  return s.cc[__ldg(&P.cls[a * P.n_dev + b])];
+}
+
+// Exact min-bottleneck Hamiltonian cycle, 3 <= n <= 8 (the reference's
+// RingSearch::dfs regime, cost_model.cpp:94-125, 196-206). The answer is a min
+// of maxes of the same doubles, so any exact method returns identical bits:
+// bounds first (LB = max over vertices of the 2nd-cheapest incident edge,
+// UB = identity tour), then a lane-parallel DFS over 2-vertex prefixes.
+__device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint8_t* devs, int n) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  for (int e = lane; e < n * n; e += 32) s.rm[e] = ecost(P, s, devs[e / n], devs[e % n]);
+  __syncwarp();
+  const double* rm = s.rm;
+  double ub = 0.0;
+  for (int i = 0; i < n; ++i) ub = smax(ub, rm[i * n + (i + 1) % n]);
+  double lb = 0.0;
+  for (int v = 0; v < n; ++v) {
+    double m1 = kInf, m2 = kInf;
+    for (int u = 0; u < n; ++u) {
+      if (u == v) continue;
+      const double c = rm[v * n + u];
+      if (c < m1) {
+        m2 = m1;
+        m1 = c;
+      } else if (c < m2) {
+        m2 = c;
+      }
+    }
+    lb = smax(lb, m2);
+  }
+  if (ub == lb) return ub;
+  double best = ub;
+  const int m = n - 1;
+  const int nprefix = m * (m - 1);
+  for (int p = lane; p < nprefix; p += 32) {
+    const int a = 1 + p / (m - 1);
+    const int bi = p % (m - 1);
+    const int b = 1 + bi + ((1 + bi) >= a ? 1 : 0);
+    const double c2 = smax(rm[a], rm[a * n + b]);
+    if (c2 >= best) continue;
+    if (n == 3) {
+      best = smin(best, smax(c2, rm[b * n]));
+      continue;
+    }
+    int path[8];
+    double cmx[8];
+    int nxt[9];
+    path[0] = 0;
+    path[1] = a;
+    path[2] = b;
+    cmx[2] = c2;
+    unsigned used = 1u | (1u << a) | (1u << b);
+    int d = 3;
+    nxt[3] = 1;
+    while (d >= 3) {
+      if (d == n) {
+        best = smin(best, smax(cmx[n - 1], rm[path[n - 1] * n]));
+        --d;
+        used &= ~(1u << path[d]);
+        continue;
+      }
+      int v = nxt[d];
+      while (v < n && ((used >> v) & 1u)) ++v;
+      if (v >= n) {
+        --d;
+        if (d >= 3) used &= ~(1u << path[d]);
+        continue;
+      }
+      nxt[d] = v + 1;
+      const double c = smax(cmx[d - 1], rm[path[d - 1] * n + v]);
+      if (c >= best) continue;
+      path[d] = v;
+      cmx[d] = c;
+      used |= 1u << v;
+      ++d;
+      nxt[d] = 1;
+    }
+  }
+  return warp_min(best);
+}
+
+// Top-2 (value, position) among edges, excluding positions ex0/ex1.
+__device__ __forceinline__ void top2_merge(double& v1, int& p1, double& v2, int& p2, double ov1,
+                                           int op1, double ov2, int op2) {
+  // merge two top-2 lists (values only matter; positions distinct by construction)
+  double a[4] = {v1, v2, ov1, ov2};
+  int b[4] = {p1, p2, op1, op2};
+  double bv1 = -kInf, bv2 = -kInf;
+  int bp1 = -1, bp2 = -1;
+  for (int i = 0; i < 4; ++i) {
+    if (b[i] < 0) continue;
+    if (b[i] == bp1 || b[i] == bp2) continue;
+    if (bp1 < 0 || a[i] > bv1) {
+      bv2 = bv1;
+      bp2 = bp1;
+      bv1 = a[i];
+      bp1 = b[i];
+    } else if (bp2 < 0 || a[i] > bv2) {
+      bv2 = a[i];
+      bp2 = b[i];
+    }
+  }
+  v1 = bv1;
+  p1 = bp1;
+  v2 = bv2;
+  p2 = bp2;
+}
+
+// Nearest neighbour from devs[0] + bottleneck 2-opt, replicated exactly
+// (heuristic_ring, cost_model.cpp:27-90): NN picks the earliest span position
+// among the minima; 2-opt scans (i, j) lexicographically, continues after an
+// acceptance, at most 8 passes, stops after a pass without improvement.
+// A swap can only be accepted when every max-valued edge is one of the two
+// removed edges, so each scan only visits the O(n) pairs that can succeed;
+// the rejected pairs the reference visits change nothing.
+__device__ __noinline__ double ring_heuristic(const DevProblem& P, Ws& s, const uint8_t* devs, int n) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* tour = s.tour;
+  double* edge = s.edge;
+  bool used[8] = {false, false, false, false, false, false, false, false};
+  if (lane == 0) used[0] = true;
+  int last = devs[0];
+  if (lane == 0) tour[0] = devs[0];
+  for (int step = 1; step < n; ++step) {
+    double bc = kInf;
+    int bi = 0x7fffffff;
+    for (int r = 0; r < 8; ++r) {
+      const int i = lane + 32 * r;
+      if (i >= n) break;
+      if (!used[r]) {
+        const double c = ecost(P, s, last, devs[i]);
+        if (c < bc) {
+          bc = c;
+          bi = i;
+        }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oc = __shfl_xor_sync(kFull, bc, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (oc < bc || (oc == bc && oi < bi)) {
+        bc = oc;
+        bi = oi;
+      }
+    }
+    if ((bi & 31) == lane) used[bi >> 5] = true;
+    last = devs[bi];
+    if (lane == 0) tour[step] = static_cast<uint8_t>(last);
+  }
+  __syncwarp();
+  double bott = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    edge[i] = ecost(P, s, tour[i], tour[(i + 1) % n]);
+    bott = smax(bott, edge[i]);
+  }
+  bott = warp_max(bott);
+  __syncwarp();
+  for (int pass = 0; pass < 8 && bott > 0; ++pass) {
+    bool improved = false;
+    int ci = 1, cj = 2;  // lexicographic resume point of the scan
+    while (ci <= n - 2) {
+      // positions holding the bottleneck value
+      int cnt = 0, p = 0x7fffffff, q = 0x7fffffff;
+      for (int i = lane; i < n; i += 32) {
+        if (edge[i] == bott) {
+          ++cnt;
+          if (i < p) {
+            q = p;
+            p = i;
+          } else if (i < q) {
+            q = i;
+          }
+        }
+      }
+      cnt = warp_sum_i(cnt);
+      if (cnt >= 3) break;
+      for (int o = 16; o > 0; o >>= 1) {
+        const int op = __shfl_xor_sync(kFull, p, o);
+        const int oq = __shfl_xor_sync(kFull, q, o);
+        int np, nq;
+        if (op < p) {
+          np = op;
+          nq = min(p, oq);
+        } else {
+          np = p;
+          nq = min(q, op);
+        }
+        p = np;
+        q = nq;
+      }
+      // top-2 among non-bottleneck positions (for "rest")
+      double v1 = -kInf, v2 = -kInf;
+      int p1 = -1, p2 = -1;
+      for (int i = lane; i < n; i += 32) {
+        if (i == p || (cnt == 2 && i == q)) continue;
+        top2_merge(v1, p1, v2, p2, edge[i], i, -kInf, -1);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov1 = __shfl_xor_sync(kFull, v1, o);
+        const int op1 = __shfl_xor_sync(kFull, p1, o);
+        const double ov2 = __shfl_xor_sync(kFull, v2, o);
+        const int op2 = __shfl_xor_sync(kFull, p2, o);
+        top2_merge(v1, p1, v2, p2, ov1, op1, ov2, op2);
+      }
+      // candidate list in lexicographic order
+      int na = 0, nb = 0;
+      int a_lo = 1, b_lo = 0;
+      if (cnt == 2) {
+        // single candidate (p+1, q)
+        na = 0;
+        if (p + 1 <= n - 2 && q >= p + 2) {
+          nb = 1;
+        }
+        b_lo = q;
+      } else {
+        if (p >= 2) na = p - 1;  // (i, p), i = 1..p-1
+        if (p + 1 <= n - 2) nb = n - 1 - (p + 1);  // (p+1, j), j = p+2..n-1
+        b_lo = p + 2;
+      }
+      const int total = na + nb;
+      bool found = false;
+      int fi = 0, fj = 0;
+      double fn1 = 0, fn2 = 0, fcand = 0;
+      for (int base = 0; base < total && !found; base += 32) {
+        const int c = base + lane;
+        bool acc = false;
+        int i = 0, j = 0;
+        double n1 = 0, n2 = 0, cd = 0;
+        if (c < total) {
+          if (c < na) {
+            i = a_lo + c;
+            j = p;
+          } else if (cnt == 2) {
+            i = p + 1;
+            j = q;
+          } else {
+            i = p + 1;
+            j = b_lo + (c - na);
+          }
+          const bool after = (i > ci) || (i == ci && j >= cj);
+          if (after) {
+            n1 = ecost(P, s, tour[i - 1], tour[j]);
+            n2 = ecost(P, s, tour[i], tour[(j + 1) % n]);
+            double rest;
+            if (cnt == 2) {
+              rest = v1;
+            } else {
+              const int x = (i - 1 == p) ? j : i - 1;
+              rest = (p1 != x) ? v1 : v2;
+            }
+            cd = smax(smax(n1, n2), rest);
+            acc = cd < bott;
+          }
+        }
+        const unsigned bal = __ballot_sync(kFull, acc);
+        if (bal) {
+          const int src = __ffs(bal) - 1;
+          fi = __shfl_sync(kFull, i, src);
+          fj = __shfl_sync(kFull, j, src);
+          fn1 = __shfl_sync(kFull, n1, src);
+          fn2 = __shfl_sync(kFull, n2, src);
+          fcand = __shfl_sync(kFull, cd, src);
+          found = true;
+        }
+      }
+      if (!found) break;
+      // std::reverse(tour+i, tour+j+1); std::reverse(edge+i, edge+j)
+      __syncwarp();
+      const int len_t = fj - fi + 1;
+      for (int k = lane; k < len_t / 2; k += 32) {
+        const uint8_t tmp = tour[fi + k];
+        tour[fi + k] = tour[fj - k];
+        tour[fj - k] = tmp;
+      }
+      const int len_e = fj - fi;
+      for (int k = lane; k < len_e / 2; k += 32) {
+        const double tmp = edge[fi + k];
+        edge[fi + k] = edge[fj - 1 - k];
+        edge[fj - 1 - k] = tmp;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        edge[fi - 1] = fn1;
+        edge[fj] = fn2;
+      }
+      __syncwarp();
+      bott = fcand;
+      improved = true;
+      ci = fi;
+      cj = fj + 1;
+      if (cj > n - 1) {
+        ci = fi + 1;
+        cj = ci + 1;
+      }
+    }
+    if (!improved) break;
+  }
+  __syncwarp();
+  return bott;
+}
+
+// min_ring_bottleneck (cost_model.cpp:179-207); class costs must be staged.
+__device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8_t* devs, int n) {
+  if (n <= 1) return 0.0;
+  if (n == 2) return ecost(P, s, devs[0], devs[1]);
+  if (n <= 8) return ring_small(P, s, devs, n);
+  return ring_heuristic(P, s, devs, n);
+}
+
+// ---- task_cost_detail (cost_model.cpp:270-396) ----
+//
+// Leaves per-cell comp/tp/pp/hbm in s.c_* for the balancers and writes the
+// aggregate TaskCost (comp, tp, pp, dp, bubble, hbm, total) to agg[0..6].
+__device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig& cfg, Ws& s, int t,
+                                 bool use_resident, double* agg) {
+  const int lane = threadIdx.x & 31;
+  const DevTask& tk = P.task[t];
+  const int dp = s.h.dp[t], pp = s.h.pp[t], tp = s.h.tp[t];
+  const int64_t seq_total = P.seq_in + P.seq_out;
+  const uint8_t* dv = s.dev + s.o.dev[t];
+  const int32_t* sl = s.sl + s.o.sl[t];
+  const int64_t* nm = s.nm + s.o.w[t];
+  const int cell0 = s.o.cell[t];
+  const int ncell = dp * pp;
+
+  // geometry memo: TP rings per cell, PP pairs per cell boundary
+  if (tp > 1 && !((s.memo_tp_ok >> t) & 1)) {
+    const double cv_tp = tp_comm_volume(tk.precision_bytes, P.mbs, seq_total, tk.h1, tp);
+    class_costs(P, s, cv_tp);
+    if (tp == 2) {
+      for (int c = lane; c < ncell; c += 32) s.rtp[cell0 + c] = ecost(P, s, dv[c * 2], dv[c * 2 + 1]);
+    } else {
+      for (int c = 0; c < ncell; ++c) {
+        const double r = ring_bottleneck(P, s, dv + c * tp, tp);
+        if (lane == 0) s.rtp[cell0 + c] = r;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) s.memo_tp_ok |= 1 << t;
+  }
+  if (pp > 1 && !((s.memo_pp_ok >> t) & 1)) {
+    const double cv_pp = pp_comm_volume(tk.precision_bytes, P.mbs, seq_total, tk.h1);
+    class_costs(P, s, cv_pp);
+    for (int c = lane; c < ncell; c += 32) {
+      const int j = c % pp;
+      if (j + 1 < pp) {
+        double best = kInf;
+        const uint8_t* a = dv + c * tp;
+        const uint8_t* b = dv + (c + 1) * tp;
+        for (int x = 0; x < tp; ++x)
+          for (int y = 0; y < tp; ++y) best = smin(best, ecost(P, s, a[x], b[y]));
+        s.ppp[cell0 + c] = best;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) s.memo_pp_ok |= 1 << t;
+  }
+  __syncwarp();
+
+  const double tpf = tp_pass_factor(tk.kind, cfg.recompute != 0);
+  const double ppf = pp_pass_factor(tk.kind);
+  const double flops = layer_flops(comp_seq(P, tk.kind), tk.h1, tk.h2);
+  const bool do_hbm = tk.kind == kGeneration && P.seq_out > 0;
+
+  // phase 1: one lane per (replica, stage) cell
+  for (int c = lane; c < ncell; c += 32) {
+    const int i = c / pp, j = c % pp;
+    const int64_t nmi = nm[i];
+    const int64_t nl_j = sl[j];
+    double comp = 0.0, hbm = 0.0;
+    for (int k = 0; k < tp; ++k) {
+      const int d = dv[c * tp + k];
+      comp = smax(comp, compute_cost(tk.kind, nmi, P.mbs, nl_j, flops, P.comp[d], tp));
+      if (do_hbm) {
+        double dbs = cfg.dbs_override;
+        if (dbs <= 0) {
+          const double kv_seq = kv_bytes_per_sequence(P, tk, static_cast<int>(nl_j), tp, cfg);
+          const double res = use_resident
+                                 ? s.resident[d]
+                                 : weights_memory_bytes(tk, static_cast<int>(nl_j), tp, j, pp, cfg);
+          const double free_bytes = P.mem[d] - res;
+          dbs = floor(free_bytes / kv_seq);
+          const double hi = static_cast<double>(nmi * P.mbs);
+          dbs = (dbs < 1.0) ? 1.0 : ((hi < dbs) ? hi : dbs);  // std::clamp
+        }
+        hbm = smax(hbm, hbm_decode_cost(P.seq_out, nmi, P.mbs, tk.precision_bytes, nl_j, tk.h1,
+                                        tk.h2, dbs, P.hbm[d], tp));
+      }
+    }
+    s.c_comp[c] = comp;
+    s.c_hbm[c] = hbm;
+    s.c_tp[c] = tp > 1 ? tpf * static_cast<double>(nmi) * static_cast<double>(nl_j) *
+                             s.rtp[cell0 + c]
+                       : 0.0;
+    s.c_pp[c] = (j + 1 < pp) ? ppf * static_cast<double>(nmi) * s.ppp[cell0 + c] : 0.0;
+  }
+  __syncwarp();
+
+  // phase 2: one lane per replica (sequential stage sums, bubble_cost :243-249)
+  const bool training = tk.kind == kTraining;
+  double m_comp = 0.0, m_tp = 0.0, m_pp = 0.0, m_hbm = 0.0, m_bub = 0.0, m_tot = 0.0;
+  for (int i = lane; i < dp; i += 32) {
+    double stage_max = 0.0;
+    for (int j = 0; j < pp; ++j) {
+      const int c = i * pp + j;
+      m_comp = smax(m_comp, s.c_comp[c]);
+      m_tp = smax(m_tp, s.c_tp[c]);
+      m_pp = smax(m_pp, s.c_pp[c]);
+      m_hbm = smax(m_hbm, s.c_hbm[c]);
+      stage_max = smax(stage_max, s.c_comp[c] + s.c_tp[c] + s.c_pp[c] + s.c_hbm[c]);
+    }
+    double bub = 0.0;
+    if (training && pp > 1) {
+      double sum = 0.0;
+      for (int j = 1; j < pp; ++j) {
+        const int c = i * pp + j;
+        sum += s.c_comp[c] + s.c_tp[c] + s.c_pp[c];
+      }
+      bub = sum / static_cast<double>(nm[i]);
+    }
+    m_bub = smax(m_bub, bub);
+    m_tot = smax(m_tot, training ? stage_max + bub : stage_max);
+  }
+  m_comp = warp_max(m_comp);
+  m_tp = warp_max(m_tp);
+  m_pp = warp_max(m_pp);
+  m_hbm = warp_max(m_hbm);
+  m_bub = warp_max(m_bub);
+  m_tot = warp_max(m_tot);
+
+  // phase 3: DP gradient rings over replica peers (training, dp > 1)
+  double a_dp = 0.0;
+  if (training && dp > 1) {
+    const int k0 = s.o.dpk[t];
+    for (int j = 0; j < pp; ++j) {
+      const int nl_j = sl[j];
+      bool need = false;
+      for (int k = 0; k < tp; ++k) need |= s.dpr_sl[k0 + j * tp + k] != nl_j;
+      if (need) {
+        const double cv_dp = dp_comm_volume(tk.precision_bytes, nl_j, tk.h1, tk.h2, dp, tp);
+        class_costs(P, s, cv_dp);
+        if (dp == 2) {
+          for (int k = lane; k < tp; k += 32) {
+            s.dpr[k0 + j * tp + k] = ecost(P, s, dv[flat(0, j, k, pp, tp)], dv[flat(1, j, k, pp, tp)]);
+            s.dpr_sl[k0 + j * tp + k] = nl_j;
+          }
+        } else {
+          for (int k = 0; k < tp; ++k) {
+            __syncwarp();
+            for (int i = lane; i < dp; i += 32) s.peers[i] = dv[flat(i, j, k, pp, tp)];
+            __syncwarp();
+            const double r = ring_bottleneck(P, s, s.peers, dp);
+            if (lane == 0) {
+              s.dpr[k0 + j * tp + k] = r;
+              s.dpr_sl[k0 + j * tp + k] = nl_j;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      for (int k = 0; k < tp; ++k) a_dp = smax(a_dp, s.dpr[k0 + j * tp + k]);
+    }
+  }
+  if (training) m_tot += a_dp;
+  agg[0] = m_comp;
+  agg[1] = m_tp;
+  agg[2] = m_pp;
+  agg[3] = a_dp;
+  agg[4] = m_bub;
+  agg[5] = m_hbm;
+  agg[6] = m_tot;
+  __syncwarp();
+}
+
+// aggregate_phi (cost_model.cpp:251-262)
+__device__ __forceinline__ double phi(const double* c, int n, double eta) {
+  double mx = -kInf, sum = 0.0;
+  for (int i = 0; i < n; ++i) {
+    mx = smax(mx, c[i]);
+    sum += c[i];
+  }
+  return mx + (1.0 - eta) * (sum - mx);
+}
+
+struct E2E {
+  double e2e;
+  double reshard;
+  double sync;
+  bool feasible;
+};
+
+// end_to_end_cost (cost_model.cpp:431-487). Per-task aggregates land in s.agg.
+__device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig& cfg, Ws& s) {
+  const int lane = threadIdx.x & 31;
+  const int N = P.n_dev;
+  __syncwarp();
+  for (int d = lane; d < N; d += 32) {
+    double r = 0.0;
+    for (int t = 0; t < P.n_tasks; ++t) {
+      const int j = s.dstage[t * N + d];
+      if (j == 0xff) continue;
+      r += weights_memory_bytes(P.task[t], s.sl[s.o.sl[t] + j], s.h.tp[t], j, s.h.pp[t], cfg);
+    }
+    s.resident[d] = r;
+  }
+  __syncwarp();
+  double tot[kMaxTasks];
+  for (int t = 0; t < P.n_tasks; ++t) {
+    task_cost(P, cfg, s, t, true, s.agg + 7 * t);
+    tot[t] = s.agg[7 * t + 6];
+  }
+  E2E r;
+  r.reshard = 0.0;
+  r.sync = 0.0;
+  double transfer = 0.0;
+  const double ov = P.mode == 0 ? cfg.reshard_override : cfg.sync_override;
+  if (ov >= 0) {
+    transfer = ov;
+  } else if (P.gen_slot >= 0 && P.train6_slot >= 0) {
+    if (!s.bridge_ok) {
+      const DevTask& g = P.task[P.gen_slot];
+      const double bytes = static_cast<double>(g.param_count) * g.precision_bytes;
+      class_costs(P, s, bytes);
+      const int ga = P.gen_slot, tb = P.train6_slot;
+      const int na = s.h.dp[ga] * s.h.pp[ga] * s.h.tp[ga];
+      const int nb = s.h.dp[tb] * s.h.pp[tb] * s.h.tp[tb];
+      const uint8_t* A = s.dev + s.o.dev[ga];
+      const uint8_t* B = s.dev + s.o.dev[tb];
+      double best = kInf;
+      for (int e = lane; e < na * nb; e += 32) best = smin(best, ecost(P, s, A[e / nb], B[e % nb]));
+      best = warp_min(best);
+      if (lane == 0) {
+        s.bridge = best;
+        s.bridge_ok = 1;
+      }
+      __syncwarp();
+    }
+    transfer = s.bridge;
+  }
+  if (P.mode == 0) {
+    r.reshard = transfer;
+  } else {
+    r.sync = transfer;
+  }
+  // compose_end_to_end (cost_model.cpp:403-429): kinds staged, phi within a kind
+  double gens[kMaxTasks], infs[kMaxTasks], trains[kMaxTasks];
+  int ng = 0, ni = 0, ntr = 0;
+  for (int t = 0; t < P.n_tasks; ++t) {
+    if (P.task[t].kind == kGeneration) gens[ng++] = tot[t];
+    else if (P.task[t].kind == kInference) infs[ni++] = tot[t];
+    else trains[ntr++] = tot[t];
+  }
+  const double gen = ng == 0 ? 0.0 : phi(gens, ng, P.eta);
+  const double inf = ni == 0 ? 0.0 : phi(infs, ni, P.eta);
+  const double trn = ntr == 0 ? 0.0 : phi(trains, ntr, P.eta);
+  if (P.mode == 0) {
+    r.e2e = gen + inf + trn + transfer;
+  } else {
+    r.e2e = smax(gen, inf + trn) + transfer;
+  }
+  r.feasible = check_memory(P, cfg, s);
+  return r;
+}
+
+}  // namespace dev
+}  // namespace hpg

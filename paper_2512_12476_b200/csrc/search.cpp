@@ -1,0 +1,1035 @@
+// Host side of the search: enumerations, candidate generation, the per-arm GA
+// (coroutines) and the nested successive-halving schedule, executed in
+// lockstep waves against eval_kernel. Reference: proj/src/search.cpp,
+// proj/src/combinatorics.cpp, proj/include/hetplan/rng.hpp.
+#include "search.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <coroutine>
+#include <cstring>
+#include <exception>
+#include <functional>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <set>
+
+#include "eval_launch.hpp"
+
+namespace hpg {
+
+namespace {
+
+int ceil_log2(size_t n) {
+  int r = 0;
+  size_t v = 1;
+  while (v < n) {
+    v <<= 1;
+    ++r;
+  }
+  return r;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+DevCostConfig Knobs::cost_config() const {
+  hpg_cost_config c = default_cost_config();
+  c.recompute = recompute ? 1 : 0;
+  c.reshard_override = reshard_override;
+  c.sync_override = sync_override;
+  return to_dev_cfg(c);
+}
+
+Knobs knobs_from_c(const Problem& P, const hpg_knobs& k) {
+  Knobs o;
+  o.budget = k.budget;
+  o.seed = k.seed;
+  o.population = k.population;
+  o.locality_bias = k.locality_bias;
+  o.quantize = k.quantize_gpu_counts;
+  o.adjacent = k.level1_filter_adjacent != 0;
+  o.level1_cap = k.level1_cap;
+  o.gg_arm_cap = k.gg_arm_cap;
+  o.swap_pair_sample = k.swap_pair_sample;
+  o.balance_data = k.balance_data != 0;
+  o.balance_layers = k.balance_layers != 0;
+  o.recompute = k.recompute != 0;
+  o.reshard_override = k.reshard_override;
+  o.sync_override = k.sync_override;
+  // parse_knobs_json validation (search.cpp:75-83)
+  if (o.population < 1 || o.swap_pair_sample < 0 || o.gg_arm_cap < 1)
+    throw InputError("knobs: population and gg_arm_cap must be >= 1");
+  if (o.locality_bias < 0 || o.locality_bias > 1)
+    throw InputError("knobs: locality_bias must be within [0, 1]");
+  if (k.n_tg_override > 0) {
+    o.has_tg_override = true;
+    for (int i = 0; i < k.n_tg_override; ++i) {
+      int ng = 0;
+      for (int s = 0; s < P.T; ++s) ng = std::max(ng, k.tg_override[i * P.T + s] + 1);
+      Grouping g(ng);
+      for (int s = 0; s < P.T; ++s) {
+        const int gi = k.tg_override[i * P.T + s];
+        if (gi < 0) throw InputError("task grouping must cover every workflow task");
+        g[gi].push_back(s);
+      }
+      for (const auto& grp : g)
+        if (grp.empty()) throw InputError("task groups must be non-empty");
+      o.tg_override.push_back(std::move(g));
+    }
+  }
+  return o;
+}
+
+// ---- enumerations ----
+
+std::vector<Grouping> enumerate_task_groupings(const Problem& P, bool adjacent) {
+  // set_partitions in restricted-growth-string order (combinatorics.cpp:10-46)
+  const int n = P.T;
+  std::vector<Grouping> out;
+  std::vector<int> a(n, 0);
+  while (true) {
+    const int blocks = *std::max_element(a.begin(), a.end()) + 1;
+    Grouping g(blocks);
+    for (int i = 0; i < n; ++i) g[a[i]].push_back(i);
+    bool keep = true;
+    if (adjacent) {  // level1_filter "adjacent" (search.cpp:636-656)
+      for (const auto& group : g) {
+        if (group.size() < 2) continue;
+        bool adj = false;
+        for (int x : group)
+          for (int y : group)
+            if (P.dep_edges.count({P.tasks[x].id, P.tasks[y].id})) adj = true;
+        if (!adj) keep = false;
+      }
+    }
+    if (keep) out.push_back(std::move(g));
+    int i = n - 1;
+    for (; i > 0; --i) {
+      int prefix_max = 0;
+      for (int j = 0; j < i; ++j) prefix_max = std::max(prefix_max, a[j]);
+      if (a[i] <= prefix_max) {
+        ++a[i];
+        std::fill(a.begin() + i + 1, a.end(), 0);
+        break;
+      }
+    }
+    if (i == 0) break;
+  }
+  return out;
+}
+
+std::vector<std::vector<int>> compositions(int total, int parts, int quantum) {
+  std::vector<std::vector<int>> out;
+  if (parts <= 0 || total < parts) return out;
+  if (quantum > 1) {
+    if (total % quantum != 0) return out;
+    out = compositions(total / quantum, parts, 1);
+    for (auto& c : out)
+      for (auto& v : c) v *= quantum;
+    return out;
+  }
+  std::vector<int> cur;
+  std::function<void(int, int)> rec = [&](int remaining, int slots) {
+    if (slots == 1) {
+      cur.push_back(remaining);
+      out.push_back(cur);
+      cur.pop_back();
+      return;
+    }
+    for (int v = 1; v <= remaining - (slots - 1); ++v) {
+      cur.push_back(v);
+      rec(remaining - v, slots - 1);
+      cur.pop_back();
+    }
+  };
+  rec(total, parts);
+  return out;
+}
+
+double composition_count(int total, int parts, int quantum) {
+  if (parts <= 0 || total < parts) return 0.0;
+  if (quantum > 1) {
+    if (total % quantum != 0) return 0.0;
+    return composition_count(total / quantum, parts, 1);
+  }
+  double r = 1.0;
+  for (int i = 1; i <= parts - 1; ++i) {
+    r = r * static_cast<double>(total - parts + i) / static_cast<double>(i);
+  }
+  return r;
+}
+
+std::vector<int> sample_composition(int total, int parts, int quantum, Rng& rng) {
+  if (quantum > 1 && total % quantum == 0 && total / quantum >= parts) {
+    auto scaled = sample_composition(total / quantum, parts, 1, rng);
+    for (auto& v : scaled) v *= quantum;
+    return scaled;
+  }
+  std::vector<int> cuts;
+  while (static_cast<int>(cuts.size()) < parts - 1) {
+    const int c = 1 + static_cast<int>(rng.bounded(static_cast<uint64_t>(total - 1)));
+    if (std::find(cuts.begin(), cuts.end(), c) == cuts.end()) cuts.push_back(c);
+  }
+  std::sort(cuts.begin(), cuts.end());
+  std::vector<int> comp;
+  int prev = 0;
+  for (int c : cuts) {
+    comp.push_back(c - prev);
+    prev = c;
+  }
+  comp.push_back(total - prev);
+  return comp;
+}
+
+namespace {
+
+struct Layout {
+  int dp, pp, tp;
+};
+
+// enumerate_layouts (search.cpp:127-150)
+std::vector<Layout> enumerate_layouts(int group_size, int64_t nl, int max_tp) {
+  std::vector<Layout> out;
+  for (int dp = 1; dp <= group_size; ++dp) {
+    if (group_size % dp != 0) continue;
+    const int rest = group_size / dp;
+    for (int pp = 1; pp <= rest; ++pp) {
+      if (rest % pp != 0) continue;
+      const int tp = rest / pp;
+      if (pp > nl || tp > max_tp) continue;
+      out.push_back({dp, pp, tp});
+    }
+  }
+  return out;
+}
+
+// ---- candidate generation (search.cpp:152-234, 318-421) ----
+
+struct ArmLayouts {
+  std::vector<int> task_order;                // slots, group order
+  std::vector<std::vector<Layout>> options;   // per slot
+  bool feasible = true;
+};
+
+ArmLayouts build_arm_layouts(const Problem& P, const Grouping& tg, const std::vector<int>& counts) {
+  ArmLayouts al;
+  al.options.resize(P.T);
+  for (size_t g = 0; g < tg.size(); ++g) {
+    for (int s : tg[g]) {
+      auto opts = enumerate_layouts(counts[g], P.tasks[s].nl, P.max_node_size);
+      if (opts.empty()) al.feasible = false;
+      al.task_order.push_back(s);
+      al.options[s] = std::move(opts);
+    }
+  }
+  return al;
+}
+
+void medium_assignment(const Problem& P, double bias, Rng& rng, std::vector<int>& flat) {
+  flat.clear();
+  const int R = static_cast<int>(P.region_nodes.size());
+  int regions[kMaxDevices];
+  for (int r = 0; r < R; ++r) regions[r] = r;
+  rng.shuffle(regions, R);
+  int nodes[kMaxDevices];
+  for (int ri = 0; ri < R; ++ri) {
+    const auto& rn = P.region_nodes[regions[ri]];
+    const int nn = static_cast<int>(rn.size());
+    for (int k = 0; k < nn; ++k) nodes[k] = k;
+    rng.shuffle(nodes, nn);
+    for (int k = 0; k < nn; ++k)
+      for (int d : rn[nodes[k]]) flat.push_back(d);
+  }
+  for (size_t i = flat.size(); i > 1; --i) {
+    const bool scramble = rng.uniform() < (1.0 - bias);
+    const uint64_t pick = rng.bounded(i);
+    if (scramble) std::swap(flat[i - 1], flat[pick]);
+  }
+}
+
+// random_fine_assignment: node blocks (lexicographic node names) shuffled,
+// devices shuffled within a block.
+void fine_assignment(const Problem& P, const int* group_devs, int n, Rng& rng, uint8_t* out) {
+  int ranks[kMaxDevices];
+  int nr = 0;
+  for (int i = 0; i < n; ++i) {
+    const int r = P.node_rank[group_devs[i]];
+    bool seen = false;
+    for (int k = 0; k < nr; ++k) seen |= ranks[k] == r;
+    if (!seen) ranks[nr++] = r;
+  }
+  std::sort(ranks, ranks + nr);
+  rng.shuffle(ranks, nr);
+  int pos = 0;
+  int bucket[kMaxDevices];
+  for (int k = 0; k < nr; ++k) {
+    int nb = 0;
+    for (int i = 0; i < n; ++i)
+      if (P.node_rank[group_devs[i]] == ranks[k]) bucket[nb++] = group_devs[i];
+    rng.shuffle(bucket, nb);
+    for (int i = 0; i < nb; ++i) out[pos++] = static_cast<uint8_t>(bucket[i]);
+  }
+}
+
+struct ArmEnv {
+  const Problem& P;
+  const Knobs& K;
+  const Grouping& tg;
+  const std::vector<int>& counts;
+  ArmLayouts al;
+  std::vector<int> group_of;  // slot -> group
+};
+
+void make_candidate(const ArmEnv& e, int64_t combo, Rng& rng, Cand& c) {
+  const Problem& P = e.P;
+  int dp[kMaxTasks], pp[kMaxTasks], tp[kMaxTasks];
+  for (int s : e.al.task_order) {
+    const auto& opts = e.al.options[s];
+    const Layout& l = opts[static_cast<size_t>(combo) % opts.size()];
+    combo /= static_cast<int64_t>(opts.size());
+    dp[s] = l.dp;
+    pp[s] = l.pp;
+    tp[s] = l.tp;
+  }
+  init_cand(c, P.T, dp, pp, tp, P);
+  std::vector<int> flat;
+  flat.reserve(P.N);
+  medium_assignment(P, e.K.locality_bias, rng, flat);
+  int cursor = 0;
+  for (size_t g = 0; g < e.tg.size(); ++g) {
+    const int cnt = e.counts[g];
+    for (int s : e.tg[g]) fine_assignment(P, flat.data() + cursor, cnt, rng, c.dev() + c.o.dev[s]);
+    cursor += cnt;
+  }
+}
+
+// group_device_set (search.cpp:336-341): devices of the group's first task in
+// lexicographic device-id order
+void group_device_set(const ArmEnv& e, const Cand& c, size_t g, int* out, int& n) {
+  const int s = e.tg[g].front();
+  n = c.size(s);
+  const uint8_t* d = c.dev() + c.o.dev[s];
+  for (int i = 0; i < n; ++i) out[i] = d[i];
+  std::sort(out, out + n, [&](int a, int b) { return e.P.id_rank[a] < e.P.id_rank[b]; });
+}
+
+bool random_move(const ArmEnv& e, Cand& c, int level, Rng& rng) {
+  if (level == 3) {
+    const size_t ng = e.tg.size();
+    if (ng < 2) return false;
+    const size_t g1 = rng.bounded(ng);
+    size_t g2 = rng.bounded(ng - 1);
+    if (g2 >= g1) ++g2;
+    int d1[kMaxDevices], d2[kMaxDevices];
+    int n1, n2;
+    group_device_set(e, c, g1, d1, n1);
+    group_device_set(e, c, g2, d2, n2);
+    // GCC evaluates the two bounded() arguments right to left
+    // (search.cpp:378-379): the d2 index is drawn first.
+    const int b = d2[rng.bounded(static_cast<uint64_t>(n2))];
+    const int a = d1[rng.bounded(static_cast<uint64_t>(n1))];
+    for (int s : e.tg[g1]) {
+      uint8_t* d = c.dev() + c.o.dev[s];
+      for (int i = 0; i < c.size(s); ++i)
+        if (d[i] == a) {
+          d[i] = static_cast<uint8_t>(b);
+          break;
+        }
+    }
+    for (int s : e.tg[g2]) {
+      uint8_t* d = c.dev() + c.o.dev[s];
+      for (int i = 0; i < c.size(s); ++i)
+        if (d[i] == b) {
+          d[i] = static_cast<uint8_t>(a);
+          break;
+        }
+    }
+    return true;
+  }
+  int eligible[kMaxTasks];
+  int ne = 0;
+  for (int s = 0; s < e.P.T; ++s)
+    if (c.size(s) >= 2) eligible[ne++] = s;
+  if (ne == 0) return false;
+  const int s = eligible[rng.bounded(static_cast<uint64_t>(ne))];
+  const size_t n = static_cast<size_t>(c.size(s));
+  const size_t p1 = rng.bounded(n);
+  size_t p2 = rng.bounded(n - 1);
+  if (p2 >= p1) ++p2;
+  uint8_t* d = c.dev() + c.o.dev[s];
+  std::swap(d[p1], d[p2]);
+  return true;
+}
+
+bool mutate(const ArmEnv& e, Cand& c, Rng& rng) {
+  const bool has_l3 = e.tg.size() >= 2;
+  bool has_l5 = false;
+  for (int s = 0; s < e.P.T; ++s)
+    if (c.size(s) >= 2) has_l5 = true;
+  if (!has_l3 && !has_l5) return false;
+  int level;
+  if (has_l3 && has_l5) {
+    level = rng.bounded(2) == 0 ? 3 : 5;
+  } else {
+    level = has_l3 ? 3 : 5;
+  }
+  return random_move(e, c, level, rng);
+}
+
+// ---- coroutine plumbing ----
+
+struct EvalReq {
+  std::vector<Cand> cands;
+  std::vector<EvalResult> res;
+};
+
+struct ArmCoro {
+  struct promise_type {
+    EvalReq* pending = nullptr;
+    std::exception_ptr exc;
+    ArmCoro get_return_object() {
+      return ArmCoro{std::coroutine_handle<promise_type>::from_promise(*this)};
+    }
+    std::suspend_always initial_suspend() noexcept { return {}; }
+    std::suspend_always final_suspend() noexcept { return {}; }
+    void return_void() {}
+    void unhandled_exception() { exc = std::current_exception(); }
+  };
+  std::coroutine_handle<promise_type> h;
+  ArmCoro() = default;
+  explicit ArmCoro(std::coroutine_handle<promise_type> hh) : h(hh) {}
+  ArmCoro(ArmCoro&& o) noexcept : h(o.h) { o.h = nullptr; }
+  ArmCoro& operator=(ArmCoro&& o) noexcept {
+    if (h) h.destroy();
+    h = o.h;
+    o.h = nullptr;
+    return *this;
+  }
+  ~ArmCoro() {
+    if (h) h.destroy();
+  }
+};
+
+struct EvalAwait {
+  EvalReq* req;
+  bool await_ready() const noexcept { return false; }
+  void await_suspend(std::coroutine_handle<ArmCoro::promise_type> h) noexcept {
+    h.promise().pending = req;
+  }
+  void await_resume() const noexcept {}
+};
+
+struct Improvement {
+  int64_t local_idx;  // 1-based evaluation index inside the run
+  double cost;
+  Cand plan;
+  double t_wall;
+};
+
+struct ArmRun {
+  int64_t ti = 0, gi = 0;
+  int64_t slice = 0;
+  Rng rng;
+  int64_t used = 0;
+  double best = kInf;
+  std::vector<Improvement> impr;
+  // ga_search result (best inserted member, search.cpp:464-469)
+  bool has_best_member = false;
+  Cand best_member;
+  double best_member_cost = kInf;
+  std::unique_ptr<ArmEnv> env;
+  ArmCoro coro;
+  double* clock = nullptr;
+};
+
+// ga_run (search.cpp:437-565) as a coroutine.
+ArmCoro ga_run(ArmRun& run) {
+  ArmEnv& e = *run.env;
+  const Knobs& K = e.K;
+  Rng& rng = run.rng;
+  const int64_t slice = run.slice;
+  if (slice <= 0) co_return;
+  if (!e.al.feasible) co_return;
+  struct Member {
+    Cand plan;
+    double cost;
+    uint64_t seq;
+  };
+  std::vector<Member> pop;
+  uint64_t seq = 0;
+  auto score = [&](const Cand& c, double cost) {
+    ++run.used;
+    if (cost < run.best) {
+      run.best = cost;
+      run.impr.push_back({run.used, cost, c, *run.clock});
+    }
+  };
+  auto insert_member = [&](const Cand& plan, double cost) {
+    if (cost < run.best_member_cost) {
+      run.best_member_cost = cost;
+      run.best_member = plan;
+      run.has_best_member = true;
+    }
+    Member m{plan, cost, seq++};
+    auto pos = std::upper_bound(pop.begin(), pop.end(), m, [](const Member& a, const Member& b) {
+      return a.cost != b.cost ? a.cost < b.cost : a.seq < b.seq;
+    });
+    pop.insert(pos, std::move(m));
+    if (static_cast<int>(pop.size()) > K.population) pop.pop_back();
+  };
+  EvalReq req;
+  std::vector<Rng> snaps;
+
+  // init: cycle layout combinations (speculative chunks, one wave each)
+  const int64_t init_target =
+      std::max<int64_t>(1, std::min({slice, static_cast<int64_t>(K.population), slice / 2}));
+  const int64_t attempt_cap = 64 + 16 * init_target;
+  int64_t attempts = 0, combo = 0, chunk = 0;
+  while (static_cast<int64_t>(pop.size()) < init_target && run.used < slice &&
+         attempts < attempt_cap) {
+    const int64_t need = init_target - static_cast<int64_t>(pop.size());
+    chunk = std::min(attempt_cap - attempts, std::max(chunk * 2, 2 * need + 2));
+    req.cands.assign(chunk, Cand{});
+    snaps.clear();
+    const int64_t combo0 = combo;
+    for (int64_t c = 0; c < chunk; ++c) {
+      make_candidate(e, combo++, rng, req.cands[c]);
+      snaps.push_back(rng);
+    }
+    co_await EvalAwait{&req};
+    for (int64_t c = 0; c < chunk; ++c) {
+      ++attempts;
+      if (!(req.res[c].flags & kResFeasIn)) continue;
+      score(req.cands[c], req.res[c].cost);
+      insert_member(req.cands[c], req.res[c].cost);
+      if (static_cast<int64_t>(pop.size()) >= init_target) {
+        rng = snaps[c];
+        combo = combo0 + c + 1;
+        break;
+      }
+    }
+  }
+  if (pop.empty()) co_return;
+
+  // offspring generations
+  int64_t streak = 0;
+  while (run.used < slice && streak < 64) {
+    Cand child = pop[rng.bounded(pop.size())].plan;
+    req.cands.clear();
+    snaps.clear();
+    int ntr = 0;
+    for (int tries = 0; tries < 8; ++tries) {
+      Cand trial = child;
+      if (!mutate(e, trial, rng)) break;
+      req.cands.push_back(std::move(trial));
+      snaps.push_back(rng);
+      ++ntr;
+    }
+    const Rng after_all = rng;
+    req.cands.push_back(child);  // the unmutated parent, in case no trial fits
+    co_await EvalAwait{&req};
+    int chosen = -1;
+    for (int i = 0; i < ntr; ++i) {
+      if (req.res[i].flags & kResFeasIn) {
+        chosen = i;
+        break;
+      }
+    }
+    double cost;
+    if (chosen >= 0) {
+      rng = snaps[chosen];
+      child = std::move(req.cands[chosen]);
+      cost = req.res[chosen].cost;
+    } else {
+      rng = after_all;
+      if (!(req.res[ntr].flags & kResFeasIn)) {
+        ++streak;
+        continue;
+      }
+      child = std::move(req.cands[ntr]);
+      cost = req.res[ntr].cost;
+    }
+    streak = 0;
+    score(child, cost);
+    for (int level : {3, 5}) {
+      if (run.used >= slice) break;
+      req.cands.clear();
+      snaps.clear();
+      const Rng before = rng;
+      int ngen = 0;
+      for (int t = 0; t < K.swap_pair_sample; ++t) {
+        Cand cand = child;
+        if (!random_move(e, cand, level, rng)) break;
+        req.cands.push_back(std::move(cand));
+        snaps.push_back(rng);
+        ++ngen;
+      }
+      if (ngen == 0) continue;
+      co_await EvalAwait{&req};
+      bool stopped = false;
+      for (int t = 0; t < ngen; ++t) {
+        if (run.used >= slice) {
+          rng = t == 0 ? before : snaps[t - 1];
+          stopped = true;
+          break;
+        }
+        if (!(req.res[t].flags & kResFeasIn)) continue;
+        const double c2 = req.res[t].cost;
+        score(req.cands[t], c2);
+        if (c2 < cost) {
+          child = std::move(req.cands[t]);
+          cost = c2;
+          rng = snaps[t];
+          stopped = true;
+          break;
+        }
+      }
+      if (!stopped) rng = snaps.back();
+    }
+    if (static_cast<int>(pop.size()) < K.population || cost < pop.back().cost) {
+      insert_member(child, cost);
+    }
+  }
+}
+
+// Runs all arm coroutines to completion, batching their requests per wave.
+void run_lockstep(Ctx& ctx, const Knobs& K, std::vector<ArmRun*>& runs, double& clock,
+                  int64_t& waves) {
+  const DevCostConfig cfg = K.cost_config();
+  const int kb = (K.balance_data ? 1 : 0) | (K.balance_layers ? 2 : 0);
+  for (ArmRun* r : runs) {
+    r->clock = &clock;
+    r->coro = ga_run(*r);
+    r->coro.h.resume();
+    if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
+  }
+  Batch b;
+  BatchOut bo;
+  std::vector<std::pair<ArmRun*, int>> owners;
+  while (true) {
+    b.cands.clear();
+    b.modes.clear();
+    owners.clear();
+    for (ArmRun* r : runs) {
+      if (r->coro.h.done()) continue;
+      EvalReq* q = r->coro.h.promise().pending;
+      if (!q) continue;
+      for (size_t i = 0; i < q->cands.size(); ++i) {
+        b.cands.push_back(&q->cands[i]);
+        b.modes.push_back(kModeEvaluate);
+      }
+      owners.emplace_back(r, static_cast<int>(q->cands.size()));
+    }
+    if (owners.empty()) break;
+    run_batch(ctx, b, cfg, kb, true, false, false, bo);
+    ++waves;
+    clock = now_s();
+    size_t k = 0;
+    for (auto& [r, cnt] : owners) {
+      EvalReq* q = r->coro.h.promise().pending;
+      q->res.resize(cnt);
+      for (int i = 0; i < cnt; ++i, ++k) {
+        q->res[i] = bo.res[k];
+        Cand& c = q->cands[i];
+        std::memcpy(c.rec.data(), bo.out_recs->p + bo.off[k], c.o.bytes);
+      }
+      r->coro.h.promise().pending = nullptr;
+    }
+    for (auto& [r, cnt] : owners) {
+      r->coro.h.resume();
+      if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
+    }
+  }
+}
+
+// best_half (search.cpp:590-620) for many segments at once, on the device.
+struct Segment {
+  std::vector<int64_t> arms;   // ascending
+  std::vector<double> scores;  // per arm
+};
+
+void best_half_batch(Ctx& ctx, std::vector<Segment>& segs, int level,
+                     std::vector<std::vector<int64_t>>& keep_out, std::vector<Halving>& ev_out,
+                     std::vector<bool>& has_event) {
+  const int ns = static_cast<int>(segs.size());
+  keep_out.assign(ns, {});
+  ev_out.assign(ns, Halving{});
+  has_event.assign(ns, false);
+  std::vector<int32_t> off(1, 0);
+  std::vector<double> sc;
+  std::vector<int32_t> idx;
+  std::vector<int> seg_of;
+  for (int s = 0; s < ns; ++s) {
+    if (segs[s].arms.size() <= 1) {
+      keep_out[s] = segs[s].arms;
+      continue;
+    }
+    for (size_t i = 0; i < segs[s].arms.size(); ++i) {
+      sc.push_back(segs[s].scores[i]);
+      idx.push_back(static_cast<int32_t>(segs[s].arms[i]));
+    }
+    off.push_back(static_cast<int32_t>(sc.size()));
+    seg_of.push_back(s);
+  }
+  const int nk = static_cast<int>(seg_of.size());
+  if (nk == 0) return;
+  const size_t n = sc.size();
+  ctx.d_scores.reserve(n);
+  ctx.d_arm_idx.reserve(n);
+  ctx.d_keep.reserve(n);
+  ctx.d_seg_off.reserve(nk + 1);
+  ctx.d_events.reserve(2 * nk);
+  cudaStream_t st = ctx.stream;
+  cuda_check(cudaMemcpyAsync(ctx.d_scores.p, sc.data(), 8 * n, cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemcpyAsync(ctx.d_arm_idx.p, idx.data(), 4 * n, cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemcpyAsync(ctx.d_seg_off.p, off.data(), 4 * (nk + 1), cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(launch_best_half(ctx.d_scores.p, ctx.d_seg_off.p, ctx.d_arm_idx.p, nk, ctx.d_keep.p,
+                              ctx.d_events.p, st),
+             "best_half launch");
+  ++ctx.launches;
+  std::vector<int32_t> keep(n);
+  std::vector<double> ev(2 * nk);
+  cuda_check(cudaMemcpyAsync(keep.data(), ctx.d_keep.p, 4 * n, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaMemcpyAsync(ev.data(), ctx.d_events.p, 16 * nk, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "best_half");
+  for (int k = 0; k < nk; ++k) {
+    const int s = seg_of[k];
+    for (int i = off[k]; i < off[k + 1]; ++i)
+      if (keep[i]) keep_out[s].push_back(idx[i]);
+    std::sort(keep_out[s].begin(), keep_out[s].end());
+    Halving h;
+    h.level = level;
+    h.before = off[k + 1] - off[k];
+    h.after = (h.before + 1) / 2;
+    h.survivor_worst = ev[2 * k];
+    h.eliminated_best = ev[2 * k + 1];
+    ev_out[s] = h;
+    has_event[s] = true;
+  }
+}
+
+struct TgArm {
+  Grouping tg;
+  std::vector<std::vector<int>> ggs;
+  std::vector<double> best;
+  std::vector<int64_t> alive;
+  std::vector<int64_t> rec;
+};
+
+}  // namespace
+
+SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
+  (void)dist;
+  if (K.budget < 1) throw UsageError("search budget must be >= 1");
+  const Problem& P = ctx.prob;
+  const double t0 = now_s();
+  const int64_t launches0 = ctx.launches, plans0 = ctx.plans_evaluated;
+  const Rng base_rng(K.seed);
+  SearchOut S;
+  S.budget = K.budget;
+  S.seed = K.seed;
+
+  std::vector<Grouping> tgs = K.has_tg_override ? K.tg_override : enumerate_task_groupings(P, K.adjacent);
+  if (K.level1_cap > 0 && tgs.size() > static_cast<size_t>(K.level1_cap)) tgs.resize(K.level1_cap);
+  S.task_groupings = static_cast<int64_t>(tgs.size());
+
+  const int n_devices = P.N;
+  std::vector<TgArm> arms;
+  for (size_t ti = 0; ti < tgs.size(); ++ti) {
+    TgArm arm;
+    arm.tg = tgs[ti];
+    const int k = static_cast<int>(arm.tg.size());
+    if (k <= n_devices) {
+      int q = K.quantize;
+      double count = composition_count(n_devices, k, q);
+      if (count == 0) {
+        q = 1;
+        count = composition_count(n_devices, k, q);
+      }
+      if (count <= K.gg_arm_cap) {
+        arm.ggs = compositions(n_devices, k, q);
+      } else {
+        std::set<std::vector<int>> seen;
+        std::vector<int> balanced(k, n_devices / k);
+        for (int i = 0; i < n_devices % k; ++i) ++balanced[i];
+        seen.insert(balanced);
+        arm.ggs.push_back(balanced);
+        Rng rng = base_rng.fork(0xA001 + ti);
+        for (int64_t tries = 0; static_cast<int>(arm.ggs.size()) < K.gg_arm_cap &&
+                                tries < 50LL * K.gg_arm_cap;
+             ++tries) {
+          auto comp = sample_composition(n_devices, k, q, rng);
+          if (seen.insert(comp).second) arm.ggs.push_back(std::move(comp));
+        }
+      }
+    }
+    arm.best.assign(arm.ggs.size(), kInf);
+    for (size_t gi = 0; gi < arm.ggs.size(); ++gi) {
+      arm.alive.push_back(static_cast<int64_t>(gi));
+      arm.rec.push_back(static_cast<int64_t>(S.arms.size()));
+      ArmRec r;
+      r.tg = static_cast<int64_t>(ti);
+      r.gg = static_cast<int64_t>(gi);
+      S.arms.push_back(r);
+    }
+    arms.push_back(std::move(arm));
+  }
+
+  double incumbent = kInf;
+  Cand inc_plan;
+  int64_t inc_ti = -1, inc_gi = -1;
+  double inc_time = t0;
+  int64_t consumed = 0;
+  double clock = t0;
+  int64_t waves = 0;
+
+  std::vector<int64_t> surv(tgs.size());
+  std::iota(surv.begin(), surv.end(), 0);
+  const int denom_out = std::max(1, ceil_log2(tgs.size()));
+  for (int m = 0; m < denom_out; ++m) {
+    const int64_t b_m = K.budget / (static_cast<int64_t>(surv.size()) * denom_out);
+    S.b_m.push_back(b_m);
+    // participating task groupings and their round budget b
+    std::vector<std::pair<int64_t, int64_t>> parts;
+    if (b_m >= 1) {
+      for (int64_t ti : surv) parts.emplace_back(ti, b_m);
+    } else {
+      int64_t ob = K.budget / denom_out;
+      if (ob == 0 && m == 0) ob = K.budget;
+      for (int64_t ti : surv) {
+        if (static_cast<int64_t>(parts.size()) >= ob) break;
+        parts.emplace_back(ti, 1);
+      }
+    }
+    struct Part {
+      int64_t ti, b;
+      std::vector<int64_t> entry, cur;
+      int rounds, denom_in;
+      std::vector<Halving> events;
+      std::vector<std::vector<int64_t>> surv_sets;
+      std::vector<std::vector<std::unique_ptr<ArmRun>>> runs;  // per n, in gi order
+    };
+    std::vector<Part> ps;
+    for (auto& [ti, b] : parts) {
+      if (arms[ti].alive.empty()) continue;
+      Part p;
+      p.ti = ti;
+      p.b = b;
+      p.entry = arms[ti].alive;
+      p.cur = p.entry;
+      p.denom_in = std::max(1, ceil_log2(p.entry.size()));
+      p.rounds = p.denom_in;
+      ps.push_back(std::move(p));
+    }
+    int max_rounds = 0;
+    for (auto& p : ps) max_rounds = std::max(max_rounds, p.rounds);
+    for (int n = 0; n < max_rounds; ++n) {
+      std::vector<ArmRun*> batch;
+      for (auto& p : ps) {
+        p.runs.emplace_back();
+        if (n >= p.rounds) continue;
+        auto& list = p.runs.back();
+        auto add = [&](int64_t gi, int64_t slice) {
+          auto r = std::make_unique<ArmRun>();
+          r->ti = p.ti;
+          r->gi = gi;
+          r->slice = slice;
+          const uint64_t salt = (static_cast<uint64_t>(p.ti) << 40) |
+                                (static_cast<uint64_t>(gi) << 16) |
+                                (static_cast<uint64_t>(m) << 8) | static_cast<uint64_t>(n);
+          r->rng = base_rng.fork(salt);
+          TgArm& arm = arms[p.ti];
+          r->env.reset(new ArmEnv{P, K, arm.tg, arm.ggs[gi], build_arm_layouts(P, arm.tg, arm.ggs[gi]), {}});
+          batch.push_back(r.get());
+          list.push_back(std::move(r));
+        };
+        const int64_t b_mn = p.b / (static_cast<int64_t>(p.cur.size()) * p.denom_in);
+        if (b_mn >= 1) {
+          for (int64_t gi : p.cur) add(gi, b_mn);
+        } else {
+          int64_t rb = p.b / p.denom_in;
+          if (rb == 0 && n == 0) rb = p.b;
+          int64_t spent = 0;
+          for (int64_t gi : p.cur) {
+            if (spent >= rb) break;
+            add(gi, 1);
+            ++spent;
+          }
+        }
+      }
+      run_lockstep(ctx, K, batch, clock, waves);
+      // fold run results into the arm records
+      for (auto& p : ps) {
+        if (n >= p.rounds) continue;
+        TgArm& arm = arms[p.ti];
+        for (auto& r : p.runs.back()) {
+          ArmRec& rec = S.arms[arm.rec[r->gi]];
+          rec.evals += r->used;
+          rec.best = std::min(rec.best, r->best);
+          arm.best[r->gi] = rec.best;
+        }
+      }
+      std::vector<Segment> segs;
+      std::vector<Part*> owners;
+      for (auto& p : ps) {
+        if (n >= p.rounds) continue;
+        Segment sg;
+        sg.arms = p.cur;
+        for (int64_t gi : p.cur) sg.scores.push_back(arms[p.ti].best[gi]);
+        segs.push_back(std::move(sg));
+        owners.push_back(&p);
+      }
+      std::vector<std::vector<int64_t>> keep;
+      std::vector<Halving> ev;
+      std::vector<bool> has_ev;
+      best_half_batch(ctx, segs, 2, keep, ev, has_ev);
+      for (size_t s = 0; s < owners.size(); ++s) {
+        owners[s]->cur = keep[s];
+        if (has_ev[s]) {
+          owners[s]->events.push_back(ev[s]);
+          owners[s]->surv_sets.push_back(keep[s]);
+        }
+      }
+    }
+    {
+      std::vector<Segment> segs;
+      for (auto& p : ps) {
+        Segment sg;
+        sg.arms = p.entry;
+        for (int64_t gi : p.entry) sg.scores.push_back(arms[p.ti].best[gi]);
+        segs.push_back(std::move(sg));
+      }
+      std::vector<std::vector<int64_t>> keep;
+      std::vector<Halving> ev;
+      std::vector<bool> has_ev;
+      best_half_batch(ctx, segs, 2, keep, ev, has_ev);
+      for (size_t s = 0; s < ps.size(); ++s) {
+        arms[ps[s].ti].alive = keep[s];
+        if (has_ev[s]) {
+          ps[s].events.push_back(ev[s]);
+          ps[s].surv_sets.push_back(keep[s]);
+        }
+      }
+    }
+    // sequential order: task groupings in survivor order, rounds, arms
+    for (auto& p : ps) {
+      for (size_t i = 0; i < p.events.size(); ++i) {
+        S.halvings.push_back(p.events[i]);
+        S.survivors.push_back(p.surv_sets[i]);
+      }
+      for (auto& list : p.runs) {
+        for (auto& r : list) {
+          for (auto& im : r->impr) {
+            if (im.cost < incumbent) {
+              incumbent = im.cost;
+              inc_plan = im.plan;
+              inc_ti = r->ti;
+              inc_gi = r->gi;
+              inc_time = im.t_wall;
+              S.trace.emplace_back(consumed + im.local_idx, im.cost);
+            }
+          }
+          consumed += r->used;
+        }
+      }
+    }
+    // level-1 halving over task groupings (tg score = min over all gg arms)
+    std::vector<Segment> segs(1);
+    segs[0].arms = surv;
+    for (int64_t ti : surv) {
+      double best = kInf;
+      for (double c : arms[ti].best) best = std::min(best, c);
+      segs[0].scores.push_back(best);
+    }
+    std::vector<std::vector<int64_t>> keep;
+    std::vector<Halving> ev;
+    std::vector<bool> has_ev;
+    best_half_batch(ctx, segs, 1, keep, ev, has_ev);
+    surv = keep[0];
+    if (has_ev[0]) {
+      S.halvings.push_back(ev[0]);
+      S.survivors.push_back(keep[0]);
+    }
+  }
+  S.consumed = consumed;
+  if (consumed > K.budget) throw InternalError("search overspent its budget");
+  if (inc_ti >= 0) {
+    S.has_plan = true;
+    S.plan = inc_plan;
+    S.plan_groups = arms[inc_ti].tg;
+    S.plan_counts = arms[inc_ti].ggs[inc_gi];
+    // breakdown of the incumbent (end_to_end_cost with the search's config)
+    Batch b;
+    b.cands.push_back(&S.plan);
+    b.modes.push_back(kModeE2E);
+    BatchOut bo;
+    run_batch(ctx, b, K.cost_config(), 0, false, true, false, bo);
+    S.per_task = bo.per_task;
+    S.reshard_s = bo.res[0].reshard_s;
+    S.sync_s = bo.res[0].sync_s;
+    S.e2e = bo.res[0].cost;
+    S.feasible = (bo.res[0].flags & kResFeasOut) != 0;
+    S.est_cost = S.e2e;
+  }
+  S.wall_s = now_s() - t0;
+  S.time_to_best_s = S.has_plan ? inc_time - t0 : 0.0;
+  S.launches = ctx.launches - launches0;
+  S.plans_gpu = ctx.plans_evaluated - plans0;
+  S.waves = waves;
+  return S;
+}
+
+SearchOut ga_search(Ctx& ctx, const Grouping& tg, const std::vector<int>& counts, int64_t slice,
+                    uint64_t seed, const Knobs& K) {
+  if (slice < 1) throw UsageError("ga_search needs a budget of at least 1 evaluation");
+  const Problem& P = ctx.prob;
+  if (counts.size() != tg.size()) throw InputError("gpu grouping must list one count per task group");
+  const double t0 = now_s();
+  const int64_t launches0 = ctx.launches, plans0 = ctx.plans_evaluated;
+  ArmRun r;
+  r.slice = slice;
+  r.rng = Rng(seed);
+  r.env.reset(new ArmEnv{P, K, tg, counts, build_arm_layouts(P, tg, counts), {}});
+  std::vector<ArmRun*> runs{&r};
+  double clock = t0;
+  int64_t waves = 0;
+  run_lockstep(ctx, K, runs, clock, waves);
+  SearchOut S;
+  S.budget = slice;
+  S.seed = seed;
+  S.consumed = r.used;
+  ArmRec rec;
+  rec.best = r.best_member_cost;
+  rec.evals = r.used;
+  S.arms.push_back(rec);
+  for (auto& im : r.impr) S.trace.emplace_back(im.local_idx, im.cost);
+  if (r.has_best_member) {
+    S.has_plan = true;
+    S.plan = r.best_member;
+    S.plan_groups = tg;
+    S.plan_counts = counts;
+    Batch b;
+    b.cands.push_back(&S.plan);
+    b.modes.push_back(kModeE2E);
+    BatchOut bo;
+    run_batch(ctx, b, K.cost_config(), 0, false, true, false, bo);
+    S.per_task = bo.per_task;
+    S.reshard_s = bo.res[0].reshard_s;
+    S.sync_s = bo.res[0].sync_s;
+    S.e2e = bo.res[0].cost;
+    S.feasible = (bo.res[0].flags & kResFeasOut) != 0;
+    S.est_cost = r.best_member_cost;
+  }
+  S.wall_s = now_s() - t0;
+  S.launches = ctx.launches - launches0;
+  S.plans_gpu = ctx.plans_evaluated - plans0;
+  S.waves = waves;
+  return S;
+}
+
+}  // namespace hpg

@@ -1,0 +1,175 @@
+"""GPU parity: the CUDA path (libhpg.so through the C ABI) against golden
+vectors produced by the compiled reference (oracle/_ref/ref_dump).
+
+The bar is bit-identity: every FP64 cost component, every feasibility flag,
+every balanced split/weight, and for searches the consumed budget, b_m, the
+incumbent trace, every arm record, every halving event, the survivor set after
+every halving round and the chosen plan. (north_star asks for 1e-9 relative;
+the kernels are built -fmad=false and restate the reference's operation order,
+so the tests demand exact bits.)
+"""
+import pytest
+
+from golden_util import check_breakdown, hx, load, plan_from_golden, same
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(wf_obj, topo_obj):
+    from paper_2512_12476_b200 import Engine, parse_topology, parse_workflow
+    return Engine(parse_workflow(wf_obj), parse_topology(topo_obj), device=0)
+
+
+def _check_plan_eq(got: dict, want: dict, ctx=""):
+    bad = []
+    if [list(g) for g in got["groups"]] != [list(g) for g in want["groups"]]:
+        bad.append(f"{ctx} groups {got['groups']} != {want['groups']}")
+    if list(got["counts"]) != list(want["counts"]):
+        bad.append(f"{ctx} counts {got['counts']} != {want['counts']}")
+    for tid, l in want["layouts"].items():
+        g = got["layouts"][int(tid)]
+        for k in ("dp", "pp", "tp", "stage_layers"):
+            if g[k] != l[k]:
+                bad.append(f"{ctx} task {tid} {k}: {g[k]} != {l[k]}")
+        if len(g["weights"]) != len(l["weights"]) or not all(
+                same(a, hx(b)) for a, b in zip(g["weights"], l["weights"])):
+            bad.append(f"{ctx} task {tid} weights differ")
+    for tid, devs in want["assignment"].items():
+        if list(got["assignment"][int(tid)]) != list(devs):
+            bad.append(f"{ctx} task {tid} assignment differs")
+    return bad
+
+
+def _check_records(eng, recs, cfg, with_eval):
+    plans = [plan_from_golden(r["plan"]) for r in recs]
+    bds = eng.end_to_end_cost(plans, cfg)
+    feas, req = eng.check_memory(plans, cfg)
+    bal_d = eng.balance_data(plans, cfg)
+    bal_l = eng.balance_layers(plans, cfg)
+    bad = []
+    for i, r in enumerate(recs):
+        bad += check_breakdown(bds[i], r["e2e"], f"plan {i}")
+        viol = r["violations"]
+        if feas[i] != (len(viol) == 0):
+            bad.append(f"plan {i}: feasible {feas[i]} vs {len(viol)} violations")
+        for d, required, cap in viol:
+            if not same(req[i][d], hx(required)):
+                bad.append(f"plan {i}: required bytes on device {d}")
+        for lab, got, want in (("balance_data", bal_d[i], r["balance_data"]),
+                               ("balance_layers", bal_l[i], r["balance_layers"])):
+            bad += _check_plan_eq(got, want, f"plan {i} {lab}")
+    if with_eval:
+        from paper_2512_12476_b200 import CostModelConfig
+        ev = eng.evaluate(plans, CostModelConfig())
+        for i, r in enumerate(recs):
+            bad += _check_plan_eq(ev[i], r["evaluate"]["plan"], f"plan {i} evaluate")
+            if not same(ev[i]["_e2e"], hx(r["evaluate"]["bd"]["end_to_end_s"])):
+                bad.append(f"plan {i} evaluate e2e {ev[i]['_e2e']!r}")
+    return bad
+
+
+def test_fuzz_instances_bit_exact():
+    """acceptance-#1-style random instances (tiny models, random topologies,
+    random CostModelConfig incl. dbs/override/memory-model variations,
+    embeddings, task subsets, async mode)."""
+    from paper_2512_12476_b200 import CostModelConfig
+    g = load("fuzz_eval.json")
+    bad = []
+    for i, r in enumerate(g["records"]):
+        with _engine(r["workflow"], r["topology"]) as eng:
+            cfg = CostModelConfig.from_json(r["cfg"])
+            bad += [f"rec {i}: {b}" for b in _check_records(eng, [r], cfg, False)]
+    assert not bad, "\n".join(bad[:20])
+
+
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3", "c4"])
+def test_config_plans_bit_exact(cfg_name):
+    """A.5 generator + testutil::random_plan plans on the survey configs:
+    end_to_end_cost, check_memory, balance_data, balance_layers and the
+    search's evaluate() chain."""
+    from paper_2512_12476_b200 import CostModelConfig
+    g = load(f"evalplans_{cfg_name}.json")
+    with _engine(g["workflow"], g["topology"]) as eng:
+        bad = _check_records(eng, g["records"], CostModelConfig.from_json(g["cfg"]), True)
+    assert not bad, "\n".join(bad[:20])
+
+
+def check_search(res, gold, ctx=""):
+    bad = []
+    if res.consumed != gold["consumed"]:
+        bad.append(f"{ctx} consumed {res.consumed} != {gold['consumed']}")
+    if res.b_m != gold["b_m"]:
+        bad.append(f"{ctx} b_m {res.b_m} != {gold['b_m']}")
+    want_trace = [(c, hx(v)) for c, v in gold["trace"]]
+    if len(res.trace) != len(want_trace) or not all(
+            a[0] == b[0] and same(a[1], b[1]) for a, b in zip(res.trace, want_trace)):
+        bad.append(f"{ctx} trace differs: {res.trace[:5]} vs {want_trace[:5]}")
+    if len(res.arms) != len(gold["arms"]):
+        bad.append(f"{ctx} arm count {len(res.arms)} != {len(gold['arms'])}")
+    else:
+        for i, (a, b) in enumerate(zip(res.arms, gold["arms"])):
+            if a[0] != b[0] or a[1] != b[1] or a[3] != b[3] or not same(a[2], hx(b[2])):
+                bad.append(f"{ctx} arm {i}: {a} != {b}")
+                break
+    want_h = [(h[0], h[1], h[2], hx(h[3]), hx(h[4])) for h in gold["halvings"]]
+    if len(res.halvings) != len(want_h) or not all(
+            a[:3] == b[:3] and same(a[3], b[3]) and same(a[4], b[4])
+            for a, b in zip(res.halvings, want_h)):
+        bad.append(f"{ctx} halvings differ")
+    if res.survivors != gold["survivors"]:
+        bad.append(f"{ctx} survivor sets differ")
+    if bool(res.plan) != bool(gold["has_plan"]):
+        bad.append(f"{ctx} has_plan {bool(res.plan)} != {gold['has_plan']}")
+    elif res.plan:
+        bad += _check_plan_eq(res.plan, gold["plan"], f"{ctx} chosen plan")
+        bad += check_breakdown(res.breakdown, gold["breakdown"], f"{ctx} breakdown")
+        if not same(res.plan["estimated_cost_s"], hx(gold["plan"]["estimated_cost_s"])):
+            bad.append(f"{ctx} estimated_cost_s")
+        if res.plan["provenance"]["budget"] != gold["plan"]["provenance"]["budget"]:
+            bad.append(f"{ctx} provenance budget")
+    return bad
+
+
+@pytest.mark.parametrize("name", ["search_c1_b1000.json", "search_c2_b1000.json"])
+def test_search_configs_identical(name):
+    from paper_2512_12476_b200 import SearchKnobs
+    g = load(name)
+    assert g["replay_consistent"]
+    with _engine(g["workflow"], g["topology"]) as eng:
+        res = eng.nested_sha_search(SearchKnobs.from_json(g["knobs"]))
+    bad = check_search(res, g, name)
+    assert not bad, "\n".join(bad[:20])
+
+
+def test_search_fuzz_identical():
+    """60 tiny searches with random knobs (balancing on/off, population,
+    locality bias, swap sample, gg cap, quantization, level-1 filter/cap,
+    overrides)."""
+    from paper_2512_12476_b200 import SearchKnobs
+    g = load("searchfuzz.json")
+    bad = []
+    for i, r in enumerate(g["records"]):
+        with _engine(r["workflow"], r["topology"]) as eng:
+            res = eng.nested_sha_search(SearchKnobs.from_json(r["knobs"]))
+        bad += check_search(res, r, f"search {i}")
+    assert not bad, "\n".join(bad[:30])
+
+
+def test_sweep_c4_bit_exact():
+    """config-5 generator on the GPU reproduces the reference's costs bit for
+    bit (plans regenerated on the CPU by ref_dump from the same counters)."""
+    from paper_2512_12476_b200 import Engine, load_topology, load_workflow
+    from golden_util import FIXTURES
+    import os
+    g = load("sweep_c4.json")
+    wf = load_workflow(os.path.join(FIXTURES, "c4.workflow.json"))
+    topo = load_topology(os.path.join(FIXTURES, "c4.topology.json"))
+    with Engine(wf, topo) as eng:
+        out = eng.sweep(g["seed"], g["k0"], g["count"])
+    want = [hx(v) for v in g["costs"]]
+    mism = [i for i, (a, b) in enumerate(zip(out["costs"], want)) if not same(a, b)]
+    assert not mism, f"{len(mism)} cost mismatches, first k={mism[:5]}"
+    assert out["feasible"] == [bool(x) for x in g["feasible"]]
+    assert out["n_feasible"] == g["n_feasible"]
+    if g["n_feasible"]:
+        assert out["best_k"] == g["best_k"] and same(out["best_cost"], hx(g["best"]))
