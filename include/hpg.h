@@ -220,6 +220,11 @@ typedef struct {
   int64_t gpu_launches;     /* kernel launches issued by the search */
   int64_t waves;            /* lockstep evaluation waves */
   int64_t plans_evaluated_gpu; /* plans scored on the device (incl. speculative) */
+  int64_t h2d_bytes;        /* host->device bytes moved by the search */
+  int64_t d2h_bytes;        /* device->host bytes moved by the search */
+  double eval_kernel_ms;    /* CUDA-event time of all eval_kernel launches */
+  int64_t eval_launches;
+  int64_t canonical_bytes;  /* SURVEY.md §8 D1 canonical bytes of all scored plans */
 } hpg_search_info;
 
 int hpg_result_info(const hpg_search_result* r, hpg_search_info* info);

@@ -324,6 +324,11 @@ int hpg_result_info(const hpg_search_result* r, hpg_search_info* info) {
   info->gpu_launches = o.launches;
   info->waves = o.waves;
   info->plans_evaluated_gpu = o.plans_gpu;
+  info->h2d_bytes = o.h2d_bytes;
+  info->d2h_bytes = o.d2h_bytes;
+  info->eval_kernel_ms = o.eval_ms;
+  info->eval_launches = o.eval_launches;
+  info->canonical_bytes = o.canonical_bytes;
   return HPG_OK;
 }
 

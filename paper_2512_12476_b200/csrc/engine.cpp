@@ -252,6 +252,8 @@ void init_cand(Cand& c, int T, const int* dp, const int* pp, const int* tp, cons
 Ctx::~Ctx() {
   if (d_blob) cudaFree(d_blob);
   if (d_sweep_tables) cudaFree(d_sweep_tables);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -273,6 +275,8 @@ Ctx* create_ctx(const hpg_problem& hp, int device) {
     ctx->device = device;
     ctx->n_sm = prop.multiProcessorCount;
     cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaEventCreate(&ctx->ev0), "event");
+    cuda_check(cudaEventCreate(&ctx->ev1), "event");
     const Problem& Q = ctx->prob;
     const int N = Q.N, C = static_cast<int>(Q.lat.size());
     const size_t bytes = 8 * (3 * N + 2 * C) + static_cast<size_t>(N) * N;
@@ -286,6 +290,7 @@ Ctx* create_ctx(const hpg_problem& hp, int device) {
     std::memcpy(blob.data() + 8 * (3 * N + 2 * C), Q.cls.data(), static_cast<size_t>(N) * N);
     cuda_check(cudaMalloc(&ctx->d_blob, bytes), "cudaMalloc problem");
     cuda_check(cudaMemcpy(ctx->d_blob, blob.data(), bytes, cudaMemcpyHostToDevice), "H2D problem");
+    ctx->h2d_bytes += static_cast<int64_t>(bytes);
     DevProblem& D = ctx->dprob;
     const double* db = reinterpret_cast<const double*>(ctx->d_blob);
     D.n_dev = N;
@@ -372,13 +377,37 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, total, cudaMemcpyHostToDevice, st), "H2D recs");
   cuda_check(cudaMemcpyAsync(ctx.d_off.p, ctx.h_off.p, 8 * n, cudaMemcpyHostToDevice, st), "H2D off");
   cuda_check(cudaMemcpyAsync(ctx.d_modes.p, ctx.h_modes.p, 4 * n, cudaMemcpyHostToDevice, st), "H2D modes");
+  cuda_check(cudaEventRecord(ctx.ev0, st), "event");
   cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, ctx.d_recs.p, ctx.d_off.p, ctx.d_modes.p, 0,
                          n, 0, want_out ? ctx.d_out.p : nullptr, ctx.d_res.p,
                          want_per_task ? ctx.d_per_task.p : nullptr,
                          want_required ? ctx.d_required.p : nullptr, ctx.n_sm, st),
              "eval_kernel launch");
+  cuda_check(cudaEventRecord(ctx.ev1, st), "event");
   ++ctx.launches;
+  ++ctx.eval_launches;
   ctx.plans_evaluated += n;
+  ctx.h2d_bytes += total + 12 * static_cast<int64_t>(n);
+  ctx.d2h_bytes += static_cast<int64_t>(sizeof(EvalResult)) * n + (want_out ? total : 0) +
+                   (want_per_task ? 8 * static_cast<int64_t>(n) * P.T * 7 : 0) +
+                   (want_required ? 8 * static_cast<int64_t>(n) * P.N : 0);
+  for (int i = 0; i < n; ++i) {
+    // canonical bytes: tg id + k counts + per task
+    // (3 + pp + slots) + 9 result bytes (+ 8*dp for a weighted generation task)
+    const Cand& c = *b.cands[i];
+    int64_t cb = 1 + c.ng + 9;
+    for (int t = 0; t < P.T; ++t) cb += 3 + c.hdr().pp[t] + c.size(t);
+    const int g = P.slot_of_id[1];
+    if (g >= 0) {
+      const double* w = c.w() + c.o.w[g];
+      for (int k = 0; k < c.hdr().dp[g]; ++k)
+        if (w[k] != 1.0) {
+          cb += 8 * c.hdr().dp[g];
+          break;
+        }
+    }
+    ctx.canonical_bytes += cb;
+  }
   cuda_check(cudaMemcpyAsync(ctx.h_res.p, ctx.d_res.p, sizeof(EvalResult) * n,
                              cudaMemcpyDeviceToHost, st), "D2H results");
   if (want_out) {
@@ -395,6 +424,9 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     cuda_check(cudaMemcpyAsync(out.required.data(), ctx.d_required.p, 8 * out.required.size(),
                                cudaMemcpyDeviceToHost, st), "D2H required");
   cuda_check(cudaStreamSynchronize(st), "eval_kernel");
+  float ms = 0.f;
+  cuda_check(cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1), "event time");
+  ctx.eval_ms += ms;
   std::memcpy(out.res.data(), ctx.h_res.p, sizeof(EvalResult) * n);
 }
 
@@ -434,6 +466,7 @@ std::vector<TablePlan> unpack_table(const Problem& P, const hpg_plan_table& t) {
     }
     init_cand(tp.cand, T, dp, pp, tpp, P);
     Cand& c = tp.cand;
+    c.ng = ng;
     std::vector<std::vector<int>> group_sets(ng);
     std::vector<bool> group_set_init(ng, false);
     for (int g = 0; g < ng; ++g) {

@@ -81,7 +81,7 @@ hpg_cost_config default_cost_config();
 struct Cand {
   std::vector<uint8_t> rec;
   RecOffsets o;
-  int tg = -1;  // arm task grouping (search only)
+  int ng = 1;   // number of task groups (canonical-bytes accounting)
   RecHeader& hdr() { return *reinterpret_cast<RecHeader*>(rec.data()); }
   const RecHeader& hdr() const { return *reinterpret_cast<const RecHeader*>(rec.data()); }
   double* w() { return reinterpret_cast<double*>(rec.data() + o.w_byte); }
@@ -171,6 +171,11 @@ struct Ctx {
   DevBuf<int32_t> d_seg_off, d_arm_idx, d_keep;
   int64_t launches = 0;
   int64_t plans_evaluated = 0;
+  // instrumentation for the bench contract
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+  int64_t eval_launches = 0, canonical_bytes = 0;
+  double eval_ms = 0.0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~Ctx();
 };
 

@@ -297,6 +297,7 @@ void make_candidate(const ArmEnv& e, int64_t combo, Rng& rng, Cand& c) {
     tp[s] = l.tp;
   }
   init_cand(c, P.T, dp, pp, tp, P);
+  c.ng = static_cast<int>(e.tg.size());
   std::vector<int> flat;
   flat.reserve(P.N);
   medium_assignment(P, e.K.locality_bias, rng, flat);
@@ -729,6 +730,9 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   const Problem& P = ctx.prob;
   const double t0 = now_s();
   const int64_t launches0 = ctx.launches, plans0 = ctx.plans_evaluated;
+  const int64_t h2d0 = ctx.h2d_bytes, d2h0 = ctx.d2h_bytes, el0 = ctx.eval_launches,
+                cb0 = ctx.canonical_bytes;
+  const double ems0 = ctx.eval_ms;
   const Rng base_rng(K.seed);
   SearchOut S;
   S.budget = K.budget;
@@ -981,6 +985,11 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   S.launches = ctx.launches - launches0;
   S.plans_gpu = ctx.plans_evaluated - plans0;
   S.waves = waves;
+  S.h2d_bytes = ctx.h2d_bytes - h2d0;
+  S.d2h_bytes = ctx.d2h_bytes - d2h0;
+  S.eval_launches = ctx.eval_launches - el0;
+  S.canonical_bytes = ctx.canonical_bytes - cb0;
+  S.eval_ms = ctx.eval_ms - ems0;
   return S;
 }
 

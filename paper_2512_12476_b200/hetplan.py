@@ -141,7 +141,9 @@ class _SearchInfo(C.Structure):
                 ("n_survivor_sets", C.c_int32), ("task_groupings", C.c_int64),
                 ("wall_s", C.c_double), ("time_to_best_s", C.c_double),
                 ("gpu_launches", C.c_int64), ("waves", C.c_int64),
-                ("plans_evaluated_gpu", C.c_int64)]
+                ("plans_evaluated_gpu", C.c_int64), ("h2d_bytes", C.c_int64),
+                ("d2h_bytes", C.c_int64), ("eval_kernel_ms", C.c_double),
+                ("eval_launches", C.c_int64), ("canonical_bytes", C.c_int64)]
 
 
 class _SweepStats(C.Structure):
