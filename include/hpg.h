@@ -225,6 +225,8 @@ typedef struct {
   double eval_kernel_ms;    /* CUDA-event time of all eval_kernel launches */
   int64_t eval_launches;
   int64_t canonical_bytes;  /* SURVEY.md §8 D1 canonical bytes of all scored plans */
+  double host_ms;           /* host GA time (candidate generation, bookkeeping) */
+  double batch_ms;          /* wall time of the evaluation waves (pack, copies, kernel, sync) */
 } hpg_search_info;
 
 int hpg_result_info(const hpg_search_result* r, hpg_search_info* info);

@@ -191,10 +191,14 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
     const uint64_t kk = k0 + done;
     cudaEventRecord(e0, st);
     cuda_check(launch_gen(tb, seed, kk, n, C.d_recs.p, stride, C.d_best.p, st), "gen_kernel");
+    int grid = 0;
+    cuda_check(eval_grid(cv, static_cast<int>(n), C.n_sm, grid), "eval_kernel occupancy");
+    const int64_t scratch = eval_scratch_doubles(P.N, C.max_nl);
+    C.d_scratch.reserve(static_cast<size_t>(grid) * scratch);
     cudaEventRecord(e1, st);
     cuda_check(launch_eval(C.dprob, cfg, cv, 0, C.d_recs.p, nullptr, nullptr, kModeE2E,
                            static_cast<int>(n), stride, nullptr, C.d_res.p, nullptr, nullptr,
-                           C.n_sm, st),
+                           C.d_scratch.p, scratch, grid, st),
                "eval_kernel");
     cudaEventRecord(e2, st);
     cuda_check(launch_reduce(C.d_res.p, n, kk, partial.p, red_blocks, st), "reduce_kernel");
@@ -329,6 +333,8 @@ int hpg_result_info(const hpg_search_result* r, hpg_search_info* info) {
   info->eval_kernel_ms = o.eval_ms;
   info->eval_launches = o.eval_launches;
   info->canonical_bytes = o.canonical_bytes;
+  info->host_ms = o.host_ms;
+  info->batch_ms = o.batch_ms;
   return HPG_OK;
 }
 

@@ -182,10 +182,12 @@ Problem build_problem(const hpg_problem& p) {
             [&](int x, int y) { return P.dev_id[x] < P.dev_id[y]; });
   P.id_rank.assign(N, 0);
   for (int r = 0; r < N; ++r) P.id_rank[order[r]] = r;
+  P.by_id_rank = order;
   std::map<std::string, int> node_names;
   for (int i = 0; i < N; ++i) node_names.emplace(P.dev_node[i], 0);
   int r = 0;
   for (auto& kv : node_names) kv.second = r++;
+  P.n_nodes = r;
   P.node_rank.assign(N, 0);
   for (int i = 0; i < N; ++i) P.node_rank[i] = node_names[P.dev_node[i]];
   std::map<std::string, std::map<std::string, std::vector<int>>> by_region;
@@ -308,6 +310,7 @@ Ctx* create_ctx(const hpg_problem& hp, int device) {
     D.seq_out = Q.seq_out;
     D.mbs = Q.mbs;
     D.total_seq = Q.global_batch * Q.rpp;
+    for (const HostTask& h : Q.tasks) ctx->max_nl = std::max(ctx->max_nl, h.nl);
     for (int t = 0; t < Q.T; ++t) {
       const HostTask& h = Q.tasks[t];
       DevTask& d = D.task[t];
@@ -377,11 +380,17 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, total, cudaMemcpyHostToDevice, st), "H2D recs");
   cuda_check(cudaMemcpyAsync(ctx.d_off.p, ctx.h_off.p, 8 * n, cudaMemcpyHostToDevice, st), "H2D off");
   cuda_check(cudaMemcpyAsync(ctx.d_modes.p, ctx.h_modes.p, 4 * n, cudaMemcpyHostToDevice, st), "H2D modes");
+  int grid = 0;
+  cuda_check(eval_grid(cv, n, ctx.n_sm, grid), "eval_kernel occupancy");
+  const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);
+  // sized once for the largest possible persistent grid (32 CTAs per SM)
+  ctx.d_scratch.reserve(static_cast<size_t>(std::max(grid, 32 * ctx.n_sm)) * scratch);
   cuda_check(cudaEventRecord(ctx.ev0, st), "event");
   cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, ctx.d_recs.p, ctx.d_off.p, ctx.d_modes.p, 0,
                          n, 0, want_out ? ctx.d_out.p : nullptr, ctx.d_res.p,
                          want_per_task ? ctx.d_per_task.p : nullptr,
-                         want_required ? ctx.d_required.p : nullptr, ctx.n_sm, st),
+                         want_required ? ctx.d_required.p : nullptr, ctx.d_scratch.p, scratch,
+                         grid, st),
              "eval_kernel launch");
   cuda_check(cudaEventRecord(ctx.ev1, st), "event");
   ++ctx.launches;

@@ -61,7 +61,9 @@ struct Problem {
   std::vector<double> lat, bw;
   // orders
   std::vector<int> id_rank;    // lexicographic rank of the device id
+  std::vector<int> by_id_rank; // device index at each id rank
   std::vector<int> node_rank;  // lexicographic rank of the node name (global)
+  int n_nodes = 0;
   // random_medium_assignment locality structure (search.cpp:163-186):
   // regions (lex) -> nodes (lex) -> devices (index order)
   std::vector<std::vector<std::vector<int>>> region_nodes;
@@ -161,6 +163,8 @@ struct Ctx {
   DevBuf<int32_t> d_modes;
   DevBuf<EvalResult> d_res;
   DevBuf<double> d_per_task, d_required;
+  DevBuf<double> d_scratch;  // per-CTA global scratch of eval_kernel
+  int64_t max_nl = 1;
   // sweep
   void* d_sweep_tables = nullptr;
   DevBuf<double> d_costs;
@@ -175,6 +179,8 @@ struct Ctx {
   int64_t h2d_bytes = 0, d2h_bytes = 0;
   int64_t eval_launches = 0, canonical_bytes = 0;
   double eval_ms = 0.0;
+  double host_ms = 0.0;   // GA coroutine time (candidate generation, bookkeeping)
+  double batch_ms = 0.0;  // run_batch wall time (pack, copies, kernel, sync)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~Ctx();
 };

@@ -69,12 +69,39 @@ struct Ws {
   int32_t* split_trial;  // [N]
   uint8_t* tour;     // [N]
   uint8_t* peers;    // [N]
+  double* mmt;       // [sum pp] model_memory_bytes per (task, stage) at the current split
+  double* wmt;       // [sum pp] working_memory_bytes per (task, stage)
+  double* wsave;     // [N]
+  int32_t* sl_save2;   // [sum pp]
+  int32_t* split_step; // [N]
+  double* dtab;      // global scratch: DP ring maxima per (stage, layer count), -1 = unknown
+  int32_t dtab_stride;
   int64_t nm_base[kMaxTasks];
   int32_t memo_tp_ok;   // bit t
   int32_t memo_pp_ok;
+  int32_t agg_ok;       // bit t: agg row t is end_to_end's task_cost for the current plan
+  int32_t resident_ok;
+  int32_t memv_ok, memv;  // cached check_memory of the current plan
   double bridge;
   int32_t bridge_ok;
 };
+
+// The current plan changed: task t's stage split (affects t, the generation
+// task's decoding batch via residency, and memory feasibility) ...
+__device__ __forceinline__ void invalidate_split(const DevProblem& P, Ws& s, int t) {
+  if ((threadIdx.x & 31) == 0) {
+    s.agg_ok &= ~(1 << t);
+    if (P.gen_slot >= 0) s.agg_ok &= ~(1 << P.gen_slot);
+    s.resident_ok = 0;
+    s.memv_ok = 0;
+  }
+  __syncwarp();
+}
+// ... or task t's replica weights (only t's micro-batch counts move).
+__device__ __forceinline__ void invalidate_weights(Ws& s, int t) {
+  if ((threadIdx.x & 31) == 0) s.agg_ok &= ~(1 << t);
+  __syncwarp();
+}
 
 __device__ __forceinline__ uint8_t* carve_ptr(uint8_t*& p, int bytes) {
   uint8_t* r = p;
@@ -109,6 +136,11 @@ __device__ inline void carve(Ws& s, uint8_t* base, const Carve& c) {
   s.dstage = carve_ptr(p, T * N);
   s.tour = carve_ptr(p, N);
   s.peers = carve_ptr(p, N);
+  s.mmt = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_sl));
+  s.wmt = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_sl));
+  s.wsave = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.sl_save2 = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
+  s.split_step = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
 }
 
 // ---- memory model (plan.cpp:160-220) ----
@@ -224,6 +256,15 @@ __device__ __noinline__ void apportion(const DevProblem& P, Ws& s, int t) {
   int64_t* out = s.nm + s.o.w[t];
   if (lane == 0) s.nm_base[t] = nm_base;
   const int64_t total = nm_base * dp;
+  // unit weights: wsum == dp exactly, every quota is exactly nm_base, no
+  // remainder to hand out
+  bool unit = true;
+  for (int i = lane; i < dp; i += 32) unit &= w[i] == 1.0;
+  if (__all_sync(kFull, unit)) {
+    for (int i = lane; i < dp; i += 32) out[i] = nm_base;
+    __syncwarp();
+    return;
+  }
   double wsum = 0.0;  // std::accumulate, sequential (all lanes redundantly)
   for (int i = 0; i < dp; ++i) wsum += w[i];
   // floor of quotas + remainders
@@ -288,26 +329,46 @@ __device__ inline void build_dstage(const DevProblem& P, Ws& s) {
 
 // check_memory (plan.cpp:351-380): sum of model memory in task order plus the
 // max working set, per device. Returns true when every device fits.
+// model_memory_bytes / working_memory_bytes of every stage of task t at the
+// current split (the per-device sums below only look these up).
+__device__ __forceinline__ void mem_tables(const DevProblem& P, const DevCostConfig& cfg, Ws& s,
+                                           int t) {
+  const int lane = threadIdx.x & 31;
+  const int pp = s.h.pp[t], tp = s.h.tp[t], o = s.o.sl[t];
+  __syncwarp();
+  for (int j = lane; j < pp; j += 32) {
+    s.mmt[o + j] = model_memory_bytes(P, P.task[t], s.sl[o + j], tp, j, pp, cfg);
+    s.wmt[o + j] = working_memory_bytes(P, P.task[t], s.sl[o + j], tp, cfg);
+  }
+  __syncwarp();
+}
+
 __device__ __noinline__ bool check_memory(const DevProblem& P, const DevCostConfig& cfg, Ws& s,
-                                    double* required_out = nullptr) {
+                                          double* required_out = nullptr) {
   const int lane = threadIdx.x & 31;
   const int N = P.n_dev;
+  if (!required_out && s.memv_ok) return s.memv != 0;
   bool viol = false;
   for (int d = lane; d < N; d += 32) {
     double ms = 0.0, wm = 0.0;
     for (int t = 0; t < P.n_tasks; ++t) {
       const int j = s.dstage[t * N + d];
       if (j == 0xff) continue;
-      const DevTask& tk = P.task[t];
-      const int sl_j = s.sl[s.o.sl[t] + j];
-      ms += model_memory_bytes(P, tk, sl_j, s.h.tp[t], j, s.h.pp[t], cfg);
-      wm = smax(wm, working_memory_bytes(P, tk, sl_j, s.h.tp[t], cfg));
+      ms += s.mmt[s.o.sl[t] + j];
+      wm = smax(wm, s.wmt[s.o.sl[t] + j]);
     }
     const double req = ms + wm;
     if (required_out) required_out[d] = req;
     if (req > P.mem[d]) viol = true;
   }
-  return !__any_sync(kFull, viol);
+  const bool ok = !__any_sync(kFull, viol);
+  __syncwarp();
+  if (lane == 0) {
+    s.memv = ok ? 1 : 0;
+    s.memv_ok = 1;
+  }
+  __syncwarp();
+  return ok;
 }
 
 // ---- communication primitives (cost_model.cpp:18-125, 179-218) ----
@@ -634,19 +695,16 @@ __device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8
 //
 // Leaves per-cell comp/tp/pp/hbm in s.c_* for the balancers and writes the
 // aggregate TaskCost (comp, tp, pp, dp, bubble, hbm, total) to agg[0..6].
-__device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig& cfg, Ws& s, int t,
-                                 bool use_resident, double* agg) {
+// Geometry memo of task t (independent of splits and weights): TP ring
+// bottleneck per (replica, stage) cell and cheapest cross-stage pair.
+__device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) {
   const int lane = threadIdx.x & 31;
   const DevTask& tk = P.task[t];
   const int dp = s.h.dp[t], pp = s.h.pp[t], tp = s.h.tp[t];
   const int64_t seq_total = P.seq_in + P.seq_out;
   const uint8_t* dv = s.dev + s.o.dev[t];
-  const int32_t* sl = s.sl + s.o.sl[t];
-  const int64_t* nm = s.nm + s.o.w[t];
   const int cell0 = s.o.cell[t];
   const int ncell = dp * pp;
-
-  // geometry memo: TP rings per cell, PP pairs per cell boundary
   if (tp > 1 && !((s.memo_tp_ok >> t) & 1)) {
     const double cv_tp = tp_comm_volume(tk.precision_bytes, P.mbs, seq_total, tk.h1, tp);
     class_costs(P, s, cv_tp);
@@ -679,6 +737,19 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
     if (lane == 0) s.memo_pp_ok |= 1 << t;
   }
   __syncwarp();
+}
+
+__device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig& cfg, Ws& s, int t,
+                                       bool use_resident, double* agg) {
+  const int lane = threadIdx.x & 31;
+  const DevTask& tk = P.task[t];
+  const int dp = s.h.dp[t], pp = s.h.pp[t], tp = s.h.tp[t];
+  const uint8_t* dv = s.dev + s.o.dev[t];
+  const int32_t* sl = s.sl + s.o.sl[t];
+  const int64_t* nm = s.nm + s.o.w[t];
+  const int cell0 = s.o.cell[t];
+  const int ncell = dp * pp;
+  ensure_geometry(P, s, t);
 
   const double tpf = tp_pass_factor(tk.kind, cfg.recompute != 0);
   const double ppf = pp_pass_factor(tk.kind);
@@ -817,19 +888,30 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
   const int lane = threadIdx.x & 31;
   const int N = P.n_dev;
   __syncwarp();
-  for (int d = lane; d < N; d += 32) {
-    double r = 0.0;
-    for (int t = 0; t < P.n_tasks; ++t) {
-      const int j = s.dstage[t * N + d];
-      if (j == 0xff) continue;
-      r += weights_memory_bytes(P.task[t], s.sl[s.o.sl[t] + j], s.h.tp[t], j, s.h.pp[t], cfg);
+  // weight residency per device, task order (cost_model.cpp:436-448); only the
+  // generation task's decoding batch reads it
+  const int g = P.gen_slot;
+  if (!s.resident_ok && g >= 0 && !((s.agg_ok >> g) & 1)) {
+    for (int d = lane; d < N; d += 32) {
+      double r = 0.0;
+      for (int t = 0; t < P.n_tasks; ++t) {
+        const int j = s.dstage[t * N + d];
+        if (j == 0xff) continue;
+        r += weights_memory_bytes(P.task[t], s.sl[s.o.sl[t] + j], s.h.tp[t], j, s.h.pp[t], cfg);
+      }
+      s.resident[d] = r;
     }
-    s.resident[d] = r;
+    __syncwarp();
+    if (lane == 0) s.resident_ok = 1;
+    __syncwarp();
   }
-  __syncwarp();
   double tot[kMaxTasks];
   for (int t = 0; t < P.n_tasks; ++t) {
-    task_cost(P, cfg, s, t, true, s.agg + 7 * t);
+    if (!((s.agg_ok >> t) & 1)) {
+      task_cost(P, cfg, s, t, true, s.agg + 7 * t);
+      if (lane == 0) s.agg_ok |= 1 << t;
+      __syncwarp();
+    }
     tot[t] = s.agg[7 * t + 6];
   }
   E2E r;

@@ -10,13 +10,17 @@
 namespace hpg {
 
 int eval_smem_bytes(const Carve& c);
+// global scratch (doubles) per CTA of eval_kernel
+int64_t eval_scratch_doubles(int n_dev, int64_t max_nl);
+// persistent grid size for n plans (occupancy-limited, multiple of the SMs)
+cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid);
 
 cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
                         int32_t kb_flags, const uint8_t* d_recs, const int64_t* d_off,
                         const int32_t* d_modes, int32_t uniform_mode, int n, int64_t stride,
-                        uint8_t* d_out,
-                        EvalResult* d_res, double* d_per_task, double* d_required, int n_sm,
-                        cudaStream_t st);
+                        uint8_t* d_out, EvalResult* d_res, double* d_per_task,
+                        double* d_required, double* d_scratch, int64_t scratch_doubles,
+                        int grid, cudaStream_t st);
 
 // Segmented best-half selection (search.cpp:590-620) for one SHA level.
 cudaError_t launch_best_half(const double* d_scores, const int32_t* d_seg_off,

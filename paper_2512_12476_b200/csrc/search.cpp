@@ -255,24 +255,30 @@ void medium_assignment(const Problem& P, double bias, Rng& rng, std::vector<int>
 // random_fine_assignment: node blocks (lexicographic node names) shuffled,
 // devices shuffled within a block.
 void fine_assignment(const Problem& P, const int* group_devs, int n, Rng& rng, uint8_t* out) {
-  int ranks[kMaxDevices];
-  int nr = 0;
-  for (int i = 0; i < n; ++i) {
-    const int r = P.node_rank[group_devs[i]];
-    bool seen = false;
-    for (int k = 0; k < nr; ++k) seen |= ranks[k] == r;
-    if (!seen) ranks[nr++] = r;
+  // bucket the group's devices by node (insertion order kept), nodes listed
+  // in lexicographic name order = ascending node rank
+  int cnt[kMaxDevices];
+  const int R = P.n_nodes;
+  for (int r = 0; r < R; ++r) cnt[r] = 0;
+  for (int i = 0; i < n; ++i) ++cnt[P.node_rank[group_devs[i]]];
+  int ranks[kMaxDevices], start[kMaxDevices];
+  int nr = 0, acc = 0;
+  for (int r = 0; r < R; ++r) {
+    if (!cnt[r]) continue;
+    ranks[nr++] = r;
+    start[r] = acc;
+    acc += cnt[r];
   }
-  std::sort(ranks, ranks + nr);
+  int bucket[kMaxDevices], fill[kMaxDevices];
+  for (int k = 0; k < nr; ++k) fill[ranks[k]] = start[ranks[k]];
+  for (int i = 0; i < n; ++i) bucket[fill[P.node_rank[group_devs[i]]]++] = group_devs[i];
   rng.shuffle(ranks, nr);
   int pos = 0;
-  int bucket[kMaxDevices];
   for (int k = 0; k < nr; ++k) {
-    int nb = 0;
-    for (int i = 0; i < n; ++i)
-      if (P.node_rank[group_devs[i]] == ranks[k]) bucket[nb++] = group_devs[i];
-    rng.shuffle(bucket, nb);
-    for (int i = 0; i < nb; ++i) out[pos++] = static_cast<uint8_t>(bucket[i]);
+    int* b = bucket + start[ranks[k]];
+    const int nb = cnt[ranks[k]];
+    rng.shuffle(b, nb);
+    for (int i = 0; i < nb; ++i) out[pos++] = static_cast<uint8_t>(b[i]);
   }
 }
 
@@ -309,14 +315,36 @@ void make_candidate(const ArmEnv& e, int64_t combo, Rng& rng, Cand& c) {
   }
 }
 
-// group_device_set (search.cpp:336-341): devices of the group's first task in
-// lexicographic device-id order
-void group_device_set(const ArmEnv& e, const Cand& c, size_t g, int* out, int& n) {
+// group_device_set (search.cpp:336-341) is the group's device set sorted by
+// device-id string; kept as a bitmask in id-rank space so the idx-th entry is
+// a select over four words instead of a sort.
+struct RankSet {
+  uint64_t w[kMaxDevices / 64];
+};
+
+void group_rank_set(const ArmEnv& e, const Cand& c, size_t g, RankSet& rs, int& n) {
   const int s = e.tg[g].front();
   n = c.size(s);
+  for (auto& x : rs.w) x = 0;
   const uint8_t* d = c.dev() + c.o.dev[s];
-  for (int i = 0; i < n; ++i) out[i] = d[i];
-  std::sort(out, out + n, [&](int a, int b) { return e.P.id_rank[a] < e.P.id_rank[b]; });
+  for (int i = 0; i < n; ++i) {
+    const int r = e.P.id_rank[d[i]];
+    rs.w[r >> 6] |= 1ull << (r & 63);
+  }
+}
+
+int select_rank(const ArmEnv& e, const RankSet& rs, uint64_t idx) {
+  for (int k = 0; k < kMaxDevices / 64; ++k) {
+    const uint64_t pc = static_cast<uint64_t>(__builtin_popcountll(rs.w[k]));
+    if (idx >= pc) {
+      idx -= pc;
+      continue;
+    }
+    uint64_t x = rs.w[k];
+    for (uint64_t i = 0; i < idx; ++i) x &= x - 1;
+    return e.P.by_id_rank[64 * k + __builtin_ctzll(x)];
+  }
+  return -1;
 }
 
 bool random_move(const ArmEnv& e, Cand& c, int level, Rng& rng) {
@@ -326,14 +354,14 @@ bool random_move(const ArmEnv& e, Cand& c, int level, Rng& rng) {
     const size_t g1 = rng.bounded(ng);
     size_t g2 = rng.bounded(ng - 1);
     if (g2 >= g1) ++g2;
-    int d1[kMaxDevices], d2[kMaxDevices];
+    RankSet d1, d2;
     int n1, n2;
-    group_device_set(e, c, g1, d1, n1);
-    group_device_set(e, c, g2, d2, n2);
+    group_rank_set(e, c, g1, d1, n1);
+    group_rank_set(e, c, g2, d2, n2);
     // GCC evaluates the two bounded() arguments right to left
     // (search.cpp:378-379): the d2 index is drawn first.
-    const int b = d2[rng.bounded(static_cast<uint64_t>(n2))];
-    const int a = d1[rng.bounded(static_cast<uint64_t>(n1))];
+    const int b = select_rank(e, d2, rng.bounded(static_cast<uint64_t>(n2)));
+    const int a = select_rank(e, d1, rng.bounded(static_cast<uint64_t>(n1)));
     for (int s : e.tg[g1]) {
       uint8_t* d = c.dev() + c.o.dev[s];
       for (int i = 0; i < c.size(s); ++i)
@@ -603,12 +631,14 @@ void run_lockstep(Ctx& ctx, const Knobs& K, std::vector<ArmRun*>& runs, double& 
                   int64_t& waves) {
   const DevCostConfig cfg = K.cost_config();
   const int kb = (K.balance_data ? 1 : 0) | (K.balance_layers ? 2 : 0);
+  double th = now_s();
   for (ArmRun* r : runs) {
     r->clock = &clock;
     r->coro = ga_run(*r);
     r->coro.h.resume();
     if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
   }
+  ctx.host_ms += 1e3 * (now_s() - th);
   Batch b;
   BatchOut bo;
   std::vector<std::pair<ArmRun*, int>> owners;
@@ -627,9 +657,11 @@ void run_lockstep(Ctx& ctx, const Knobs& K, std::vector<ArmRun*>& runs, double& 
       owners.emplace_back(r, static_cast<int>(q->cands.size()));
     }
     if (owners.empty()) break;
+    const double tb = now_s();
     run_batch(ctx, b, cfg, kb, true, false, false, bo);
     ++waves;
     clock = now_s();
+    ctx.batch_ms += 1e3 * (clock - tb);
     size_t k = 0;
     for (auto& [r, cnt] : owners) {
       EvalReq* q = r->coro.h.promise().pending;
@@ -645,6 +677,7 @@ void run_lockstep(Ctx& ctx, const Knobs& K, std::vector<ArmRun*>& runs, double& 
       r->coro.h.resume();
       if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
     }
+    ctx.host_ms += 1e3 * (now_s() - clock);
   }
 }
 
@@ -732,7 +765,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   const int64_t launches0 = ctx.launches, plans0 = ctx.plans_evaluated;
   const int64_t h2d0 = ctx.h2d_bytes, d2h0 = ctx.d2h_bytes, el0 = ctx.eval_launches,
                 cb0 = ctx.canonical_bytes;
-  const double ems0 = ctx.eval_ms;
+  const double ems0 = ctx.eval_ms, hms0 = ctx.host_ms, bms0 = ctx.batch_ms;
   const Rng base_rng(K.seed);
   SearchOut S;
   S.budget = K.budget;
@@ -990,6 +1023,8 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   S.eval_launches = ctx.eval_launches - el0;
   S.canonical_bytes = ctx.canonical_bytes - cb0;
   S.eval_ms = ctx.eval_ms - ems0;
+  S.host_ms = ctx.host_ms - hms0;
+  S.batch_ms = ctx.batch_ms - bms0;
   return S;
 }
 

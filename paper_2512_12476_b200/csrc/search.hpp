@@ -78,7 +78,7 @@ struct SearchOut {
   double wall_s = 0, time_to_best_s = 0;
   int64_t launches = 0, waves = 0, plans_gpu = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0, eval_launches = 0, canonical_bytes = 0;
-  double eval_ms = 0.0;
+  double eval_ms = 0.0, host_ms = 0.0, batch_ms = 0.0;
 };
 
 // Multi-GPU: per-arm records all-gathered across ranks after every round.

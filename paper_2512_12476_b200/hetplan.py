@@ -143,7 +143,8 @@ class _SearchInfo(C.Structure):
                 ("gpu_launches", C.c_int64), ("waves", C.c_int64),
                 ("plans_evaluated_gpu", C.c_int64), ("h2d_bytes", C.c_int64),
                 ("d2h_bytes", C.c_int64), ("eval_kernel_ms", C.c_double),
-                ("eval_launches", C.c_int64), ("canonical_bytes", C.c_int64)]
+                ("eval_launches", C.c_int64), ("canonical_bytes", C.c_int64),
+                ("host_ms", C.c_double), ("batch_ms", C.c_double)]
 
 
 class _SweepStats(C.Structure):
