@@ -970,6 +970,18 @@ int main(int argc, char** argv) {
   };
   try {
     if (cmd == "fixtures") return cmd_fixtures(arg(2));
+    if (cmd == "rngpin") {  // same lines as tests/host_units.cpp prints
+      const uint64_t seed = std::stoull(arg(2));
+      Rng s(seed);
+      const uint64_t a = s.next(), b = s.next(), c = s.next();
+      std::printf("draws %" PRIu64 " %" PRIu64 " %" PRIu64 "\n", a, b, c);
+      Rng f = Rng(seed).fork(7);
+      const uint64_t x = f.next();
+      const uint64_t y = f.bounded(100);
+      const double z = f.uniform();
+      std::printf("fork7 %" PRIu64 " bounded100 %" PRIu64 " uniform %.17g\n", x, y, z);
+      return 0;
+    }
     if (cmd == "evalplans")
       return cmd_evalplans(arg(2), arg(3), std::stoull(arg(4)), std::stoi(arg(5)), arg(6));
     if (cmd == "fuzz") return cmd_fuzz(std::stoull(arg(2)), std::stoi(arg(3)), arg(4));

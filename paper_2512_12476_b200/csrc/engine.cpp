@@ -9,6 +9,7 @@
 #include <numeric>
 
 #include "eval_launch.hpp"
+#include "host_pool.hpp"
 
 namespace hpg {
 
@@ -364,11 +365,11 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   ctx.h_off.reserve(n);
   ctx.h_modes.reserve(n);
   ctx.h_res.reserve(n);
-  for (int i = 0; i < n; ++i) {
+host_parallel_for(n, n >= 4096, [&](int i) {
     std::memcpy(ctx.h_recs.p + out.off[i], b.cands[i]->rec.data(), b.cands[i]->o.bytes);
     ctx.h_off.p[i] = out.off[i];
     ctx.h_modes.p[i] = b.modes[i];
-  }
+  });
   ctx.d_recs.reserve(total);
   ctx.d_off.reserve(n);
   ctx.d_modes.reserve(n);

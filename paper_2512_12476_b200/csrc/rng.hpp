@@ -12,6 +12,34 @@
 
 namespace hpg {
 
+#ifndef __CUDA_ARCH__
+// Exact 64-bit remainder by a precomputed 128-bit reciprocal (Lemire,
+// Kaser & Kurz, "Faster remainder by direct computation", 2019): for every
+// 64-bit a and d >= 1, fastmod(a) == a % d. Replaces the hardware divide in
+// the host-side candidate generator (thousands of bounded() draws per
+// candidate); results are identical by construction and checked in
+// tests/test_host_units.py.
+struct FastModTable {
+  static constexpr int kMax = 1024;
+  unsigned __int128 m[kMax + 1];
+  FastModTable() {
+    m[0] = 0;
+    for (int d = 1; d <= kMax; ++d) m[d] = ~static_cast<unsigned __int128>(0) / d + 1;
+  }
+};
+inline const FastModTable& fastmod_table() {
+  static const FastModTable t;
+  return t;
+}
+inline uint64_t fastmod_u64(uint64_t a, unsigned __int128 M, uint64_t d) {
+  const unsigned __int128 low = M * a;
+  unsigned __int128 bottom = (low & 0xFFFFFFFFFFFFFFFFull) * d;
+  bottom >>= 64;
+  const unsigned __int128 top = (low >> 64) * d;
+  return static_cast<uint64_t>((bottom + top) >> 64);
+}
+#endif
+
 HPG_HD uint64_t mix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ULL;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -43,7 +71,12 @@ struct Rng {
     s[3] = rotl(s[3], 45);
     return result;
   }
-  HPG_HD uint64_t bounded(uint64_t n) { return next() % n; }
+  HPG_HD uint64_t bounded(uint64_t n) {
+#ifndef __CUDA_ARCH__
+    if (n <= FastModTable::kMax) return fastmod_u64(next(), fastmod_table().m[n], n);
+#endif
+    return next() % n;
+  }
   HPG_HD double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
   HPG_HD double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
   // Rng::fork (rng.hpp:64): derived from the original seed, not the state.

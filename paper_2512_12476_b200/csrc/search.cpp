@@ -16,6 +16,7 @@
 #include <set>
 
 #include "eval_launch.hpp"
+#include "host_pool.hpp"
 
 namespace hpg {
 
@@ -632,16 +633,22 @@ void run_lockstep(Ctx& ctx, const Knobs& K, std::vector<ArmRun*>& runs, double& 
   const DevCostConfig cfg = K.cost_config();
   const int kb = (K.balance_data ? 1 : 0) | (K.balance_layers ? 2 : 0);
   double th = now_s();
-  for (ArmRun* r : runs) {
+  // arms are independent: their GA steps (candidate generation, population
+  // bookkeeping) run on a host thread pool; only the GPU wave is shared
+  const int nr = static_cast<int>(runs.size());
+host_parallel_for(nr, nr >= 16, [&](int i) {
+    ArmRun* r = runs[i];
     r->clock = &clock;
     r->coro = ga_run(*r);
     r->coro.h.resume();
+  });
+  for (ArmRun* r : runs)
     if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
-  }
   ctx.host_ms += 1e3 * (now_s() - th);
   Batch b;
   BatchOut bo;
   std::vector<std::pair<ArmRun*, int>> owners;
+  std::vector<size_t> first;
   while (true) {
     b.cands.clear();
     b.modes.clear();
@@ -662,21 +669,29 @@ void run_lockstep(Ctx& ctx, const Knobs& K, std::vector<ArmRun*>& runs, double& 
     ++waves;
     clock = now_s();
     ctx.batch_ms += 1e3 * (clock - tb);
+    first.resize(owners.size());
     size_t k = 0;
-    for (auto& [r, cnt] : owners) {
+    for (size_t o = 0; o < owners.size(); ++o) {
+      first[o] = k;
+      k += owners[o].second;
+    }
+    const int no = static_cast<int>(owners.size());
+    host_parallel_for(no, no >= 16, [&](int o) {
+      ArmRun* r = owners[o].first;
+      const int cnt = owners[o].second;
       EvalReq* q = r->coro.h.promise().pending;
       q->res.resize(cnt);
-      for (int i = 0; i < cnt; ++i, ++k) {
-        q->res[i] = bo.res[k];
+      for (int i = 0; i < cnt; ++i) {
+        const size_t kk = first[o] + i;
+        q->res[i] = bo.res[kk];
         Cand& c = q->cands[i];
-        std::memcpy(c.rec.data(), bo.out_recs->p + bo.off[k], c.o.bytes);
+        std::memcpy(c.rec.data(), bo.out_recs->p + bo.off[kk], c.o.bytes);
       }
       r->coro.h.promise().pending = nullptr;
-    }
-    for (auto& [r, cnt] : owners) {
       r->coro.h.resume();
+    });
+    for (auto& [r, cnt] : owners)
       if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
-    }
     ctx.host_ms += 1e3 * (now_s() - clock);
   }
 }
