@@ -170,8 +170,8 @@ HPG_HD int carve_bytes(const Carve& c) {
 }
 
 HPG_HD int carve2_bytes(const Carve& c) {
-  return carve_bytes(c) + 2 * carve_round(8 * c.max_sl) + carve_round(8 * c.n_dev) +
-         carve_round(4 * c.max_sl) + carve_round(4 * c.n_dev);
+  return carve_bytes(c) + carve_round(8 * c.max_cells) + 2 * carve_round(8 * c.max_sl) +
+         carve_round(8 * c.n_dev) + carve_round(4 * c.max_sl) + carve_round(4 * c.n_dev);
 }
 
 }  // namespace hpg

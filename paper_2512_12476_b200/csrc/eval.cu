@@ -86,24 +86,11 @@ __device__ __forceinline__ void cell_pieces(const DevProblem& P, const DevCostCo
   const uint8_t* dv = s.dev + s.o.dev[c.t];
   const int64_t nmi = s.nm[s.o.w[c.t] + i];
   const int cell = i * c.pp + j;
-  double comp = 0.0, hbm = 0.0;
-  for (int k = 0; k < c.tp; ++k) {
-    const int d = dv[cell * c.tp + k];
-    comp = smax(comp, compute_cost(c.kind, nmi, P.mbs, nl_j, c.flops, P.comp[d], c.tp));
-    if (c.do_hbm) {
-      double dbs = cfg.dbs_override;
-      if (dbs <= 0) {
-        const double kv_seq = kv_bytes_per_sequence(P, tk, nl_j, c.tp, cfg);
-        const double res = weights_memory_bytes(tk, nl_j, c.tp, j, c.pp, cfg);
-        const double free_bytes = P.mem[d] - res;
-        dbs = floor(free_bytes / kv_seq);
-        const double hi = static_cast<double>(nmi * P.mbs);
-        dbs = (dbs < 1.0) ? 1.0 : ((hi < dbs) ? hi : dbs);
-      }
-      hbm = smax(hbm, hbm_decode_cost(P.seq_out, nmi, P.mbs, tk.precision_bytes, nl_j, tk.h1,
-                                      tk.h2, dbs, P.hbm[d], c.tp));
-    }
-  }
+  const double comp = smax(0.0, compute_cost(c.kind, nmi, P.mbs, nl_j, c.flops,
+                                             s.cmin[s.o.cell[c.t] + cell], c.tp));
+  const double hbm =
+      c.do_hbm ? smax(0.0, hbm_cell(P, cfg, s, tk, dv + cell * c.tp, c.tp, j, c.pp, nmi, nl_j, false))
+               : 0.0;
   const double tpc = c.tp > 1 ? c.tpf * static_cast<double>(nmi) * static_cast<double>(nl_j) *
                                     s.rtp[s.o.cell[c.t] + cell]
                               : 0.0;
@@ -133,6 +120,16 @@ __device__ double trial_total(const DevProblem& P, const DevCostConfig& cfg, con
   const DevTask& tk = P.task[c.t];
   const uint8_t* dv = s.dev + s.o.dev[c.t];
   const int size = c.dp * c.pp * c.tp;
+  // task t's per-stage memory at the trial split (stages are few in the exact
+  // regime; large greedy pipelines fall back to per-device evaluation)
+  double mmj[8], wmj[8];
+  const bool tab = c.pp <= 8;
+  if (tab) {
+    for (int j = 0; j < c.pp; ++j) {
+      mmj[j] = model_memory_bytes(P, tk, sp[j], c.tp, j, c.pp, cfg);
+      wmj[j] = working_memory_bytes(P, tk, sp[j], c.tp, cfg);
+    }
+  }
   for (int e = 0; e < size; ++e) {
     const int d = dv[e];
     const int j = (e / c.tp) % c.pp;
@@ -141,8 +138,8 @@ __device__ double trial_total(const DevProblem& P, const DevCostConfig& cfg, con
     for (int u = 0; u < P.n_tasks; ++u) {
       double m, w;
       if (u == c.t) {
-        m = model_memory_bytes(P, tk, L, c.tp, j, c.pp, cfg);
-        w = working_memory_bytes(P, tk, L, c.tp, cfg);
+        m = tab ? mmj[j] : model_memory_bytes(P, tk, L, c.tp, j, c.pp, cfg);
+        w = tab ? wmj[j] : working_memory_bytes(P, tk, L, c.tp, cfg);
       } else {
         const int jj = s.dstage[u * N + d];
         if (jj == 0xff) continue;
@@ -512,6 +509,7 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
       rec_offsets(s.h, s.o);
       s.memo_tp_ok = 0;
       s.memo_pp_ok = 0;
+      s.memo_cm_ok = 0;
       s.bridge_ok = 0;
       s.agg_ok = 0;
       s.resident_ok = 0;

@@ -51,6 +51,7 @@ struct Ws {
   // memo
   double* rtp;       // [cells] TP ring bottleneck per (task, replica, stage)
   double* ppp;       // [cells] cheapest cross-stage pair per (task, replica, stage)
+  double* cmin;      // [cells] min over the cell's shards of Device::comp
   double* dpr;       // [dpk]   DP ring per (task, stage, shard)
   int32_t* dpr_sl;   // [dpk]   stage layers the DP memo was computed for
   // scratch
@@ -79,6 +80,7 @@ struct Ws {
   int64_t nm_base[kMaxTasks];
   int32_t memo_tp_ok;   // bit t
   int32_t memo_pp_ok;
+  int32_t memo_cm_ok;
   int32_t agg_ok;       // bit t: agg row t is end_to_end's task_cost for the current plan
   int32_t resident_ok;
   int32_t memv_ok, memv;  // cached check_memory of the current plan
@@ -136,6 +138,7 @@ __device__ inline void carve(Ws& s, uint8_t* base, const Carve& c) {
   s.dstage = carve_ptr(p, T * N);
   s.tour = carve_ptr(p, N);
   s.peers = carve_ptr(p, N);
+  s.cmin = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_cells));
   s.mmt = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_sl));
   s.wmt = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_sl));
   s.wsave = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
@@ -395,14 +398,14 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
   for (int e = lane; e < n * n; e += 32) s.rm[e] = ecost(P, s, devs[e / n], devs[e % n]);
   __syncwarp();
   const double* rm = s.rm;
-  double ub = 0.0;
-  for (int i = 0; i < n; ++i) ub = smax(ub, rm[i * n + (i + 1) % n]);
-  double lb = 0.0;
-  for (int v = 0; v < n; ++v) {
+  // lane v: its identity-tour edge (UB) and its 2nd-cheapest incident edge (LB)
+  double ub = 0.0, lb = 0.0;
+  if (lane < n) {
+    ub = rm[lane * n + (lane + 1) % n];
     double m1 = kInf, m2 = kInf;
     for (int u = 0; u < n; ++u) {
-      if (u == v) continue;
-      const double c = rm[v * n + u];
+      if (u == lane) continue;
+      const double c = rm[lane * n + u];
       if (c < m1) {
         m2 = m1;
         m1 = c;
@@ -410,8 +413,10 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
         m2 = c;
       }
     }
-    lb = smax(lb, m2);
+    lb = m2;
   }
+  ub = warp_max(ub);
+  lb = warp_max(lb);
   if (ub == lb) return ub;
   double best = ub;
   const int m = n - 1;
@@ -695,6 +700,40 @@ __device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8
 //
 // Leaves per-cell comp/tp/pp/hbm in s.c_* for the balancers and writes the
 // aggregate TaskCost (comp, tp, pp, dp, bubble, hbm, total) to agg[0..6].
+// HBM decode cost of one generation cell (cost_model.cpp:315-337): max over
+// the cell's shards of hbm_decode_cost. The shards share the numerator, so
+// the max is the numerator over the smallest denominator (dbs*hbm_d)*tp
+// (IEEE division is monotone); dbs per shard from the free memory after the
+// resident weights (whole-plan residency, or the task's own weights).
+__device__ __forceinline__ double hbm_cell(const DevProblem& P, const DevCostConfig& cfg,
+                                           const Ws& s, const DevTask& tk, const uint8_t* shards,
+                                           int tp, int j, int pp, int64_t nmi, int nl_j,
+                                           bool use_resident) {
+  const double weight_bytes =
+      static_cast<double>(tk.precision_bytes) * static_cast<double>(nl_j) *
+      (4.0 * static_cast<double>(tk.h1) * static_cast<double>(tk.h1) +
+       3.0 * static_cast<double>(tk.h1) * static_cast<double>(tk.h2));
+  const double num = static_cast<double>(P.seq_out) * static_cast<double>(nmi) *
+                     static_cast<double>(P.mbs) * weight_bytes;
+  double den = kInf;
+  if (cfg.dbs_override > 0) {
+    for (int k = 0; k < tp; ++k) den = smin(den, cfg.dbs_override * P.hbm[shards[k]] * tp);
+  } else {
+    const double kv_seq = kv_bytes_per_sequence(P, tk, nl_j, tp, cfg);
+    const double own = use_resident ? 0.0 : weights_memory_bytes(tk, nl_j, tp, j, pp, cfg);
+    const double hi = static_cast<double>(nmi * P.mbs);
+    for (int k = 0; k < tp; ++k) {
+      const int d = shards[k];
+      const double res = use_resident ? s.resident[d] : own;
+      const double free_bytes = P.mem[d] - res;
+      double dbs = floor(free_bytes / kv_seq);
+      dbs = (dbs < 1.0) ? 1.0 : ((hi < dbs) ? hi : dbs);  // std::clamp
+      den = smin(den, dbs * P.hbm[d] * tp);
+    }
+  }
+  return num / den;
+}
+
 // Geometry memo of task t (independent of splits and weights): TP ring
 // bottleneck per (replica, stage) cell and cheapest cross-stage pair.
 __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) {
@@ -705,6 +744,19 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
   const uint8_t* dv = s.dev + s.o.dev[t];
   const int cell0 = s.o.cell[t];
   const int ncell = dp * pp;
+  if (!((s.memo_cm_ok >> t) & 1)) {
+    // compute_cost is x / (comp_d * tp) with x >= 0: IEEE multiplication and
+    // division are monotone, so the max over a cell's shards
+    // (cost_model.cpp:310-314) is attained at the slowest device
+    for (int c = lane; c < ncell; c += 32) {
+      double m = P.comp[dv[c * tp]];
+      for (int k = 1; k < tp; ++k) m = smin(m, P.comp[dv[c * tp + k]]);
+      s.cmin[cell0 + c] = m;
+    }
+    __syncwarp();
+    if (lane == 0) s.memo_cm_ok |= 1 << t;
+    __syncwarp();
+  }
   if (tp > 1 && !((s.memo_tp_ok >> t) & 1)) {
     const double cv_tp = tp_comm_volume(tk.precision_bytes, P.mbs, seq_total, tk.h1, tp);
     class_costs(P, s, cv_tp);
@@ -761,25 +813,12 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
     const int i = c / pp, j = c % pp;
     const int64_t nmi = nm[i];
     const int64_t nl_j = sl[j];
-    double comp = 0.0, hbm = 0.0;
-    for (int k = 0; k < tp; ++k) {
-      const int d = dv[c * tp + k];
-      comp = smax(comp, compute_cost(tk.kind, nmi, P.mbs, nl_j, flops, P.comp[d], tp));
-      if (do_hbm) {
-        double dbs = cfg.dbs_override;
-        if (dbs <= 0) {
-          const double kv_seq = kv_bytes_per_sequence(P, tk, static_cast<int>(nl_j), tp, cfg);
-          const double res = use_resident
-                                 ? s.resident[d]
-                                 : weights_memory_bytes(tk, static_cast<int>(nl_j), tp, j, pp, cfg);
-          const double free_bytes = P.mem[d] - res;
-          dbs = floor(free_bytes / kv_seq);
-          const double hi = static_cast<double>(nmi * P.mbs);
-          dbs = (dbs < 1.0) ? 1.0 : ((hi < dbs) ? hi : dbs);  // std::clamp
-        }
-        hbm = smax(hbm, hbm_decode_cost(P.seq_out, nmi, P.mbs, tk.precision_bytes, nl_j, tk.h1,
-                                        tk.h2, dbs, P.hbm[d], tp));
-      }
+    const double comp =
+        smax(0.0, compute_cost(tk.kind, nmi, P.mbs, nl_j, flops, s.cmin[cell0 + c], tp));
+    double hbm = 0.0;
+    if (do_hbm) {
+      hbm = smax(0.0, hbm_cell(P, cfg, s, tk, dv + c * tp, tp, j, pp, nmi,
+                                static_cast<int>(nl_j), use_resident));
     }
     s.c_comp[c] = comp;
     s.c_hbm[c] = hbm;
