@@ -29,7 +29,7 @@ NcclApi& api() {
   if (a.lib) return a;
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
   for (const char* n : names) {
-    a.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    a.lib = dlopen(n, RTLD_NOW | RTLD_LOCAL);
     if (a.lib) break;
   }
   if (!a.lib) throw InternalError("multi-GPU search needs NCCL (libnccl.so.2 not found)");

@@ -475,6 +475,7 @@ struct ArmRun {
   std::unique_ptr<ArmEnv> env;
   ArmCoro coro;
   double* clock = nullptr;
+  int owner = 0;  // rank that runs it (multi-GPU)
 };
 
 // ga_run (search.cpp:437-565) as a coroutine.
@@ -770,6 +771,73 @@ struct TgArm {
   std::vector<int64_t> rec;
 };
 
+// ---- multi-GPU: per-run records all-gathered after every lockstep round ----
+
+struct RunSummary {
+  int64_t used;
+  double best;
+  int64_t n_impr;
+  int64_t pad;
+};
+struct ImprRec {
+  int64_t run;
+  int64_t local_idx;
+  double cost;
+};
+
+template <typename T>
+std::vector<T> allgather_host(Ctx& ctx, Dist& d, const std::vector<T>& mine) {
+  const size_t bytes = sizeof(T) * mine.size();
+  DevBuf<uint8_t>& snd = ctx.d_xch_send;
+  DevBuf<uint8_t>& rcv = ctx.d_xch_recv;
+  snd.reserve(bytes + 8);
+  rcv.reserve(bytes * d.world + 8);
+  std::vector<T> out(mine.size() * d.world);
+  if (bytes == 0) return out;
+  cuda_check(cudaMemcpyAsync(snd.p, mine.data(), bytes, cudaMemcpyHostToDevice, ctx.stream), "H2D");
+  dist_allgather(d, snd.p, rcv.p, bytes, ctx.stream);
+  cuda_check(cudaMemcpyAsync(out.data(), rcv.p, bytes * d.world, cudaMemcpyDeviceToHost,
+                             ctx.stream), "D2H");
+  cuda_check(cudaStreamSynchronize(ctx.stream), "allgather");
+  ctx.h2d_bytes += static_cast<int64_t>(bytes);
+  ctx.d2h_bytes += static_cast<int64_t>(bytes * d.world);
+  return out;
+}
+
+// Every rank ends with identical (used, best, improvement list) for every run
+// of the round; improvement plans stay with the owning rank.
+void exchange_runs(Ctx& ctx, Dist& d, std::vector<ArmRun*>& all, double now) {
+  const int R = static_cast<int>(all.size());
+  std::vector<RunSummary> s(R, RunSummary{0, 0.0, 0, 0});
+  std::vector<ImprRec> imp;
+  for (int r = 0; r < R; ++r) {
+    if (r % d.world != d.rank) continue;
+    s[r] = RunSummary{all[r]->used, all[r]->best, static_cast<int64_t>(all[r]->impr.size()), 0};
+    for (const auto& im : all[r]->impr) imp.push_back(ImprRec{r, im.local_idx, im.cost});
+  }
+  const std::vector<RunSummary> gs = allgather_host(ctx, d, s);
+  std::vector<int64_t> cnt{static_cast<int64_t>(imp.size())};
+  const std::vector<int64_t> gc = allgather_host(ctx, d, cnt);
+  const int64_t mx = *std::max_element(gc.begin(), gc.end());
+  imp.resize(mx, ImprRec{-1, 0, 0.0});
+  const std::vector<ImprRec> gi = allgather_host(ctx, d, imp);
+  for (int r = 0; r < R; ++r) {
+    const int owner = r % d.world;
+    if (owner == d.rank) continue;
+    const RunSummary& x = gs[static_cast<size_t>(owner) * R + r];
+    all[r]->used = x.used;
+    all[r]->best = x.best;
+    all[r]->impr.clear();
+  }
+  for (int k = 0; k < d.world; ++k) {
+    if (k == d.rank) continue;
+    for (int64_t e = 0; e < gc[k]; ++e) {
+      const ImprRec& ir = gi[static_cast<size_t>(k) * mx + e];
+      all[ir.run]->impr.push_back(Improvement{ir.local_idx, ir.cost, Cand{}, now});
+    }
+  }
+}
+
 }  // namespace
 
 SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
@@ -834,6 +902,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
 
   double incumbent = kInf;
   Cand inc_plan;
+  int inc_owner = 0;
   int64_t inc_ti = -1, inc_gi = -1;
   double inc_time = t0;
   int64_t consumed = 0;
@@ -914,7 +983,19 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
           }
         }
       }
-      run_lockstep(ctx, K, batch, clock, waves);
+      if (dist && dist->world > 1) {
+        // runs dealt round-robin over ranks (balanced by count; every run of
+        // one (task grouping, round) has the same slice), then all-gathered
+        std::vector<ArmRun*> mine;
+        for (size_t r = 0; r < batch.size(); ++r) {
+          batch[r]->owner = static_cast<int>(r % dist->world);
+          if (batch[r]->owner == dist->rank) mine.push_back(batch[r]);
+        }
+        run_lockstep(ctx, K, mine, clock, waves);
+        exchange_runs(ctx, *dist, batch, clock);
+      } else {
+        run_lockstep(ctx, K, batch, clock, waves);
+      }
       // fold run results into the arm records
       for (auto& p : ps) {
         if (n >= p.rounds) continue;
@@ -980,6 +1061,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
             if (im.cost < incumbent) {
               incumbent = im.cost;
               inc_plan = im.plan;
+              inc_owner = r->owner;
               inc_ti = r->ti;
               inc_gi = r->gi;
               inc_time = im.t_wall;
@@ -1010,6 +1092,20 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   }
   S.consumed = consumed;
   if (consumed > K.budget) throw InternalError("search overspent its budget");
+  if (inc_ti >= 0 && dist && dist->world > 1) {
+    // the incumbent's plan lives on the rank that evaluated it
+    std::vector<int64_t> sz{dist->rank == inc_owner ? static_cast<int64_t>(inc_plan.rec.size())
+                                                    : 0};
+    const std::vector<int64_t> gsz = allgather_host(ctx, *dist, sz);
+    const int64_t bytes = gsz[inc_owner];
+    std::vector<uint8_t> mine(bytes, 0);
+    if (dist->rank == inc_owner) std::memcpy(mine.data(), inc_plan.rec.data(), bytes);
+    const std::vector<uint8_t> all = allgather_host(ctx, *dist, mine);
+    inc_plan.rec.assign(all.begin() + static_cast<int64_t>(inc_owner) * bytes,
+                        all.begin() + static_cast<int64_t>(inc_owner + 1) * bytes);
+    rec_offsets(inc_plan.hdr(), inc_plan.o);
+    inc_plan.ng = static_cast<int>(arms[inc_ti].tg.size());
+  }
   if (inc_ti >= 0) {
     S.has_plan = true;
     S.plan = inc_plan;
