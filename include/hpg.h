@@ -165,6 +165,9 @@ void hpg_knobs_default(hpg_knobs* knobs);             /* SearchKnobs{} */
 int hpg_create(const hpg_problem* problem, int cuda_device, hpg_ctx** out, char* err,
                size_t errlen);
 void hpg_destroy(hpg_ctx* ctx);
+/* Re-validates and re-uploads a (possibly different) problem into an existing
+ * context, keeping its device buffers, streams and NCCL communicator. */
+int hpg_restage(hpg_ctx* ctx, const hpg_problem* problem, char* err, size_t errlen);
 
 /* DeviceTopology::max_devices_per_node (topology.hpp:79) */
 int hpg_max_devices_per_node(const hpg_ctx* ctx);
@@ -196,7 +199,9 @@ int hpg_search(hpg_ctx* ctx, const hpg_knobs* knobs, hpg_search_result** out, ch
 /* Multi-GPU: one context per rank, same problem and knobs on every rank; the
  * arms of every halving round are sharded across ranks and per-arm records
  * are all-gathered (NCCL) after each round. nccl_id is the 128-byte
- * ncclUniqueId produced by hpg_nccl_unique_id on rank 0 and broadcast. */
+ * ncclUniqueId produced by hpg_nccl_unique_id on rank 0 and broadcast; it is
+ * consumed by the first sharded search of the context (the communicator is
+ * kept and reused; later ids are ignored unless rank/world change). */
 int hpg_nccl_unique_id(uint8_t id_out[128], char* err, size_t errlen);
 int hpg_search_dist(hpg_ctx* ctx, const hpg_knobs* knobs, int rank, int world,
                     const uint8_t nccl_id[128], hpg_search_result** out, char* err,

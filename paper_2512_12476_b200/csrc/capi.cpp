@@ -101,6 +101,14 @@ int hpg_max_devices_per_node(const hpg_ctx* ctx) {
   return ctx && ctx->impl ? ctx->impl->prob.max_node_size : -1;
 }
 
+int hpg_restage(hpg_ctx* ctx, const hpg_problem* problem, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    check_ctx(ctx);
+    if (!problem) throw UsageError("hpg_restage: null problem");
+    restage(*ctx->impl, *problem);
+  });
+}
+
 int hpg_link(const hpg_ctx* ctx, int a, int b, double* latency_s, double* bandwidth_bps) {
   if (!ctx || !ctx->impl) return HPG_USAGE;
   const Problem& P = ctx->impl->prob;

@@ -92,11 +92,8 @@ struct SweepHost {
   void* blob = nullptr;
 };
 
-std::map<Ctx*, SweepHost> g_sweep;
-
 SweepTablesDev& sweep_tables(Ctx& C) {
-  auto it = g_sweep.find(&C);
-  if (it != g_sweep.end()) return it->second.tb;
+  if (C.d_sweep_tables) return C.sweep_tb;
   const Problem& P = C.prob;
   if (P.N < P.T) throw InputError("sweep needs at least as many devices as workflow tasks");
   const auto tgs = enumerate_task_groupings(P, false);
@@ -151,7 +148,9 @@ SweepTablesDev& sweep_tables(Ctx& C) {
   h.tb.tg_ng = reinterpret_cast<const int8_t*>(b + o_ng);
   h.tb.opt_off = reinterpret_cast<const int32_t*>(b + o_off);
   h.tb.opt = reinterpret_cast<const int16_t*>(b + o_opt);
-  return g_sweep.emplace(&C, h).first->second.tb;
+  C.d_sweep_tables = h.blob;
+  C.sweep_tb = h.tb;
+  return C.sweep_tb;
 }
 
 struct SweepAcc {
@@ -278,15 +277,13 @@ int hpg_search_dist(hpg_ctx* ctx, const hpg_knobs* knobs, int rank, int world,
       *out = wrap(nested_sha_search(C, K, nullptr), C.prob);
       return;
     }
-    Dist d;
-    dist_init(d, rank, world, nccl_id, C.device);
-    try {
-      *out = wrap(nested_sha_search(C, K, &d), C.prob);
-    } catch (...) {
-      dist_destroy(d);
-      throw;
+    // the communicator is created on the first sharded search of a context
+    // (nccl_id consumed then) and reused afterwards
+    if (!C.dist.comm || C.dist.rank != rank || C.dist.world != world) {
+      if (C.dist.comm) dist_destroy(C.dist);
+      dist_init(C.dist, rank, world, nccl_id, C.device);
     }
-    dist_destroy(d);
+    *out = wrap(nested_sha_search(C, K, &C.dist), C.prob);
   });
 }
 

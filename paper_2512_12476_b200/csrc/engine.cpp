@@ -253,6 +253,7 @@ void init_cand(Cand& c, int T, const int* dp, const int* pp, const int* tp, cons
 }
 
 Ctx::~Ctx() {
+  if (dist.comm) dist_destroy(dist);
   if (d_blob) cudaFree(d_blob);
   if (d_sweep_tables) cudaFree(d_sweep_tables);
   if (ev0) cudaEventDestroy(ev0);
@@ -274,26 +275,58 @@ Ctx* create_ctx(const hpg_problem& hp, int device) {
   }
   auto* ctx = new Ctx();
   try {
-    ctx->prob = std::move(P);
     ctx->device = device;
     ctx->n_sm = prop.multiProcessorCount;
     cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreate(&ctx->ev0), "event");
     cuda_check(cudaEventCreate(&ctx->ev1), "event");
+    stage_problem(*ctx, std::move(P));
+  } catch (...) {
+    delete ctx;
+    throw;
+  }
+  return ctx;
+}
+
+void restage(Ctx& ctx, const hpg_problem& hp) {
+  Problem P = build_problem(hp);
+  cuda_check(cudaSetDevice(ctx.device), "cudaSetDevice");
+  stage_problem(ctx, std::move(P));
+}
+
+// Uploads the flattened problem (device attributes, link classes) and fills
+// the by-value kernel header. Validation already happened in build_problem.
+void stage_problem(Ctx& ctxr, Problem&& P) {
+  Ctx* ctx = &ctxr;
+  {
+    // sweep tables belong to the previous problem
+    if (ctx->d_sweep_tables) {
+      cudaFree(ctx->d_sweep_tables);
+      ctx->d_sweep_tables = nullptr;
+    }
+    ctx->prob = std::move(P);
     const Problem& Q = ctx->prob;
     const int N = Q.N, C = static_cast<int>(Q.lat.size());
     const size_t bytes = 8 * (3 * N + 2 * C) + static_cast<size_t>(N) * N;
-    std::vector<uint8_t> blob(bytes);
-    double* dd = reinterpret_cast<double*>(blob.data());
+    ctx->h_blob.reserve(bytes);
+    double* dd = reinterpret_cast<double*>(ctx->h_blob.p);
     std::memcpy(dd, Q.comp.data(), 8 * N);
     std::memcpy(dd + N, Q.mem.data(), 8 * N);
     std::memcpy(dd + 2 * N, Q.hbm.data(), 8 * N);
     std::memcpy(dd + 3 * N, Q.lat.data(), 8 * C);
     std::memcpy(dd + 3 * N + C, Q.bw.data(), 8 * C);
-    std::memcpy(blob.data() + 8 * (3 * N + 2 * C), Q.cls.data(), static_cast<size_t>(N) * N);
-    cuda_check(cudaMalloc(&ctx->d_blob, bytes), "cudaMalloc problem");
-    cuda_check(cudaMemcpy(ctx->d_blob, blob.data(), bytes, cudaMemcpyHostToDevice), "H2D problem");
+    std::memcpy(ctx->h_blob.p + 8 * (3 * N + 2 * C), Q.cls.data(), static_cast<size_t>(N) * N);
+    if (bytes > ctx->blob_bytes) {
+      if (ctx->d_blob) cudaFree(ctx->d_blob);
+      ctx->d_blob = nullptr;
+      cuda_check(cudaMalloc(&ctx->d_blob, bytes), "cudaMalloc problem");
+      ctx->blob_bytes = bytes;
+    }
+    cuda_check(cudaMemcpyAsync(ctx->d_blob, ctx->h_blob.p, bytes, cudaMemcpyHostToDevice,
+                               ctx->stream), "H2D problem");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "H2D problem");
     ctx->h2d_bytes += static_cast<int64_t>(bytes);
+    ctx->max_nl = 1;
     DevProblem& D = ctx->dprob;
     const double* db = reinterpret_cast<const double*>(ctx->d_blob);
     D.n_dev = N;
@@ -332,11 +365,7 @@ Ctx* create_ctx(const hpg_problem& hp, int device) {
     D.lat = db + 3 * N;
     D.bw = db + 3 * N + C;
     D.cls = reinterpret_cast<const uint8_t*>(ctx->d_blob) + 8 * (3 * N + 2 * C);
-  } catch (...) {
-    delete ctx;
-    throw;
   }
-  return ctx;
 }
 
 void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags, bool want_out,

@@ -14,6 +14,7 @@
 #include "../../include/hpg.h"
 #include "common.hpp"
 #include "rng.hpp"
+#include "sweep.hpp"
 
 namespace hpg {
 
@@ -138,6 +139,14 @@ struct Batch {
   std::vector<int32_t> modes;
 };
 
+// Multi-GPU: NCCL communicator of a context (created once, reused by every
+// sharded search on it).
+struct Dist {
+  int rank = 0, world = 1;
+  void* comm = nullptr;  // ncclComm_t
+};
+void dist_destroy(Dist& d);
+
 struct BatchOut {
   std::vector<EvalResult> res;
   HostBuf<uint8_t>* out_recs = nullptr;  // same offsets as packed input
@@ -153,6 +162,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   DevProblem dprob{};
   void* d_blob = nullptr;
+  size_t blob_bytes = 0;
+  HostBuf<uint8_t> h_blob;  // pinned staging of the problem tables
   // batch staging
   HostBuf<uint8_t> h_recs, h_out;
   HostBuf<int64_t> h_off;
@@ -165,9 +176,11 @@ struct Ctx {
   DevBuf<double> d_per_task, d_required;
   DevBuf<double> d_scratch;  // per-CTA global scratch of eval_kernel
   DevBuf<uint8_t> d_xch_send, d_xch_recv;  // multi-GPU record exchange
+  Dist dist;                               // world 1 until hpg_search_dist attaches
   int64_t max_nl = 1;
   // sweep
-  void* d_sweep_tables = nullptr;
+  void* d_sweep_tables = nullptr;  // owns sweep_tb's arrays
+  SweepTablesDev sweep_tb{};
   DevBuf<double> d_costs;
   DevBuf<uint8_t> d_feas;
   DevBuf<unsigned long long> d_best;
@@ -187,6 +200,8 @@ struct Ctx {
 };
 
 Ctx* create_ctx(const hpg_problem& p, int device);
+void stage_problem(Ctx& ctx, Problem&& P);
+void restage(Ctx& ctx, const hpg_problem& p);
 
 // Packs `b`, runs eval_kernel, returns per-plan results (and balanced records).
 void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,

@@ -81,13 +81,6 @@ struct SearchOut {
   double eval_ms = 0.0, host_ms = 0.0, batch_ms = 0.0;
 };
 
-// Multi-GPU: per-arm records all-gathered across ranks after every round.
-struct Dist {
-  int rank = 0, world = 1;
-  void* comm = nullptr;  // ncclComm_t
-  void* lib = nullptr;   // dlopen handle
-};
-
 SearchOut nested_sha_search(Ctx& ctx, const Knobs& k, Dist* dist);
 SearchOut ga_search(Ctx& ctx, const Grouping& tg, const std::vector<int>& counts, int64_t slice,
                     uint64_t seed, const Knobs& k);

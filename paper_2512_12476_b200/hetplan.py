@@ -158,7 +158,7 @@ _lib = None
 
 EXPORTED_SYMBOLS = [
     "hpg_abi_version", "hpg_cost_config_default", "hpg_knobs_default", "hpg_create",
-    "hpg_destroy", "hpg_max_devices_per_node", "hpg_link", "hpg_eval", "hpg_check_memory",
+    "hpg_destroy", "hpg_restage", "hpg_max_devices_per_node", "hpg_link", "hpg_eval", "hpg_check_memory",
     "hpg_balance", "hpg_search", "hpg_nccl_unique_id", "hpg_search_dist", "hpg_ga_search",
     "hpg_result_info", "hpg_result_b_m", "hpg_result_trace", "hpg_result_arms",
     "hpg_result_halvings", "hpg_result_survivor_sizes", "hpg_result_survivors",
@@ -184,6 +184,7 @@ def load_library(path: str = LIB_PATH):
         "hpg_knobs_default": (None, [P(_Knobs)]),
         "hpg_create": (C.c_int, [P(_Problem), C.c_int, P(C.c_void_p), E, L]),
         "hpg_destroy": (None, [C.c_void_p]),
+        "hpg_restage": (C.c_int, [C.c_void_p, P(_Problem), E, L]),
         "hpg_max_devices_per_node": (C.c_int, [C.c_void_p]),
         "hpg_link": (C.c_int, [C.c_void_p, C.c_int, C.c_int, P(C.c_double), P(C.c_double)]),
         "hpg_eval": (C.c_int, [C.c_void_p, P(_PlanTable), P(_CostConfig), P(_EvalOut), E, L]),
@@ -479,6 +480,14 @@ class Engine:
 
     def __init__(self, wf: Workflow, topo: Topology, device: int = 0):
         self.lib = load_library()
+        prob = self._problem(wf, topo)
+        self._h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = self.lib.hpg_create(C.byref(prob), device, C.byref(self._h), err, 1024)
+        _raise(rc, err)
+
+    def _problem(self, wf: Workflow, topo: Topology) -> "_Problem":
+        """hpg_problem from host objects (kept alive on self)"""
         self.wf, self.topo = wf, topo
         tasks = (_Task * len(wf.tasks))(*[
             _Task(t["id"], t["kind"], t["h1"], t["h2"], t["nl"], int(t["emb"]), t["vocab"],
@@ -497,17 +506,20 @@ class Engine:
         links = (_RegionLink * max(1, len(topo.region_links)))(*[
             _RegionLink(s(l["src"]), s(l["dst"]), l["latency_ms"], l["bandwidth_gbps"])
             for l in topo.region_links])
-        prob = _Problem(0 if wf.algorithm == "ppo" else 1, 0 if wf.mode == "sync" else 1,
+        self._keep = (tasks, devs, links, _arr(C.c_int32, edges))
+        return _Problem(0 if wf.algorithm == "ppo" else 1, 0 if wf.mode == "sync" else 1,
                         wf.eta, wf.global_batch, wf.responses_per_prompt, wf.seq_in,
                         wf.seq_out, wf.micro_batch_size, len(wf.tasks), tasks,
-                        len(wf.dep_edges), _arr(C.c_int32, edges), topo.n, devs,
+                        len(wf.dep_edges), self._keep[3], topo.n, devs,
                         len(topo.region_links), links,
                         topo.defaults["intra_region_latency_ms"],
                         topo.defaults["intra_region_bandwidth_gbps"])
-        self._h = C.c_void_p()
+
+    def restage(self, wf: Workflow, topo: Topology) -> None:
+        """hpg_restage: upload a (new) problem into this context"""
+        prob = self._problem(wf, topo)
         err = C.create_string_buffer(1024)
-        rc = self.lib.hpg_create(C.byref(prob), device, C.byref(self._h), err, 1024)
-        _raise(rc, err)
+        _raise(self.lib.hpg_restage(self._h, C.byref(prob), err, 1024), err)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -1,0 +1,66 @@
+"""world_size-2 gloo tests (CPU) of the multi-process plumbing the sharded
+search and bench.py use: id broadcast, max/sum over ranks, run ownership."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    from paper_2512_12476_b200 import distutil
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    payload = bytes(range(128)) if rank == 0 else None
+    got = distutil.broadcast_bytes(payload, 0, 128)
+    mx = distutil.max_over_ranks(10.0 * (rank + 1))
+    sm = distutil.sum_over_ranks(1.0)
+    owned = [r for r in range(10) if distutil.shard_of(r, world) == rank]
+    q.put((rank, got == bytes(range(128)), mx, sm, owned))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_plumbing():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] for r in res)
+    assert all(r[2] == 20.0 and r[3] == 2.0 for r in res)
+    owned = sorted(i for r in res for i in r[4])
+    assert owned == list(range(10))            # every run has exactly one owner
+    assert res[0][4] == [0, 2, 4, 6, 8]
+
+
+@pytest.mark.gpu
+def test_multi_gpu_search_parity():
+    """sharded search == reference goldens on every rank (needs >= 2 GPUs)"""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(_free_port()),
+                        os.path.join(root, "scripts", "dist_check.py")],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
