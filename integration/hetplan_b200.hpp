@@ -1,0 +1,61 @@
+// hetplan_b200 — reference-side adapter: the hetplan API (same names, same
+// argument meaning, same exceptions) implemented over the B200 engine's C ABI
+// (include/hpg.h). A hetplan maintainer adds this header + hetplan_b200.cpp to
+// proj/src and links libhpg.so; call sites switch from hetplan::X to
+// hetplan::b200::X (or keep an Engine per problem to amortise staging).
+//
+// Compiled against the reference headers (proj/include/hetplan/*.hpp); it is
+// not part of the engine library itself.
+#pragma once
+
+#include <memory>
+#include <optional>
+#include <vector>
+
+#include "hetplan/balance.hpp"
+#include "hetplan/cost_model.hpp"
+#include "hetplan/plan.hpp"
+#include "hetplan/search.hpp"
+#include "hetplan/topology.hpp"
+#include "hetplan/workflow.hpp"
+
+struct hpg_ctx;
+
+namespace hetplan::b200 {
+
+// One (workflow, topology) staged on one GPU. Throws InputError / UsageError
+// like the reference; engine faults surface as std::runtime_error.
+class Engine {
+ public:
+  Engine(const WorkflowGraph& wf, const DeviceTopology& topo, int cuda_device = 0);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  // end_to_end_cost (cost_model.hpp:115-117), batched
+  std::vector<CostBreakdown> end_to_end_cost(const std::vector<Plan>& plans,
+                                             const CostModelConfig& cfg = {});
+  // check_memory (plan.hpp:116-119)
+  std::vector<MemoryViolation> check_memory(const Plan& plan, const MemoryModel& mm = {});
+  // balance_data / balance_layers (balance.hpp:23-31)
+  Plan balance_data(const Plan& plan, const CostModelConfig& cfg = {});
+  Plan balance_layers(const Plan& plan, const CostModelConfig& cfg = {});
+  // nested_sha_search (search.hpp:115-118)
+  SearchResult nested_sha_search(const SearchKnobs& knobs,
+                                 const std::vector<TaskGrouping>* tg_override = nullptr);
+
+ private:
+  const WorkflowGraph& wf_;
+  const DeviceTopology& topo_;
+  hpg_ctx* ctx_ = nullptr;
+};
+
+// Free-function forms with the reference signatures (stage the problem per
+// call; prefer Engine for repeated calls).
+CostBreakdown end_to_end_cost(const Plan& plan, const WorkflowGraph& wf,
+                              const DeviceTopology& topo, const CostModelConfig& cfg = {});
+SearchResult nested_sha_search(const WorkflowGraph& wf, const DeviceTopology& topo,
+                               const SearchKnobs& knobs,
+                               const std::vector<TaskGrouping>* tg_override = nullptr);
+
+}  // namespace hetplan::b200

@@ -64,3 +64,18 @@ def test_multi_gpu_search_parity():
                         os.path.join(root, "scripts", "dist_check.py")],
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+def test_reference_adapter_shim():
+    """the reference's own API (hetplan_b200 adapter over the C ABI) gives
+    byte-identical plans vs the compiled reference (needs oracle/_ref/shim_check,
+    built here by `make -C oracle shim`)"""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "shim_check")
+    if not os.path.exists(exe):
+        pytest.skip("shim_check not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, os.path.join(root, "fixtures")], capture_output=True, text=True,
+                       timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
