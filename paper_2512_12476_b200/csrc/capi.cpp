@@ -188,7 +188,7 @@ int hpg_balance(hpg_ctx* ctx, const hpg_plan_table* plans, const hpg_cost_config
     const int T = C.prob.T;
     for (size_t i = 0; i < tps.size(); ++i) {
       const Cand& in = tps[i].cand;
-      const uint8_t* rec = bo.out_recs->p + bo.off[i];
+      const uint8_t* rec = bo.out_recs + bo.off[i];
       const double* w = reinterpret_cast<const double*>(rec + in.o.w_byte);
       const int32_t* sl = reinterpret_cast<const int32_t*>(rec + in.o.sl_byte);
       for (int s = 0; s < T; ++s) {

@@ -390,35 +390,42 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     cv.max_cells = std::max(cv.max_cells, c.o.cell[T]);
     cv.max_dpk = std::max(cv.max_dpk, c.o.dpk[T]);
   }
-  ctx.h_recs.reserve(total);
-  ctx.h_off.reserve(n);
-  ctx.h_modes.reserve(n);
-  ctx.h_res.reserve(n);
-host_parallel_for(n, n >= 4096, [&](int i) {
-    std::memcpy(ctx.h_recs.p + out.off[i], b.cands[i]->rec.data(), b.cands[i]->o.bytes);
-    ctx.h_off.p[i] = out.off[i];
-    ctx.h_modes.p[i] = b.modes[i];
+  // one input transfer: [offsets i64 | modes i32 (8-aligned) | records]
+  const int64_t in_off = 0, in_modes = 8 * static_cast<int64_t>(n),
+                in_recs = in_modes + ((4 * static_cast<int64_t>(n) + 7) & ~int64_t(7));
+  const int64_t in_bytes = in_recs + total;
+  ctx.h_recs.reserve(in_bytes);
+  int64_t* h_off = reinterpret_cast<int64_t*>(ctx.h_recs.p + in_off);
+  int32_t* h_modes = reinterpret_cast<int32_t*>(ctx.h_recs.p + in_modes);
+  uint8_t* h_rec = ctx.h_recs.p + in_recs;
+  host_parallel_for(n, n >= 4096, [&](int i) {
+    std::memcpy(h_rec + out.off[i], b.cands[i]->rec.data(), b.cands[i]->o.bytes);
+    h_off[i] = out.off[i];
+    h_modes[i] = b.modes[i];
   });
-  ctx.d_recs.reserve(total);
-  ctx.d_off.reserve(n);
-  ctx.d_modes.reserve(n);
-  ctx.d_res.reserve(n);
-  if (want_out) ctx.d_out.reserve(total);
+  // one output transfer: [results 32 B each | balanced records]
+  const int64_t out_res = 0, out_recs = 32 * static_cast<int64_t>(n);
+  const int64_t out_bytes = out_recs + (want_out ? total : 0);
+  ctx.d_recs.reserve(in_bytes);
+  ctx.d_out.reserve(out_bytes);
   if (want_per_task) ctx.d_per_task.reserve(static_cast<size_t>(n) * P.T * 7);
   if (want_required) ctx.d_required.reserve(static_cast<size_t>(n) * P.N);
   cudaStream_t st = ctx.stream;
-  cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, total, cudaMemcpyHostToDevice, st), "H2D recs");
-  cuda_check(cudaMemcpyAsync(ctx.d_off.p, ctx.h_off.p, 8 * n, cudaMemcpyHostToDevice, st), "H2D off");
-  cuda_check(cudaMemcpyAsync(ctx.d_modes.p, ctx.h_modes.p, 4 * n, cudaMemcpyHostToDevice, st), "H2D modes");
+  cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, in_bytes, cudaMemcpyHostToDevice, st),
+             "H2D wave");
+  const int64_t* d_off = reinterpret_cast<const int64_t*>(ctx.d_recs.p + in_off);
+  const int32_t* d_modes = reinterpret_cast<const int32_t*>(ctx.d_recs.p + in_modes);
+  const uint8_t* d_rec = ctx.d_recs.p + in_recs;
+  EvalResult* d_res = reinterpret_cast<EvalResult*>(ctx.d_out.p + out_res);
+  uint8_t* d_orec = want_out ? ctx.d_out.p + out_recs : nullptr;
   int grid = 0;
   cuda_check(eval_grid(cv, n, ctx.n_sm, grid), "eval_kernel occupancy");
   const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);
   // sized once for the largest possible persistent grid (32 CTAs per SM)
   ctx.d_scratch.reserve(static_cast<size_t>(std::max(grid, 32 * ctx.n_sm)) * scratch);
   cuda_check(cudaEventRecord(ctx.ev0, st), "event");
-  cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, ctx.d_recs.p, ctx.d_off.p, ctx.d_modes.p, 0,
-                         n, 0, want_out ? ctx.d_out.p : nullptr, ctx.d_res.p,
-                         want_per_task ? ctx.d_per_task.p : nullptr,
+  cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, d_rec, d_off, d_modes, 0, n, 0, d_orec,
+                         d_res, want_per_task ? ctx.d_per_task.p : nullptr,
                          want_required ? ctx.d_required.p : nullptr, ctx.d_scratch.p, scratch,
                          grid, st),
              "eval_kernel launch");
@@ -426,9 +433,8 @@ host_parallel_for(n, n >= 4096, [&](int i) {
   ++ctx.launches;
   ++ctx.eval_launches;
   ctx.plans_evaluated += n;
-  ctx.h2d_bytes += total + 12 * static_cast<int64_t>(n);
-  ctx.d2h_bytes += static_cast<int64_t>(sizeof(EvalResult)) * n + (want_out ? total : 0) +
-                   (want_per_task ? 8 * static_cast<int64_t>(n) * P.T * 7 : 0) +
+  ctx.h2d_bytes += in_bytes;
+  ctx.d2h_bytes += out_bytes + (want_per_task ? 8 * static_cast<int64_t>(n) * P.T * 7 : 0) +
                    (want_required ? 8 * static_cast<int64_t>(n) * P.N : 0);
   for (int i = 0; i < n; ++i) {
     // canonical bytes: tg id + k counts + per task
@@ -447,13 +453,10 @@ host_parallel_for(n, n >= 4096, [&](int i) {
     }
     ctx.canonical_bytes += cb;
   }
-  cuda_check(cudaMemcpyAsync(ctx.h_res.p, ctx.d_res.p, sizeof(EvalResult) * n,
-                             cudaMemcpyDeviceToHost, st), "D2H results");
-  if (want_out) {
-    ctx.h_out.reserve(total);
-    cuda_check(cudaMemcpyAsync(ctx.h_out.p, ctx.d_out.p, total, cudaMemcpyDeviceToHost, st), "D2H recs");
-    out.out_recs = &ctx.h_out;
-  }
+  ctx.h_out.reserve(out_bytes);
+  cuda_check(cudaMemcpyAsync(ctx.h_out.p, ctx.d_out.p, out_bytes, cudaMemcpyDeviceToHost, st),
+             "D2H wave");
+  out.out_recs = want_out ? ctx.h_out.p + out_recs : nullptr;
   if (want_per_task) out.per_task.resize(static_cast<size_t>(n) * P.T * 7);
   if (want_required) out.required.resize(static_cast<size_t>(n) * P.N);
   if (want_per_task)
@@ -466,7 +469,7 @@ host_parallel_for(n, n >= 4096, [&](int i) {
   float ms = 0.f;
   cuda_check(cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1), "event time");
   ctx.eval_ms += ms;
-  std::memcpy(out.res.data(), ctx.h_res.p, sizeof(EvalResult) * n);
+  std::memcpy(out.res.data(), ctx.h_out.p + out_res, sizeof(EvalResult) * n);
 }
 
 std::vector<TablePlan> unpack_table(const Problem& P, const hpg_plan_table& t) {

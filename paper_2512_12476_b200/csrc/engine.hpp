@@ -149,7 +149,7 @@ void dist_destroy(Dist& d);
 
 struct BatchOut {
   std::vector<EvalResult> res;
-  HostBuf<uint8_t>* out_recs = nullptr;  // same offsets as packed input
+  const uint8_t* out_recs = nullptr;  // balanced records, same offsets as packed input
   std::vector<int64_t> off;
   std::vector<double> per_task;          // if requested
   std::vector<double> required;          // if requested

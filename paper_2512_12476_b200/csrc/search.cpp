@@ -514,7 +514,7 @@ ArmCoro ga_run(ArmRun& run) {
     if (static_cast<int>(pop.size()) > K.population) pop.pop_back();
   };
   EvalReq req;
-  std::vector<Rng> snaps;
+  std::vector<Rng> snaps, snaps5;
 
   // init: cycle layout combinations (speculative chunks, one wave each)
   const int64_t init_target =
@@ -587,40 +587,66 @@ ArmCoro ga_run(ArmRun& run) {
     }
     streak = 0;
     score(child, cost);
-    for (int level : {3, 5}) {
-      if (run.used >= slice) break;
-      req.cands.clear();
-      snaps.clear();
-      const Rng before = rng;
-      int ngen = 0;
+    // improving swaps, first improvement per level (search.cpp:534-558).
+    // Both levels' trials are drawn from the current child and scored in one
+    // wave; the level-5 set stays valid unless a level-3 trial is accepted
+    // (then level 5 is redrawn from the new child, as the reference does).
+    // walk(): the sequential trial loop over already-scored trials
+    // [b, b+n); returns 1 accepted, 2 budget stop, 0 ran out.
+    auto walk = [&](int b, int n, const Rng& before, const std::vector<Rng>& sn) {
+      for (int t = 0; t < n; ++t) {
+        if (run.used >= slice) {
+          rng = t == 0 ? before : sn[t - 1];
+          return 2;
+        }
+        if (!(req.res[b + t].flags & kResFeasIn)) continue;
+        const double c2 = req.res[b + t].cost;
+        score(req.cands[b + t], c2);
+        if (c2 < cost) {
+          child = std::move(req.cands[b + t]);
+          cost = c2;
+          rng = sn[t];
+          return 1;
+        }
+      }
+      if (n > 0) rng = sn.back();
+      return 0;
+    };
+    auto draw = [&](int level, std::vector<Rng>& sn) {
+      int ng = 0;
       for (int t = 0; t < K.swap_pair_sample; ++t) {
         Cand cand = child;
         if (!random_move(e, cand, level, rng)) break;
         req.cands.push_back(std::move(cand));
-        snaps.push_back(rng);
-        ++ngen;
+        sn.push_back(rng);
+        ++ng;
       }
-      if (ngen == 0) continue;
-      co_await EvalAwait{&req};
-      bool stopped = false;
-      for (int t = 0; t < ngen; ++t) {
-        if (run.used >= slice) {
-          rng = t == 0 ? before : snaps[t - 1];
-          stopped = true;
-          break;
-        }
-        if (!(req.res[t].flags & kResFeasIn)) continue;
-        const double c2 = req.res[t].cost;
-        score(req.cands[t], c2);
-        if (c2 < cost) {
-          child = std::move(req.cands[t]);
-          cost = c2;
-          rng = snaps[t];
-          stopped = true;
-          break;
+      return ng;
+    };
+    if (run.used < slice) {
+      req.cands.clear();
+      snaps.clear();
+      snaps5.clear();
+      const Rng before3 = rng;
+      const int n3 = draw(3, snaps);
+      const Rng before5 = rng;
+      const int n5 = draw(5, snaps5);
+      if (n3 + n5 > 0) co_await EvalAwait{&req};
+      rng = before5;  // stream position after the level-3 draws (walk may rewind it)
+      const int w3 = walk(0, n3, before3, snaps);
+      if (w3 == 0 && run.used < slice) {
+        rng = before5;
+        walk(n3, n5, before5, snaps5);
+      } else if (w3 == 1 && run.used < slice) {
+        req.cands.clear();
+        snaps5.clear();
+        const Rng b5 = rng;
+        const int m5 = draw(5, snaps5);
+        if (m5 > 0) {
+          co_await EvalAwait{&req};
+          walk(0, m5, b5, snaps5);
         }
       }
-      if (!stopped) rng = snaps.back();
     }
     if (static_cast<int>(pop.size()) < K.population || cost < pop.back().cost) {
       insert_member(child, cost);
@@ -686,7 +712,7 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
         const size_t kk = first[o] + i;
         q->res[i] = bo.res[kk];
         Cand& c = q->cands[i];
-        std::memcpy(c.rec.data(), bo.out_recs->p + bo.off[kk], c.o.bytes);
+        std::memcpy(c.rec.data(), bo.out_recs + bo.off[kk], c.o.bytes);
       }
       r->coro.h.promise().pending = nullptr;
       r->coro.h.resume();
