@@ -195,7 +195,10 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
     const int64_t scratch = eval_scratch_doubles(P.N, C.max_nl);
     C.d_scratch.reserve(static_cast<size_t>(grid) * scratch);
     cudaEventRecord(e1, st);
-    cuda_check(launch_eval(C.dprob, cfg, cv, 0, C.d_recs.p, nullptr, nullptr, kModeE2E,
+    // independent random plans share no rings: the ring memo would only fill
+    DevProblem sweep_prob = C.dprob;
+    sweep_prob.ring_cache = nullptr;
+    cuda_check(launch_eval(sweep_prob, cfg, cv, 0, C.d_recs.p, nullptr, nullptr, kModeE2E,
                            static_cast<int>(n), stride, nullptr, C.d_res.p, nullptr, nullptr,
                            C.d_scratch.p, scratch, grid, st),
                "eval_kernel");

@@ -49,6 +49,19 @@ struct DevCostConfig {
   double act_factor;
 };
 
+// Device-wide ring memo (open addressing in HBM). A ring's bottleneck is a
+// pure function of (ordered device list, volume bits) for a fixed topology,
+// so concurrent inserts can only duplicate work, never change a result.
+// Key: k1/k3 = two independent 64-bit hashes of the ordered device list
+// (exact packing when n <= 7), k2 = volume bits; state 1 = value published.
+struct RingSlot {
+  unsigned long long k1, k2, k3;
+  double value;
+  unsigned long long state;
+  unsigned long long pad;
+};
+static_assert(sizeof(RingSlot) == 48, "ring slot layout");
+
 // Problem header, passed by value to every kernel. Arrays live in one device
 // allocation owned by the context.
 struct DevProblem {
@@ -69,6 +82,8 @@ struct DevProblem {
   const uint8_t* cls;  // [n_dev * n_dev] link class of (a, b)
   const double* lat;   // [n_classes] seconds
   const double* bw;    // [n_classes] bytes/s (inf for self)
+  RingSlot* ring_cache;       // nullptr = disabled
+  unsigned long long ring_mask;  // slots - 1 (power of two)
 };
 
 // ---- packed plan record ----

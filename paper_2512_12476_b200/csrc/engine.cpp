@@ -365,6 +365,20 @@ void stage_problem(Ctx& ctxr, Problem&& P) {
     D.lat = db + 3 * N;
     D.bw = db + 3 * N + C;
     D.cls = reinterpret_cast<const uint8_t*>(ctx->d_blob) + 8 * (3 * N + 2 * C);
+    // device-wide ring memo: 2^20 slots (48 MiB), cleared per problem.
+    // HPG_RING_CACHE=0 disables it (A/B measurements).
+    const char* rc = std::getenv("HPG_RING_CACHE");
+    const bool use_rc = !(rc && rc[0] == '0');
+    constexpr size_t kSlots = size_t(1) << 20;
+    D.ring_cache = nullptr;
+    D.ring_mask = kSlots - 1;
+    if (use_rc) {
+      ctx->d_ring.reserve(kSlots * sizeof(RingSlot));
+      cuda_check(cudaMemsetAsync(ctx->d_ring.p, 0, kSlots * sizeof(RingSlot), ctx->stream),
+                 "ring cache clear");
+      cuda_check(cudaStreamSynchronize(ctx->stream), "ring cache clear");
+      D.ring_cache = reinterpret_cast<RingSlot*>(ctx->d_ring.p);
+    }
   }
 }
 
@@ -423,6 +437,13 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);
   // sized once for the largest possible persistent grid (32 CTAs per SM)
   ctx.d_scratch.reserve(static_cast<size_t>(std::max(grid, 32 * ctx.n_sm)) * scratch);
+  static const char* plan_prof_log = std::getenv("HPG_PLAN_PROFILE");  // diagnostics only
+  long long* d_prof = nullptr;
+  if (plan_prof_log) {
+    cuda_check(cudaMalloc(&d_prof, sizeof(long long) * 5 * n), "profile alloc");
+    cuda_check(cudaMemsetAsync(d_prof, 0, sizeof(long long) * 5 * n, st), "profile clear");
+    cuda_check(eval_set_plan_profile(d_prof), "profile symbol");
+  }
   cuda_check(cudaEventRecord(ctx.ev0, st), "event");
   cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, d_rec, d_off, d_modes, 0, n, 0, d_orec,
                          d_res, want_per_task ? ctx.d_per_task.p : nullptr,
@@ -469,6 +490,37 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   float ms = 0.f;
   cuda_check(cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1), "event time");
   ctx.eval_ms += ms;
+  static const char* wave_log = std::getenv("HPG_WAVE_LOG");  // diagnostics only
+  if (wave_log) {
+    if (FILE* f = std::fopen(wave_log, "a")) {
+      int nev = 0;
+      for (int i = 0; i < n; ++i) nev += b.modes[i] == kModeEvaluate;
+      std::fprintf(f, "%d %d %.4f\n", n, nev, ms);
+      std::fclose(f);
+    }
+  }
+  if (d_prof) {
+    std::vector<long long> pr(static_cast<size_t>(5) * n);
+    cuda_check(cudaMemcpy(pr.data(), d_prof, sizeof(long long) * 5 * n, cudaMemcpyDeviceToHost),
+               "profile D2H");
+    cuda_check(eval_set_plan_profile(nullptr), "profile symbol");
+    cudaFree(d_prof);
+    static int wave_no = 0;
+    if (FILE* f = std::fopen(plan_prof_log, "a")) {
+      // wave n ms | per plan: mode stage bal_data bal_layers e2e | dp,pp,tp per task
+      for (int i = 0; i < n; ++i) {
+        const long long* q = &pr[5 * static_cast<size_t>(i)];
+        const long long t1 = q[1] ? q[1] : q[0], t2 = q[2] ? q[2] : t1, t3 = q[3] ? q[3] : t2;
+        std::fprintf(f, "%d %d %.4f %d %lld %lld %lld %lld", wave_no, n, ms, b.modes[i], t1 - q[0],
+                     t2 - t1, t3 - t2, q[4] - t3);
+        const RecHeader& h = b.cands[i]->hdr();
+        for (int t = 0; t < P.T; ++t) std::fprintf(f, " %d,%d,%d", h.dp[t], h.pp[t], h.tp[t]);
+        std::fputc('\n', f);
+      }
+      std::fclose(f);
+    }
+    ++wave_no;
+  }
   std::memcpy(out.res.data(), ctx.h_out.p + out_res, sizeof(EvalResult) * n);
 }
 

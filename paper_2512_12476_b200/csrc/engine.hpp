@@ -175,6 +175,7 @@ struct Ctx {
   DevBuf<EvalResult> d_res;
   DevBuf<double> d_per_task, d_required;
   DevBuf<double> d_scratch;  // per-CTA global scratch of eval_kernel
+  DevBuf<uint8_t> d_ring;    // device-wide ring memo (RingSlot table)
   DevBuf<uint8_t> d_xch_send, d_xch_recv;  // multi-GPU record exchange
   Dist dist;                               // world 1 until hpg_search_dist attaches
   int64_t max_nl = 1;

@@ -182,7 +182,8 @@ __device__ __noinline__ void ensure_dtab(const DevProblem& P, Ws& s, int t, int 
   const DevTask& tk = P.task[t];
   const int dp = s.h.dp[t], pp = s.h.pp[t], tp = s.h.tp[t];
   const uint8_t* dv = s.dev + s.o.dev[t];
-  class_costs(P, s, dp_comm_volume(tk.precision_bytes, L, tk.h1, tk.h2, dp, tp));
+  const double cv_dp = dp_comm_volume(tk.precision_bytes, L, tk.h1, tk.h2, dp, tp);
+  class_costs(P, s, cv_dp);
   double m = 0.0;
   for (int k = 0; k < tp; ++k) {
     if (dp == 2) {
@@ -192,7 +193,7 @@ __device__ __noinline__ void ensure_dtab(const DevProblem& P, Ws& s, int t, int 
     __syncwarp();
     for (int i = lane; i < dp; i += 32) s.peers[i] = dv[flat(i, j, k, pp, tp)];
     __syncwarp();
-    m = smax(m, ring_bottleneck(P, s, s.peers, dp));
+    m = smax(m, ring_bottleneck(P, s, s.peers, dp, cv_dp));
   }
   __syncwarp();
   if (lane == 0) *slot = m;
@@ -482,6 +483,9 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
   }
 }
 
+// diagnostics only (HPG_PLAN_PROFILE): per-plan clock64 phase stamps
+__device__ long long* g_plan_prof = nullptr;
+
 __global__ void __launch_bounds__(32)
 eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
             const uint8_t* __restrict__ recs, const int64_t* __restrict__ off,
@@ -502,6 +506,8 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
     const int64_t rec_at = off ? off[p] : static_cast<int64_t>(p) * stride;
     const uint8_t* rec = recs + rec_at;
     const int mode = modes ? modes[p] : uniform_mode;
+    long long* prof = g_plan_prof ? g_plan_prof + 5 * static_cast<int64_t>(p) : nullptr;
+    if (prof && lane == 0) prof[0] = clock64();
     // ---- stage the plan ----
     if (lane < 20) reinterpret_cast<int32_t*>(&s.h)[lane] = reinterpret_cast<const int32_t*>(rec)[lane];
     __syncwarp();
@@ -568,13 +574,16 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
         bool have_cur = false, ch = false;
         E2E cur;
         if ((chain && (kb_flags & 1)) || mode == kModeBalanceData) {
+          if (prof && lane == 0) prof[1] = clock64();
           have_cur = balance_data_dev(P, cfg, s, cur, ch);
           if (ch) r.flags |= kResWeights;
         }
+        if (prof && lane == 0) prof[2] = clock64();
         if ((chain && (kb_flags & 2)) || mode == kModeBalanceLayers) {
           balance_layers_dev(P, cfg, s, have_cur, cur, ch);
           if (ch) r.flags |= kResLayers;
         }
+        if (prof && lane == 0) prof[3] = clock64();
         if (!have_cur) cur = end_to_end(P, cfg, s);
         r.cost = cur.e2e;
         r.reshard_s = cur.reshard;
@@ -593,6 +602,7 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
       for (int i = lane; i < nsl; i += 32) osl[i] = s.sl[i];
       for (int i = lane; i < nslot; i += 32) odev[i] = s.dev[i];
     }
+    if (prof && lane == 0) prof[4] = clock64();
     if (lane == 0) res[p] = r;
     __syncwarp();
   }
@@ -601,6 +611,10 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
 }  // namespace dev
 
 int eval_smem_bytes(const Carve& c) { return carve2_bytes(c); }
+
+cudaError_t eval_set_plan_profile(long long* d_buf) {
+  return cudaMemcpyToSymbol(dev::g_plan_prof, &d_buf, sizeof(d_buf));
+}
 
 int64_t eval_scratch_doubles(int n_dev, int64_t max_nl) {
   // per CTA: DP-ring table [pp <= N][nl + 1]

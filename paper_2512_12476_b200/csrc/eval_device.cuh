@@ -86,6 +86,8 @@ struct Ws {
   int32_t memv_ok, memv;  // cached check_memory of the current plan
   double bridge;
   int32_t bridge_ok;
+  unsigned long long cc_sig;  // class-cost order signature of the staged volume
+  double cc_vol;              // staged volume
 };
 
 // The current plan changed: task t's stage split (affects t, the generation
@@ -270,12 +272,14 @@ __device__ __noinline__ void apportion(const DevProblem& P, Ws& s, int t) {
   }
   double wsum = 0.0;  // std::accumulate, sequential (all lanes redundantly)
   for (int i = 0; i < dp; ++i) wsum += w[i];
-  // floor of quotas + remainders
+  // floor of quotas + remainders (remainders staged in s.edge, free here)
+  double* rem = s.edge;
   int64_t assigned_part = 0;
   for (int i = lane; i < dp; i += 32) {
     const double quota = static_cast<double>(total) * w[i] / wsum;
     const int64_t f = static_cast<int64_t>(floor(quota));
     out[i] = f;
+    rem[i] = quota - static_cast<double>(f);
     assigned_part += f;
   }
   for (int o = 16; o > 0; o >>= 1) assigned_part += __shfl_xor_sync(kFull, assigned_part, o);
@@ -285,13 +289,11 @@ __device__ __noinline__ void apportion(const DevProblem& P, Ws& s, int t) {
     // rank of replica i in (remainder desc, index asc); deficit hands out one
     // micro-batch per rank position, cycling (plan.cpp:236-244)
     for (int i = lane; i < dp; i += 32) {
-      const double qi = static_cast<double>(total) * w[i] / wsum;
-      const double ri = qi - static_cast<double>(out[i]);
+      const double ri = rem[i];
       int rank = 0;
       for (int k = 0; k < dp; ++k) {
-        const double qk = static_cast<double>(total) * w[k] / wsum;
-        const double rk = qk - floor(qk);
-        if (rk > ri || (!(ri > rk) && rk == ri && k < i) ) ++rank;
+        const double rk = rem[k];
+        if (rk > ri || (rk == ri && k < i)) ++rank;
       }
       const int64_t extra = deficit / dp + (rank < deficit % dp ? 1 : 0);
       out[i] += extra;
@@ -381,10 +383,140 @@ __device__ __forceinline__ void class_costs(const DevProblem& P, Ws& s, double v
   __syncwarp();
   for (int c = lane; c < P.n_classes; c += 32) s.cc[c] = P.lat[c] + volume / P.bw[c];
   __syncwarp();
+  // order signature: rank of every class cost among all classes (ties share a
+  // rank), 4 bits per class. Every ring algorithm below decides only by
+  // comparing class costs, so equal signatures mean identical decisions.
+  unsigned long long sig = 0;
+  if (P.n_classes <= 16 && lane < P.n_classes) {
+    int rank = 0;
+    for (int c = 0; c < P.n_classes; ++c) rank += s.cc[c] < s.cc[lane] ? 1 : 0;
+    sig = static_cast<unsigned long long>(rank) << (4 * lane);
+  }
+  for (int o = 16; o > 0; o >>= 1) sig |= __shfl_xor_sync(kFull, sig, o);
+  if (lane == 0) {
+    s.cc_sig = sig;
+    s.cc_vol = volume;
+  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ double ecost(const DevProblem& P, const Ws& s, int a, int b) {
   return s.cc[__ldg(&P.cls[a * P.n_dev + b])];
+}
+
+// ---- device-wide ring memo (common.hpp RingSlot) ----
+
+__device__ __forceinline__ unsigned long long mix64d(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+struct RingKey {
+  unsigned long long k1, k2, k3;
+};
+
+// Exact key for n <= 8 (packed device bytes + n); two independent 64-bit
+// position-aware hashes otherwise (collision odds ~2^-128). k2 is the
+// class-cost order signature (<= 16 classes; the slot then stores the
+// bottleneck's link class, valid at every volume with the same order) or the
+// volume bits (the slot stores the value). Warp-collective.
+constexpr unsigned long long kSigMode = 1ull << 63;
+
+__device__ __forceinline__ RingKey ring_key(const DevProblem& P, const Ws& s,
+                                            const uint8_t* devs, int n) {
+  const int lane = threadIdx.x & 31;
+  RingKey k;
+  const bool sig = P.n_classes <= 16;
+  k.k2 = sig ? s.cc_sig : static_cast<unsigned long long>(__double_as_longlong(s.cc_vol));
+  const unsigned long long mode = sig ? kSigMode : 0ull;
+  if (n <= 8) {
+    unsigned long long p = 0;
+    for (int i = 0; i < n; ++i) p |= static_cast<unsigned long long>(devs[i]) << (8 * i);
+    k.k1 = p == 0 ? 1 : p;
+    k.k3 = static_cast<unsigned long long>(n) | mode;
+    return k;
+  }
+  unsigned long long a = 0, b = 0;
+  for (int i = lane; i < n; i += 32) {
+    const unsigned long long x = (static_cast<unsigned long long>(i) << 8) | devs[i];
+    a += mix64d(x ^ 0x5851f42d4c957f2dULL);
+    b += mix64d(x ^ 0x14057b7ef767814fULL);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(kFull, a, o);
+    b += __shfl_xor_sync(kFull, b, o);
+  }
+  k.k1 = a == 0 ? 1 : a;
+  k.k3 = ((b + static_cast<unsigned long long>(n)) & ~kSigMode) | mode;
+  return k;
+}
+
+// cached payload -> ring value at the staged volume
+__device__ __forceinline__ double ring_payload_value(const Ws& s, const RingKey& k, double stored) {
+  if (k.k3 & kSigMode) return s.cc[__double_as_longlong(stored)];
+  return stored;
+}
+
+// ring value -> payload: the class whose cost equals the bottleneck (any of
+// equal-cost classes: they stay equal under the same order signature)
+__device__ __forceinline__ bool ring_payload_of(const DevProblem& P, const Ws& s, const RingKey& k,
+                                                double v, double& stored) {
+  if (!(k.k3 & kSigMode)) {
+    stored = v;
+    return true;
+  }
+  const int lane = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(kFull, lane < P.n_classes && s.cc[lane] == v);
+  if (!bal) return false;
+  stored = __longlong_as_double(static_cast<long long>(__ffs(bal) - 1));
+  return true;
+}
+
+// lane 0 probes; result broadcast. Returns true and sets v on a hit.
+__device__ __forceinline__ bool ring_lookup(const DevProblem& P, const RingKey& k, double& v) {
+  const int lane = threadIdx.x & 31;
+  int hit = 0;
+  double val = 0.0;
+  if (lane == 0 && P.ring_cache) {
+    const unsigned long long h = (k.k1 ^ mix64d(k.k2 ^ k.k3)) & P.ring_mask;
+    for (int pr = 0; pr < 8; ++pr) {
+      volatile RingSlot* sl = P.ring_cache + ((h + pr) & P.ring_mask);
+      const unsigned long long a = sl->k1;
+      if (a == 0) break;
+      if (a != k.k1) continue;
+      if (sl->state != 1) break;  // being published: treat as a miss
+      __threadfence();
+      if (sl->k2 == k.k2 && sl->k3 == k.k3) {
+        val = sl->value;
+        hit = 1;
+        break;
+      }
+    }
+  }
+  hit = __shfl_sync(kFull, hit, 0);
+  v = __shfl_sync(kFull, val, 0);
+  return hit != 0;
+}
+
+__device__ __forceinline__ void ring_insert(const DevProblem& P, const RingKey& k, double v) {
+  if ((threadIdx.x & 31) != 0 || !P.ring_cache) return;
+  const unsigned long long h = (k.k1 ^ mix64d(k.k2 ^ k.k3)) & P.ring_mask;
+  for (int pr = 0; pr < 8; ++pr) {
+    RingSlot* sl = P.ring_cache + ((h + pr) & P.ring_mask);
+    const unsigned long long prev = atomicCAS(&sl->k1, 0ULL, k.k1);
+    if (prev == 0) {
+      volatile RingSlot* vs = sl;
+      vs->k2 = k.k2;
+      vs->k3 = k.k3;
+      vs->value = v;
+      __threadfence();
+      vs->state = 1;
+      return;
+    }
+    if (prev == k.k1) return;  // someone else owns this key's slot
+  }
 }
 
 // Exact min-bottleneck Hamiltonian cycle, 3 <= n <= 8 (the reference's
@@ -392,7 +524,8 @@ __device__ __forceinline__ double ecost(const DevProblem& P, const Ws& s, int a,
 // of maxes of the same doubles, so any exact method returns identical bits:
 // bounds first (LB = max over vertices of the 2nd-cheapest incident edge,
 // UB = identity tour), then a lane-parallel DFS over 2-vertex prefixes.
-__device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint8_t* devs, int n) {
+__device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint8_t* devs, int n,
+                                          double volume) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
   for (int e = lane; e < n * n; e += 32) s.rm[e] = ecost(P, s, devs[e / n], devs[e % n]);
@@ -418,6 +551,10 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
   ub = warp_max(ub);
   lb = warp_max(lb);
   if (ub == lb) return ub;
+  (void)volume;
+  const RingKey key = ring_key(P, s, devs, n);
+  double cached;
+  if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
   double best = ub;
   const int m = n - 1;
   const int nprefix = m * (m - 1);
@@ -465,7 +602,10 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
       nxt[d] = 1;
     }
   }
-  return warp_min(best);
+  best = warp_min(best);
+  double stored;
+  if (ring_payload_of(P, s, key, best, stored)) ring_insert(P, key, stored);
+  return best;
 }
 
 // Top-2 (value, position) among edges, excluding positions ex0/ex1.
@@ -689,11 +829,18 @@ __device__ __noinline__ double ring_heuristic(const DevProblem& P, Ws& s, const 
 }
 
 // min_ring_bottleneck (cost_model.cpp:179-207); class costs must be staged.
-__device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8_t* devs, int n) {
+__device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8_t* devs, int n,
+                                         double volume) {
   if (n <= 1) return 0.0;
   if (n == 2) return ecost(P, s, devs[0], devs[1]);
-  if (n <= 8) return ring_small(P, s, devs, n);
-  return ring_heuristic(P, s, devs, n);
+  if (n <= 8) return ring_small(P, s, devs, n, volume);
+  const RingKey key = ring_key(P, s, devs, n);
+  double v;
+  if (ring_lookup(P, key, v)) return ring_payload_value(s, key, v);
+  v = ring_heuristic(P, s, devs, n);
+  double stored;
+  if (ring_payload_of(P, s, key, v, stored)) ring_insert(P, key, stored);
+  return v;
 }
 
 // ---- task_cost_detail (cost_model.cpp:270-396) ----
@@ -764,7 +911,7 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
       for (int c = lane; c < ncell; c += 32) s.rtp[cell0 + c] = ecost(P, s, dv[c * 2], dv[c * 2 + 1]);
     } else {
       for (int c = 0; c < ncell; ++c) {
-        const double r = ring_bottleneck(P, s, dv + c * tp, tp);
+        const double r = ring_bottleneck(P, s, dv + c * tp, tp, cv_tp);
         if (lane == 0) s.rtp[cell0 + c] = r;
       }
     }
@@ -854,12 +1001,17 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
     m_bub = smax(m_bub, bub);
     m_tot = smax(m_tot, training ? stage_max + bub : stage_max);
   }
-  m_comp = warp_max(m_comp);
-  m_tp = warp_max(m_tp);
-  m_pp = warp_max(m_pp);
-  m_hbm = warp_max(m_hbm);
-  m_bub = warp_max(m_bub);
-  m_tot = warp_max(m_tot);
+  for (int o = 16; o > 0; o >>= 1) {  // six independent butterflies, interleaved
+    const double a = __shfl_xor_sync(kFull, m_comp, o), b = __shfl_xor_sync(kFull, m_tp, o),
+                 c = __shfl_xor_sync(kFull, m_pp, o), d = __shfl_xor_sync(kFull, m_hbm, o),
+                 e = __shfl_xor_sync(kFull, m_bub, o), f = __shfl_xor_sync(kFull, m_tot, o);
+    m_comp = smax(m_comp, a);
+    m_tp = smax(m_tp, b);
+    m_pp = smax(m_pp, c);
+    m_hbm = smax(m_hbm, d);
+    m_bub = smax(m_bub, e);
+    m_tot = smax(m_tot, f);
+  }
 
   // phase 3: DP gradient rings over replica peers (training, dp > 1)
   double a_dp = 0.0;
@@ -882,7 +1034,7 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
             __syncwarp();
             for (int i = lane; i < dp; i += 32) s.peers[i] = dv[flat(i, j, k, pp, tp)];
             __syncwarp();
-            const double r = ring_bottleneck(P, s, s.peers, dp);
+            const double r = ring_bottleneck(P, s, s.peers, dp, cv_dp);
             if (lane == 0) {
               s.dpr[k0 + j * tp + k] = r;
               s.dpr_sl[k0 + j * tp + k] = nl_j;

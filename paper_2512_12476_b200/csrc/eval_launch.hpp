@@ -10,6 +10,8 @@
 namespace hpg {
 
 int eval_smem_bytes(const Carve& c);
+// diagnostics: per-plan clock64 phase stamps (5 per plan) or nullptr
+cudaError_t eval_set_plan_profile(long long* d_buf);
 // global scratch (doubles) per CTA of eval_kernel
 int64_t eval_scratch_doubles(int n_dev, int64_t max_nl);
 // persistent grid size for n plans (occupancy-limited, multiple of the SMs)
