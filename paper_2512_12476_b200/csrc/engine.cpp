@@ -2,6 +2,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -388,6 +389,9 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   out.res.resize(n);
   out.off.resize(n);
   if (n == 0) return;
+  static const char* batch_log = std::getenv("HPG_BATCH_LOG");  // diagnostics only
+  const auto bt0 = std::chrono::steady_clock::now();
+  auto bt1 = bt0, bt2 = bt0, bt3 = bt0;
   const Problem& P = ctx.prob;
   Carve cv{};
   cv.n_dev = P.N;
@@ -425,6 +429,7 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   if (want_per_task) ctx.d_per_task.reserve(static_cast<size_t>(n) * P.T * 7);
   if (want_required) ctx.d_required.reserve(static_cast<size_t>(n) * P.N);
   cudaStream_t st = ctx.stream;
+  if (batch_log) bt1 = std::chrono::steady_clock::now();
   cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, in_bytes, cudaMemcpyHostToDevice, st),
              "H2D wave");
   const int64_t* d_off = reinterpret_cast<const int64_t*>(ctx.d_recs.p + in_off);
@@ -440,8 +445,8 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   static const char* plan_prof_log = std::getenv("HPG_PLAN_PROFILE");  // diagnostics only
   long long* d_prof = nullptr;
   if (plan_prof_log) {
-    cuda_check(cudaMalloc(&d_prof, sizeof(long long) * 5 * n), "profile alloc");
-    cuda_check(cudaMemsetAsync(d_prof, 0, sizeof(long long) * 5 * n, st), "profile clear");
+    cuda_check(cudaMalloc(&d_prof, sizeof(long long) * kPlanProfSlots * n), "profile alloc");
+    cuda_check(cudaMemsetAsync(d_prof, 0, sizeof(long long) * kPlanProfSlots * n, st), "profile clear");
     cuda_check(eval_set_plan_profile(d_prof), "profile symbol");
   }
   cuda_check(cudaEventRecord(ctx.ev0, st), "event");
@@ -486,7 +491,9 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   if (want_required)
     cuda_check(cudaMemcpyAsync(out.required.data(), ctx.d_required.p, 8 * out.required.size(),
                                cudaMemcpyDeviceToHost, st), "D2H required");
+  if (batch_log) bt2 = std::chrono::steady_clock::now();
   cuda_check(cudaStreamSynchronize(st), "eval_kernel");
+  if (batch_log) bt3 = std::chrono::steady_clock::now();
   float ms = 0.f;
   cuda_check(cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1), "event time");
   ctx.eval_ms += ms;
@@ -500,8 +507,8 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     }
   }
   if (d_prof) {
-    std::vector<long long> pr(static_cast<size_t>(5) * n);
-    cuda_check(cudaMemcpy(pr.data(), d_prof, sizeof(long long) * 5 * n, cudaMemcpyDeviceToHost),
+    std::vector<long long> pr(static_cast<size_t>(kPlanProfSlots) * n);
+    cuda_check(cudaMemcpy(pr.data(), d_prof, sizeof(long long) * kPlanProfSlots * n, cudaMemcpyDeviceToHost),
                "profile D2H");
     cuda_check(eval_set_plan_profile(nullptr), "profile symbol");
     cudaFree(d_prof);
@@ -509,19 +516,41 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     if (FILE* f = std::fopen(plan_prof_log, "a")) {
       // wave n ms | per plan: mode stage bal_data bal_layers e2e | dp,pp,tp per task
       for (int i = 0; i < n; ++i) {
-        const long long* q = &pr[5 * static_cast<size_t>(i)];
+        const long long* q = &pr[kPlanProfSlots * static_cast<size_t>(i)];
         const long long t1 = q[1] ? q[1] : q[0], t2 = q[2] ? q[2] : t1, t3 = q[3] ? q[3] : t2;
         std::fprintf(f, "%d %d %.4f %d %lld %lld %lld %lld", wave_no, n, ms, b.modes[i], t1 - q[0],
                      t2 - t1, t3 - t2, q[4] - t3);
         const RecHeader& h = b.cands[i]->hdr();
         for (int t = 0; t < P.T; ++t) std::fprintf(f, " %d,%d,%d", h.dp[t], h.pp[t], h.tp[t]);
+        std::fprintf(f, " |");
+        for (int k = 5; k < kPlanProfSlots; ++k) std::fprintf(f, " %lld", q[k]);
         std::fputc('\n', f);
       }
+      std::fclose(f);
+    }
+    unsigned long long acc[32];
+    cuda_check(eval_phase_acc(acc), "phase acc");
+    const std::string acc_path = std::string(plan_prof_log) + ".phases";
+    if (FILE* f = std::fopen(acc_path.c_str(), "w")) {
+      for (int k = 0; k < 32; ++k) std::fprintf(f, "%d %llu\n", k, acc[k]);
       std::fclose(f);
     }
     ++wave_no;
   }
   std::memcpy(out.res.data(), ctx.h_out.p + out_res, sizeof(EvalResult) * n);
+  if (batch_log) {
+    const auto bt4 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) {
+      return std::chrono::duration<double, std::micro>(b - a).count();
+    };
+    if (FILE* f = std::fopen(batch_log, "a")) {
+      // n in_bytes out_bytes pack_us enqueue_us sync_us post_us kernel_ms
+      std::fprintf(f, "%d %lld %lld %.1f %.1f %.1f %.1f %.4f\n", n,
+                   static_cast<long long>(in_bytes), static_cast<long long>(out_bytes),
+                   us(bt0, bt1), us(bt1, bt2), us(bt2, bt3), us(bt3, bt4), ms);
+      std::fclose(f);
+    }
+  }
 }
 
 std::vector<TablePlan> unpack_table(const Problem& P, const hpg_plan_table& t) {

@@ -109,61 +109,121 @@ struct Split {
   }
 };
 
-// task_total_with_split (balance.cpp:61-77) for one split, serially in the
-// calling lane: whole-plan C3 check (only task t's devices can change; the
-// other devices' verdict is `others_ok`), then task_cost(...).total with the
-// task's own weights for dbs. DP rings come from dtab.
-__device__ double trial_total(const DevProblem& P, const DevCostConfig& cfg, const Ws& s,
-                              const TrialCtx& c, const Split& sp, bool others_ok) {
-  if (!others_ok) return kInf;
+// task_total_with_split (balance.cpp:61-77) from per-(stage, layer-count)
+// columns. With the devices, the other tasks' splits and the weights fixed,
+// a trial's pieces depend on each stage's own layer count only:
+//   cflag[j][L]  C3 verdict of stage j's devices at L layers (-1 = unknown;
+//                whole-plan C3 = others_ok AND every stage's verdict)
+//   ccell[j][L]  per replica i: (s4, s3) of cell (i, j) at L layers
+//   dtab[j][L]   DP-ring maximum (training, dp > 1)
+// A trial then reads pp columns; the replica maxima and the sequential bubble
+// sum are evaluated in the reference's order (bit-exact).
+__device__ __forceinline__ double* ccell_of(const Ws& s, int dp, int j, int L) {
+  return s.ccell + static_cast<int64_t>(j * s.dtab_stride + L) * 2 * dp;
+}
+
+// Fills the missing columns among (js[q], Ls[q]), q < nq, with the whole warp.
+__device__ __noinline__ void ensure_cols(const DevProblem& P, const DevCostConfig& cfg, Ws& s,
+                                         const TrialCtx& c, const int* js, const int* Ls,
+                                         int nq) {
+  const int lane = threadIdx.x & 31;
   const int N = P.n_dev;
   const DevTask& tk = P.task[c.t];
   const uint8_t* dv = s.dev + s.o.dev[c.t];
-  const int size = c.dp * c.pp * c.tp;
-  // task t's per-stage memory at the trial split (stages are few in the exact
-  // regime; large greedy pipelines fall back to per-device evaluation)
-  double mmj[8], wmj[8];
-  const bool tab = c.pp <= 8;
-  if (tab) {
-    for (int j = 0; j < c.pp; ++j) {
-      mmj[j] = model_memory_bytes(P, tk, sp[j], c.tp, j, c.pp, cfg);
-      wmj[j] = working_memory_bytes(P, tk, sp[j], c.tp, cfg);
-    }
-  }
-  for (int e = 0; e < size; ++e) {
-    const int d = dv[e];
-    const int j = (e / c.tp) % c.pp;
-    const int L = sp[j];
-    double ms = 0.0, wm = 0.0;
-    for (int u = 0; u < P.n_tasks; ++u) {
-      double m, w;
-      if (u == c.t) {
-        m = tab ? mmj[j] : model_memory_bytes(P, tk, L, c.tp, j, c.pp, cfg);
-        w = tab ? wmj[j] : working_memory_bytes(P, tk, L, c.tp, cfg);
-      } else {
-        const int jj = s.dstage[u * N + d];
-        if (jj == 0xff) continue;
-        m = s.mmt[s.o.sl[u] + jj];
-        w = s.wmt[s.o.sl[u] + jj];
+  const int per = c.dp + c.dp * c.tp;  // cells + devices of one column
+  __syncwarp();
+  int missing = 0;  // bit q: column q to fill (columns are distinct)
+  for (int q = 0; q < nq; ++q)
+    if (s.cflag[js[q] * s.dtab_stride + Ls[q]] < 0) missing |= 1 << q;
+  if (!missing) return;
+  __syncwarp();
+  if (lane == 0)
+    for (int q = 0; q < nq; ++q)
+      if ((missing >> q) & 1) s.cflag[js[q] * s.dtab_stride + Ls[q]] = 1;
+  __syncwarp();
+  for (int it = lane; it < nq * per; it += 32) {
+    const int q = it / per, r = it - q * per;
+    if (!((missing >> q) & 1)) continue;
+    const int j = js[q], L = Ls[q];
+    if (r < c.dp) {
+      double s4, s3;
+      cell_pieces(P, cfg, s, c, r, j, L, s4, s3);
+      double* col = ccell_of(s, c.dp, j, L);
+      col[2 * r] = s4;
+      col[2 * r + 1] = s3;
+    } else {
+      const int e = r - c.dp;  // (replica i, shard k) of stage j
+      const int i = e / c.tp, k = e - (e / c.tp) * c.tp;
+      const int d = dv[flat(i, j, k, c.pp, c.tp)];
+      double ms = 0.0, wm = 0.0;
+      for (int u = 0; u < P.n_tasks; ++u) {
+        double m, w;
+        if (u == c.t) {
+          m = model_memory_bytes(P, tk, L, c.tp, j, c.pp, cfg);
+          w = working_memory_bytes(P, tk, L, c.tp, cfg);
+        } else {
+          const int jj = s.dstage[u * N + d];
+          if (jj == 0xff) continue;
+          m = s.mmt[s.o.sl[u] + jj];
+          w = s.wmt[s.o.sl[u] + jj];
+        }
+        ms += m;
+        wm = smax(wm, w);
       }
-      ms += m;
-      wm = smax(wm, w);
+      if (ms + wm > P.mem[d]) s.cflag[j * s.dtab_stride + L] = 0;
     }
-    if (ms + wm > P.mem[d]) return kInf;
   }
+  __syncwarp();
+}
+
+// One trial from the columns, serially in the calling lane.
+__device__ __forceinline__ double trial_cols(const Ws& s, const TrialCtx& c, const Split& sp,
+                                             bool others_ok) {
+  if (!others_ok) return kInf;
+  for (int j = 0; j < c.pp; ++j)
+    if (s.cflag[j * s.dtab_stride + sp[j]] == 0) return kInf;
   double total = 0.0;
   for (int i = 0; i < c.dp; ++i) {
     double stage_max = 0.0, sum = 0.0;
     for (int j = 0; j < c.pp; ++j) {
-      double s4, s3;
-      cell_pieces(P, cfg, s, c, i, j, sp[j], s4, s3);
-      stage_max = smax(stage_max, s4);
-      if (j >= 1) sum += s3;
+      const double* col = ccell_of(s, c.dp, j, sp[j]);
+      stage_max = smax(stage_max, col[2 * i]);
+      if (j >= 1) sum += col[2 * i + 1];
     }
     const double bub =
         (c.training && c.pp > 1) ? sum / static_cast<double>(s.nm[s.o.w[c.t] + i]) : 0.0;
     total = smax(total, c.training ? stage_max + bub : stage_max);
   }
+  if (c.training) {
+    double dpm = 0.0;
+    if (c.dp > 1) {
+      for (int j = 0; j < c.pp; ++j) dpm = smax(dpm, s.dtab[j * s.dtab_stride + sp[j]]);
+    }
+    total += dpm;
+  }
+  return total;
+}
+
+// One trial from the columns with the replicas spread over the lanes.
+__device__ __forceinline__ double trial_cols_warp(const Ws& s, const TrialCtx& c,
+                                                  const Split& sp, bool others_ok) {
+  if (!others_ok) return kInf;
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < c.pp; ++j)
+    if (s.cflag[j * s.dtab_stride + sp[j]] == 0) return kInf;
+  double total = 0.0;
+  for (int i = lane; i < c.dp; i += 32) {
+    double stage_max = 0.0, sum = 0.0;
+    for (int j = 0; j < c.pp; ++j) {
+      const double* col = ccell_of(s, c.dp, j, sp[j]);
+      stage_max = smax(stage_max, col[2 * i]);
+      if (j >= 1) sum += col[2 * i + 1];
+    }
+    const double bub =
+        (c.training && c.pp > 1) ? sum / static_cast<double>(s.nm[s.o.w[c.t] + i]) : 0.0;
+    total = smax(total, c.training ? stage_max + bub : stage_max);
+  }
+  total = warp_max(total);
   if (c.training) {
     double dpm = 0.0;
     if (c.dp > 1) {
@@ -324,31 +384,53 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
     if (pp < 2 || nl == pp) continue;
     int32_t* sl_t = s.sl + s.o.sl[t];
     const TrialCtx tc = trial_ctx(P, cfg, s, t);
+    HPG_PH_BEGIN(0);
     ensure_geometry(P, s, t);
-    // fresh DP-ring table for this task (devices fixed, volume follows L)
-    if (lane == 0) s.dtab_stride = static_cast<int>(nl) + 1;
+    HPG_PH_END(0);
+    // fresh column tables for this task (devices, weights and the other
+    // tasks' splits stay fixed while its split moves)
+    const int stride = static_cast<int>(nl) + 1;
+    if (lane == 0) {
+      s.dtab_stride = stride;
+      s.cflag = reinterpret_cast<int32_t*>(s.dtab + pp * stride);
+      s.ccell = s.dtab + pp * stride + (pp * stride + 1) / 2;
+    }
     __syncwarp();
     const bool need_dp = tc.training && tc.dp > 1;
-    if (need_dp) {
-      for (int e = lane; e < pp * s.dtab_stride; e += 32) s.dtab[e] = -1.0;
-      __syncwarp();
+    for (int e = lane; e < pp * stride; e += 32) {
+      s.cflag[e] = -1;
+      if (need_dp) s.dtab[e] = -1.0;
     }
+    __syncwarp();
+    HPG_PH_BEGIN(1);
     const bool others = others_fit(P, s, t);
+    HPG_PH_END(1);
     copy_i32(s.split_best, sl_t, pp);
     if (static_cast<int64_t>(pp) * nl <= 64) {
       const int lmax = static_cast<int>(nl) - pp + 1;
+      HPG_PH_BEGIN(2);
       if (need_dp) {
         for (int j = 0; j < pp; ++j)
           for (int L = 1; L <= lmax; ++L) ensure_dtab(P, s, t, j, L);
       }
-      // best = current split (lane 0), then every composition in parallel
-      const uint64_t ntr = binom(static_cast<int>(nl) - 1, pp - 1);
-      double best0 = 0.0;
       {
-        double v = 0.0;
-        if (lane == 0) v = trial_total(P, cfg, s, tc, Split{sl_t, -1, 0, -1, 0}, others);
-        best0 = __shfl_sync(kFull, v, 0);
+        int js[16], Ls[16], nq = 0;
+        for (int j = 0; j < pp; ++j)
+          for (int L = 1; L <= lmax; ++L) {
+            js[nq] = j;
+            Ls[nq] = L;
+            if (++nq == 16) {
+              ensure_cols(P, cfg, s, tc, js, Ls, nq);
+              nq = 0;
+            }
+          }
+        if (nq) ensure_cols(P, cfg, s, tc, js, Ls, nq);
       }
+      HPG_PH_END(2);
+      HPG_PH_BEGIN(3);
+      // best = current split, then every composition, one per lane
+      const uint64_t ntr = binom(static_cast<int>(nl) - 1, pp - 1);
+      const double best0 = trial_cols_warp(s, tc, Split{sl_t, -1, 0, -1, 0}, others);
       double bv = kInf;
       uint64_t br = ~0ull;
       int32_t comp[8];
@@ -356,7 +438,7 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
         const uint64_t r = base + lane;
         if (r < ntr) {
           unrank_composition(r, static_cast<int>(nl), pp, comp);
-          const double v = trial_total(P, cfg, s, tc, Split{comp, -1, 0, -1, 0}, others);
+          const double v = trial_cols(s, tc, Split{comp, -1, 0, -1, 0}, others);
           if (v < bv) {  // first strict minimum within the lane's ranks
             bv = v;
             br = r;
@@ -371,6 +453,8 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
           br = orr;
         }
       }
+      HPG_PH_END(3);
+      HPG_PH_COUNT(28, ntr);
       if (bv < best0) {  // strict improvement over the current split
         if (lane == 0) unrank_composition(br, static_cast<int>(nl), pp, s.split_best);
         __syncwarp();
@@ -378,21 +462,38 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
       bool diff = false;
       for (int j = lane; j < pp; j += 32) diff |= s.split_best[j] != sl_t[j];
       if (__any_sync(kFull, diff)) {
+        HPG_PH_BEGIN(4);
         set_split(P, cfg, s, t, s.split_best);
+        HPG_PH_END(4);
         touched = true;
       }
     } else {
       // greedy: shed one layer from the bottleneck stage to a neighbour; the
-      // candidate is updated in place after every accepted step
+      // candidate is updated in place after every accepted step (its memory
+      // tables and caches are refreshed once, after the walk: nothing in the
+      // walk reads task t's own tables)
       double best = 0.0;
+      bool moved = false;
+      HPG_PH_COUNT(30, 1);
       {
+        HPG_PH_BEGIN(5);
         if (need_dp)
           for (int j = 0; j < pp; ++j) ensure_dtab(P, s, t, j, sl_t[j]);
-        double v = 0.0;
-        if (lane == 0) v = trial_total(P, cfg, s, tc, Split{sl_t, -1, 0, -1, 0}, others);
-        best = __shfl_sync(kFull, v, 0);
+        int js[16], Ls[16];
+        for (int j0 = 0; j0 < pp; j0 += 16) {
+          const int nq = min(16, pp - j0);
+          for (int q = 0; q < nq; ++q) {
+            js[q] = j0 + q;
+            Ls[q] = sl_t[j0 + q];
+          }
+          ensure_cols(P, cfg, s, tc, js, Ls, nq);
+        }
+        best = trial_cols_warp(s, tc, Split{sl_t, -1, 0, -1, 0}, others);
+        HPG_PH_END(5);
       }
       while (true) {
+        HPG_PH_COUNT(27, 1);
+        HPG_PH_BEGIN(6);
         // bottleneck stage: load_j = max_i stage sum, first j with the largest
         double worst = -1.0;
         int bn = 0;
@@ -401,11 +502,8 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
           double load = -kInf;
           if (j < pp) {
             load = 0.0;
-            for (int i = 0; i < tc.dp; ++i) {
-              double s4, s3;
-              cell_pieces(P, cfg, s, tc, i, j, sl_t[j], s4, s3);
-              load = smax(load, s4);
-            }
+            const double* col = ccell_of(s, tc.dp, j, sl_t[j]);
+            for (int i = 0; i < tc.dp; ++i) load = smax(load, col[2 * i]);
           }
           const double m = warp_max(load);
           if (m > worst) {
@@ -414,23 +512,39 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
             bn = j0 + __ffs(bal) - 1;
           }
         }
+        HPG_PH_END(6);
         if (sl_t[bn] <= 1) break;
         const int nbs[2] = {bn - 1, bn + 1};
+        HPG_PH_BEGIN(7);
         if (need_dp) {
           ensure_dtab(P, s, t, bn, sl_t[bn] - 1);
           for (int side = 0; side < 2; ++side)
             if (nbs[side] >= 0 && nbs[side] < pp)
               ensure_dtab(P, s, t, nbs[side], sl_t[nbs[side]] + 1);
         }
-        double v = kInf;
-        if (lane < 2) {
-          const int nb = nbs[lane];
-          if (nb >= 0 && nb < pp) {
-            v = trial_total(P, cfg, s, tc, Split{sl_t, bn, sl_t[bn] - 1, nb, sl_t[nb] + 1},
-                            others);
-          }
+        {
+          int js[3], Ls[3], nq = 0;
+          js[nq] = bn;
+          Ls[nq++] = sl_t[bn] - 1;
+          for (int side = 0; side < 2; ++side)
+            if (nbs[side] >= 0 && nbs[side] < pp) {
+              js[nq] = nbs[side];
+              Ls[nq++] = sl_t[nbs[side]] + 1;
+            }
+          ensure_cols(P, cfg, s, tc, js, Ls, nq);
         }
-        const double c0 = __shfl_sync(kFull, v, 0), c1 = __shfl_sync(kFull, v, 1);
+        HPG_PH_END(7);
+        HPG_PH_BEGIN(8);
+        double cv2[2];
+        for (int side = 0; side < 2; ++side) {
+          const int nb = nbs[side];
+          cv2[side] = (nb >= 0 && nb < pp)
+                          ? trial_cols_warp(s, tc, Split{sl_t, bn, sl_t[bn] - 1, nb, sl_t[nb] + 1},
+                                            others)
+                          : kInf;
+        }
+        const double c0 = cv2[0], c1 = cv2[1];
+        HPG_PH_END(8);
         int pick = -1;
         double step_best = best;
         if (c0 < step_best) {
@@ -446,24 +560,35 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
         const int nb = nbs[pick];
         __syncwarp();
         if (lane == 0) {
-          for (int j = 0; j < pp; ++j) s.split_step[j] = sl_t[j];
-          --s.split_step[bn];
-          ++s.split_step[nb];
+          --sl_t[bn];
+          ++sl_t[nb];
         }
         __syncwarp();
-        set_split(P, cfg, s, t, s.split_step);
+        moved = true;
+      }
+      if (moved) {
+        HPG_PH_BEGIN(9);
+        mem_tables(P, cfg, s, t);
+        invalidate_split(P, s, t);
+        HPG_PH_END(9);
       }
     }
   }
+  HPG_PH_COUNT(29, 1);
   if (!touched) {
     set_all_splits(P, cfg, s, s.sl_save);
     return;
   }
-  if (!check_memory(P, cfg, s)) {
+  HPG_PH_BEGIN(10);
+  const bool mem_ok = check_memory(P, cfg, s);
+  HPG_PH_END(10);
+  if (!mem_ok) {
     set_all_splits(P, cfg, s, s.sl_save);
     return;
   }
+  HPG_PH_BEGIN(11);
   const E2E after = end_to_end(P, cfg, s);
+  HPG_PH_END(11);
   E2E before;
   if (have_cur) {
     before = cur;
@@ -482,9 +607,6 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
     cur = before;
   }
 }
-
-// diagnostics only (HPG_PLAN_PROFILE): per-plan clock64 phase stamps
-__device__ long long* g_plan_prof = nullptr;
 
 __global__ void __launch_bounds__(32)
 eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
@@ -506,8 +628,11 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
     const int64_t rec_at = off ? off[p] : static_cast<int64_t>(p) * stride;
     const uint8_t* rec = recs + rec_at;
     const int mode = modes ? modes[p] : uniform_mode;
-    long long* prof = g_plan_prof ? g_plan_prof + 5 * static_cast<int64_t>(p) : nullptr;
-    if (prof && lane == 0) prof[0] = clock64();
+    long long* prof = g_plan_prof ? g_plan_prof + kPlanProfSlots * static_cast<int64_t>(p) : nullptr;
+    if (prof && lane == 0) {
+      s.prof = prof;
+      prof[0] = clock64();
+    }
     // ---- stage the plan ----
     if (lane < 20) reinterpret_cast<int32_t*>(&s.h)[lane] = reinterpret_cast<const int32_t*>(rec)[lane];
     __syncwarp();
@@ -616,9 +741,14 @@ cudaError_t eval_set_plan_profile(long long* d_buf) {
   return cudaMemcpyToSymbol(dev::g_plan_prof, &d_buf, sizeof(d_buf));
 }
 
+cudaError_t eval_phase_acc(unsigned long long* out16) {
+  return cudaMemcpyFromSymbol(out16, dev::g_phase_acc, 32 * sizeof(unsigned long long));
+}
+
 int64_t eval_scratch_doubles(int n_dev, int64_t max_nl) {
-  // per CTA: DP-ring table [pp <= N][nl + 1]
-  return static_cast<int64_t>(n_dev) * (max_nl + 2);
+  // per CTA (pp * dp <= N): DP-ring table [pp][nl + 1], column verdicts
+  // (int32) [pp][nl + 1] and column cell pieces [pp][nl + 1][dp][2]
+  return 4 * static_cast<int64_t>(n_dev) * (max_nl + 2);
 }
 
 cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid) {

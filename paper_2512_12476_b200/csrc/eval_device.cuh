@@ -76,6 +76,8 @@ struct Ws {
   int32_t* sl_save2;   // [sum pp]
   int32_t* split_step; // [N]
   double* dtab;      // global scratch: DP ring maxima per (stage, layer count), -1 = unknown
+  int32_t* cflag;    // global scratch after dtab: balance_layers column verdicts
+  double* ccell;     // global scratch: balance_layers column cell pieces
   int32_t dtab_stride;
   int64_t nm_base[kMaxTasks];
   int32_t memo_tp_ok;   // bit t
@@ -88,7 +90,28 @@ struct Ws {
   int32_t bridge_ok;
   unsigned long long cc_sig;  // class-cost order signature of the staged volume
   double cc_vol;              // staged volume
+  long long* prof;            // diagnostics: this plan's profile slots
 };
+
+// diagnostics only (HPG_PLAN_PROFILE): per-plan clock64 phase stamps and
+// per-phase cycle accumulators (sub-phase k < 27 also lands in the plan's
+// slot 5 + k)
+__device__ long long* g_plan_prof = nullptr;
+__device__ unsigned long long g_phase_acc[32];
+#define HPG_PH_BEGIN(k) const long long ph_##k = g_plan_prof ? clock64() : 0
+#define HPG_PH_END(k)                                                         \
+  do {                                                                        \
+    if (g_plan_prof && (threadIdx.x & 31) == 0) {                             \
+      const long long dt_ = clock64() - ph_##k;                               \
+      atomicAdd(&g_phase_acc[k], static_cast<unsigned long long>(dt_));       \
+      if (k < 27) s.prof[5 + k] += dt_;                                       \
+    }                                                                         \
+  } while (0)
+#define HPG_PH_COUNT(k, v)                                                    \
+  do {                                                                        \
+    if (g_plan_prof && (threadIdx.x & 31) == 0)                               \
+      atomicAdd(&g_phase_acc[k], static_cast<unsigned long long>(v));         \
+  } while (0)
 
 // The current plan changed: task t's stage split (affects t, the generation
 // task's decoding batch via residency, and memory feasibility) ...
@@ -380,6 +403,7 @@ __device__ __noinline__ bool check_memory(const DevProblem& P, const DevCostConf
 
 __device__ __forceinline__ void class_costs(const DevProblem& P, Ws& s, double volume) {
   const int lane = threadIdx.x & 31;
+  HPG_PH_BEGIN(20);
   __syncwarp();
   for (int c = lane; c < P.n_classes; c += 32) s.cc[c] = P.lat[c] + volume / P.bw[c];
   __syncwarp();
@@ -398,6 +422,7 @@ __device__ __forceinline__ void class_costs(const DevProblem& P, Ws& s, double v
     s.cc_vol = volume;
   }
   __syncwarp();
+  HPG_PH_END(20);
 }
 
 __device__ __forceinline__ double ecost(const DevProblem& P, const Ws& s, int a, int b) {
@@ -829,8 +854,8 @@ __device__ __noinline__ double ring_heuristic(const DevProblem& P, Ws& s, const 
 }
 
 // min_ring_bottleneck (cost_model.cpp:179-207); class costs must be staged.
-__device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8_t* devs, int n,
-                                         double volume) {
+__device__ inline double ring_bottleneck_impl(const DevProblem& P, Ws& s, const uint8_t* devs,
+                                              int n, double volume) {
   if (n <= 1) return 0.0;
   if (n == 2) return ecost(P, s, devs[0], devs[1]);
   if (n <= 8) return ring_small(P, s, devs, n, volume);
@@ -840,6 +865,14 @@ __device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8
   v = ring_heuristic(P, s, devs, n);
   double stored;
   if (ring_payload_of(P, s, key, v, stored)) ring_insert(P, key, stored);
+  return v;
+}
+
+__device__ inline double ring_bottleneck(const DevProblem& P, Ws& s, const uint8_t* devs, int n,
+                                         double volume) {
+  HPG_PH_BEGIN(21);
+  const double v = ring_bottleneck_impl(P, s, devs, n, volume);
+  HPG_PH_END(21);
   return v;
 }
 
@@ -885,6 +918,7 @@ __device__ __forceinline__ double hbm_cell(const DevProblem& P, const DevCostCon
 // bottleneck per (replica, stage) cell and cheapest cross-stage pair.
 __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) {
   const int lane = threadIdx.x & 31;
+  HPG_PH_BEGIN(12);
   const DevTask& tk = P.task[t];
   const int dp = s.h.dp[t], pp = s.h.pp[t], tp = s.h.tp[t];
   const int64_t seq_total = P.seq_in + P.seq_out;
@@ -905,6 +939,7 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
     __syncwarp();
   }
   if (tp > 1 && !((s.memo_tp_ok >> t) & 1)) {
+    HPG_PH_BEGIN(13);
     const double cv_tp = tp_comm_volume(tk.precision_bytes, P.mbs, seq_total, tk.h1, tp);
     class_costs(P, s, cv_tp);
     if (tp == 2) {
@@ -917,8 +952,10 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
     }
     __syncwarp();
     if (lane == 0) s.memo_tp_ok |= 1 << t;
+    HPG_PH_END(13);
   }
   if (pp > 1 && !((s.memo_pp_ok >> t) & 1)) {
+    HPG_PH_BEGIN(14);
     const double cv_pp = pp_comm_volume(tk.precision_bytes, P.mbs, seq_total, tk.h1);
     class_costs(P, s, cv_pp);
     for (int c = lane; c < ncell; c += 32) {
@@ -934,8 +971,10 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
     }
     __syncwarp();
     if (lane == 0) s.memo_pp_ok |= 1 << t;
+    HPG_PH_END(14);
   }
   __syncwarp();
+  HPG_PH_END(12);
 }
 
 __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig& cfg, Ws& s, int t,
@@ -948,6 +987,7 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
   const int64_t* nm = s.nm + s.o.w[t];
   const int cell0 = s.o.cell[t];
   const int ncell = dp * pp;
+  HPG_PH_BEGIN(16);
   ensure_geometry(P, s, t);
 
   const double tpf = tp_pass_factor(tk.kind, cfg.recompute != 0);
@@ -1015,6 +1055,7 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
 
   // phase 3: DP gradient rings over replica peers (training, dp > 1)
   double a_dp = 0.0;
+  HPG_PH_BEGIN(15);
   if (training && dp > 1) {
     const int k0 = s.o.dpk[t];
     for (int j = 0; j < pp; ++j) {
@@ -1046,6 +1087,7 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
       for (int k = 0; k < tp; ++k) a_dp = smax(a_dp, s.dpr[k0 + j * tp + k]);
     }
   }
+  HPG_PH_END(15);
   if (training) m_tot += a_dp;
   agg[0] = m_comp;
   agg[1] = m_tp;
@@ -1055,6 +1097,7 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
   agg[5] = m_hbm;
   agg[6] = m_tot;
   __syncwarp();
+  HPG_PH_END(16);
 }
 
 // aggregate_phi (cost_model.cpp:251-262)
@@ -1079,10 +1122,12 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
   const int lane = threadIdx.x & 31;
   const int N = P.n_dev;
   __syncwarp();
+  HPG_PH_BEGIN(17);
   // weight residency per device, task order (cost_model.cpp:436-448); only the
   // generation task's decoding batch reads it
   const int g = P.gen_slot;
   if (!s.resident_ok && g >= 0 && !((s.agg_ok >> g) & 1)) {
+    HPG_PH_BEGIN(22);
     for (int d = lane; d < N; d += 32) {
       double r = 0.0;
       for (int t = 0; t < P.n_tasks; ++t) {
@@ -1095,6 +1140,7 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
     __syncwarp();
     if (lane == 0) s.resident_ok = 1;
     __syncwarp();
+    HPG_PH_END(22);
   }
   double tot[kMaxTasks];
   for (int t = 0; t < P.n_tasks; ++t) {
@@ -1114,6 +1160,7 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
     transfer = ov;
   } else if (P.gen_slot >= 0 && P.train6_slot >= 0) {
     if (!s.bridge_ok) {
+      HPG_PH_BEGIN(23);
       const DevTask& g = P.task[P.gen_slot];
       const double bytes = static_cast<double>(g.param_count) * g.precision_bytes;
       class_costs(P, s, bytes);
@@ -1130,6 +1177,7 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
         s.bridge_ok = 1;
       }
       __syncwarp();
+      HPG_PH_END(23);
     }
     transfer = s.bridge;
   }
@@ -1155,6 +1203,7 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
     r.e2e = smax(gen, inf + trn) + transfer;
   }
   r.feasible = check_memory(P, cfg, s);
+  HPG_PH_END(17);
   return r;
 }
 

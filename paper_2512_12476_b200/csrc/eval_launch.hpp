@@ -10,8 +10,12 @@
 namespace hpg {
 
 int eval_smem_bytes(const Carve& c);
-// diagnostics: per-plan clock64 phase stamps (5 per plan) or nullptr
+// diagnostics: per-plan clock64 phase stamps (5) + sub-phase
+// cycles (27), or nullptr
+constexpr int kPlanProfSlots = 32;
 cudaError_t eval_set_plan_profile(long long* d_buf);
+// diagnostics: cumulative balance_layers phase cycles / counters (32 slots)
+cudaError_t eval_phase_acc(unsigned long long* out16);
 // global scratch (doubles) per CTA of eval_kernel
 int64_t eval_scratch_doubles(int n_dev, int64_t max_nl);
 // persistent grid size for n plans (occupancy-limited, multiple of the SMs)

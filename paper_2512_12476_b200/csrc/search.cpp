@@ -547,43 +547,95 @@ ArmCoro ga_run(ArmRun& run) {
   }
   if (pop.empty()) co_return;
 
-  // offspring generations
+  // offspring generations. Each offspring is a mutation wave (up to 8 trials
+  // and the unmutated parent, first feasible trial wins) followed by a swap
+  // wave. The next offspring's mutation stage depends on this offspring only
+  // through the RNG position and the population after insertion; both are
+  // known in advance when the swap walk accepts nothing, so its trials ride
+  // along in the swap wave and are used only if that turns out to hold
+  // (exact: the RNG state is compared, everything else follows from it).
+  struct MutStage {
+    std::vector<Cand> cands;  // ntr trials + the unmutated parent
+    std::vector<EvalResult> res;
+    std::vector<Rng> snaps;
+    Rng start, after_all;
+    int ntr = 0;
+  };
+  auto draw_mut = [&](Rng r, const Cand& parent, MutStage& m) {
+    m.cands.clear();
+    m.snaps.clear();
+    m.ntr = 0;
+    for (int tries = 0; tries < 8; ++tries) {
+      Cand trial = parent;
+      if (!mutate(e, trial, r)) break;
+      m.cands.push_back(std::move(trial));
+      m.snaps.push_back(r);
+      ++m.ntr;
+    }
+    m.after_all = r;
+    m.cands.push_back(parent);
+  };
+  // speculative next mutation stage from RNG state r, assuming (child, cost)
+  // is inserted as it stands; appended to req after index base
+  MutStage spec;
+  auto speculate = [&](const Rng& r, const Cand& ch, double ch_cost) {
+    const bool ins =
+        static_cast<int>(pop.size()) < K.population || ch_cost < pop.back().cost;
+    size_t pos = pop.size(), n_spec = pop.size();
+    if (ins) {
+      pos = 0;
+      while (pos < pop.size() && !(pop[pos].cost > ch_cost)) ++pos;
+      n_spec = std::min(pop.size() + 1, static_cast<size_t>(K.population));
+    }
+    Rng rr = r;
+    const size_t i = static_cast<size_t>(rr.bounded(n_spec));
+    const Cand& parent = !ins || i < pos ? pop[i].plan : (i == pos ? ch : pop[i - 1].plan);
+    draw_mut(rr, parent, spec);
+    spec.start = r;
+    for (const Cand& c : spec.cands) req.cands.push_back(c);
+  };
+  auto same_rng = [](const Rng& a, const Rng& b) {
+    return a.seed == b.seed && a.s[0] == b.s[0] && a.s[1] == b.s[1] && a.s[2] == b.s[2] &&
+           a.s[3] == b.s[3];
+  };
+  MutStage cur;
+  bool have_spec = false;
   int64_t streak = 0;
   while (run.used < slice && streak < 64) {
-    Cand child = pop[rng.bounded(pop.size())].plan;
-    req.cands.clear();
-    snaps.clear();
-    int ntr = 0;
-    for (int tries = 0; tries < 8; ++tries) {
-      Cand trial = child;
-      if (!mutate(e, trial, rng)) break;
-      req.cands.push_back(std::move(trial));
-      snaps.push_back(rng);
-      ++ntr;
+    if (have_spec && same_rng(spec.start, rng)) {
+      std::swap(cur, spec);
+    } else {
+      Rng r = rng;
+      const size_t i = static_cast<size_t>(r.bounded(pop.size()));
+      draw_mut(r, pop[i].plan, cur);
+      req.cands = cur.cands;
+      co_await EvalAwait{&req};
+      cur.res = req.res;
+      cur.cands = std::move(req.cands);
     }
-    const Rng after_all = rng;
-    req.cands.push_back(child);  // the unmutated parent, in case no trial fits
-    co_await EvalAwait{&req};
+    have_spec = false;
+    const int ntr = cur.ntr;
     int chosen = -1;
     for (int i = 0; i < ntr; ++i) {
-      if (req.res[i].flags & kResFeasIn) {
+      if (cur.res[i].flags & kResFeasIn) {
         chosen = i;
         break;
       }
     }
+    Cand child;
     double cost;
     if (chosen >= 0) {
-      rng = snaps[chosen];
-      child = std::move(req.cands[chosen]);
-      cost = req.res[chosen].cost;
+      rng = cur.snaps[chosen];
+      child = std::move(cur.cands[chosen]);
+      cost = cur.res[chosen].cost;
     } else {
-      rng = after_all;
-      if (!(req.res[ntr].flags & kResFeasIn)) {
+      rng = cur.after_all;
+      if (!(cur.res[ntr].flags & kResFeasIn)) {
         ++streak;
         continue;
       }
-      child = std::move(req.cands[ntr]);
-      cost = req.res[ntr].cost;
+      child = std::move(cur.cands[ntr]);
+      cost = cur.res[ntr].cost;
     }
     streak = 0;
     score(child, cost);
@@ -623,6 +675,14 @@ ArmCoro ga_run(ArmRun& run) {
       }
       return ng;
     };
+    // keeps the speculative stage at req[base...] if the walk accepted nothing
+    auto take_spec = [&](int base, int w) {
+      if (w != 0) return;
+      const int ns = static_cast<int>(spec.cands.size());
+      spec.res.assign(req.res.begin() + base, req.res.begin() + base + ns);
+      for (int k = 0; k < ns; ++k) spec.cands[k] = std::move(req.cands[base + k]);
+      have_spec = true;
+    };
     if (run.used < slice) {
       req.cands.clear();
       snaps.clear();
@@ -631,21 +691,29 @@ ArmCoro ga_run(ArmRun& run) {
       const int n3 = draw(3, snaps);
       const Rng before5 = rng;
       const int n5 = draw(5, snaps5);
-      if (n3 + n5 > 0) co_await EvalAwait{&req};
-      rng = before5;  // stream position after the level-3 draws (walk may rewind it)
-      const int w3 = walk(0, n3, before3, snaps);
-      if (w3 == 0 && run.used < slice) {
-        rng = before5;
-        walk(n3, n5, before5, snaps5);
-      } else if (w3 == 1 && run.used < slice) {
-        req.cands.clear();
-        snaps5.clear();
-        const Rng b5 = rng;
-        const int m5 = draw(5, snaps5);
-        if (m5 > 0) {
-          co_await EvalAwait{&req};
-          walk(0, m5, b5, snaps5);
+      if (n3 + n5 > 0) {
+        const int base = static_cast<int>(req.cands.size());
+        speculate(n5 > 0 ? snaps5.back() : before5, child, cost);
+        co_await EvalAwait{&req};
+        rng = before5;  // stream position after the level-3 draws (walk may rewind it)
+        const int w3 = walk(0, n3, before3, snaps);
+        if (w3 == 0 && run.used < slice) {
+          rng = before5;
+          take_spec(base, walk(n3, n5, before5, snaps5));
+        } else if (w3 == 1 && run.used < slice) {
+          req.cands.clear();
+          snaps5.clear();
+          const Rng b5 = rng;
+          const int m5 = draw(5, snaps5);
+          if (m5 > 0) {
+            const int base5 = static_cast<int>(req.cands.size());
+            speculate(snaps5.back(), child, cost);
+            co_await EvalAwait{&req};
+            take_spec(base5, walk(0, m5, b5, snaps5));
+          }
         }
+      } else {
+        rng = before5;
       }
     }
     if (static_cast<int>(pop.size()) < K.population || cost < pop.back().cost) {

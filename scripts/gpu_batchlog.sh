@@ -1,0 +1,17 @@
+# per-wave host/transfer/kernel breakdown of run_batch (diagnostics)
+mkdir -p gpurun_out
+for c in ${CFGS:-c2 c3}; do
+HPG_BATCH_LOG=gpurun_out/batchlog_$c.txt timeout 600 python - <<PY
+import sys, time; sys.path.insert(0, '.')
+from paper_2512_12476_b200 import Engine, SearchKnobs, load_topology, load_workflow
+KNOBS = dict(budget=10000, seed=42, population=16, locality_bias=0.8, quantize_gpu_counts=1,
+             level1_filter="off", gg_arm_cap=64, swap_pair_sample=8, balance_data=True,
+             balance_layers=True, balance_seqlen=True, recompute=True)
+e = Engine(load_workflow('fixtures/$c.workflow.json'), load_topology('fixtures/$c.topology.json'))
+for rep in range(2):
+    open('gpurun_out/batchlog_$c.txt', 'a').write('# run %d\n' % rep)
+    t0 = time.perf_counter()
+    r = e.nested_sha_search(SearchKnobs.from_json(KNOBS))
+    print('$c', rep, time.perf_counter() - t0, r.info['eval_kernel_ms'], r.info['batch_ms'], r.info['host_ms'])
+PY
+done
