@@ -108,7 +108,8 @@ struct DevBuf {
     if (n <= cap) return;
     if (p) cudaFree(p);
     p = nullptr;
-    const size_t c = n > cap * 2 ? n : cap * 2;
+    size_t c = n > cap * 2 ? n : cap * 2;
+    if (c * sizeof(T) < (size_t{4} << 20)) c = (size_t{4} << 20) / sizeof(T);
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), c * sizeof(T)), "cudaMalloc");
     cap = c;
   }
@@ -124,7 +125,9 @@ struct HostBuf {  // pinned
     if (n <= cap) return;
     if (p) cudaFreeHost(p);
     p = nullptr;
-    const size_t c = n > cap * 2 ? n : cap * 2;
+    // geometric growth from 4 MiB: pinned allocations are slow, keep them rare
+    size_t c = n > cap * 2 ? n : cap * 2;
+    if (c * sizeof(T) < (size_t{4} << 20)) c = (size_t{4} << 20) / sizeof(T);
     cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&p), c * sizeof(T), cudaHostAllocDefault),
                "cudaHostAlloc");
     cap = c;

@@ -279,11 +279,25 @@ __device__ __noinline__ bool others_fit(const DevProblem& P, const Ws& s, int t)
   return !__any_sync(kFull, viol);
 }
 
+// binomials for the exact split regime (pp * nl <= 64 => n < 64, k <= 6)
+struct BinomTab {
+  uint64_t v[64][8];
+};
+constexpr BinomTab make_binom_tab() {
+  BinomTab t{};
+  for (int n = 0; n < 64; ++n)
+    for (int k = 0; k < 8; ++k) {
+      uint64_t r = k <= n ? 1 : 0;
+      for (int i = 0; i < k && k <= n; ++i) r = r * static_cast<uint64_t>(n - i) / (i + 1);
+      t.v[n][k] = r;
+    }
+  return t;
+}
+__constant__ BinomTab c_binom = make_binom_tab();
+
 __device__ __forceinline__ uint64_t binom(int n, int k) {
   if (k < 0 || n < k) return 0;
-  uint64_t r = 1;
-  for (int i = 0; i < k; ++i) r = r * static_cast<uint64_t>(n - i) / static_cast<uint64_t>(i + 1);
-  return r;
+  return c_binom.v[n & 63][k & 7];  // callers stay inside the table
 }
 
 // r-th composition of nl into pp positive parts in lexicographic order (the

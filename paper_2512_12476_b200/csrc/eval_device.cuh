@@ -26,11 +26,11 @@ constexpr unsigned kFull = 0xffffffffu;
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
 
-__device__ __forceinline__ double warp_max(double v) {
+__device__ __noinline__ double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = smax(v, __shfl_xor_sync(kFull, v, o));
   return v;
 }
-__device__ __forceinline__ double warp_min(double v) {
+__device__ __noinline__ double warp_min(double v) {
   for (int o = 16; o > 0; o >>= 1) v = smin(v, __shfl_xor_sync(kFull, v, o));
   return v;
 }
@@ -89,6 +89,7 @@ struct Ws {
   double bridge;
   int32_t bridge_ok;
   unsigned long long cc_sig;  // class-cost order signature of the staged volume
+  int32_t cc_sig_ok;
   double cc_vol;              // staged volume
   long long* prof;            // diagnostics: this plan's profile slots
 };
@@ -406,10 +407,21 @@ __device__ __forceinline__ void class_costs(const DevProblem& P, Ws& s, double v
   HPG_PH_BEGIN(20);
   __syncwarp();
   for (int c = lane; c < P.n_classes; c += 32) s.cc[c] = P.lat[c] + volume / P.bw[c];
+  if (lane == 0) {
+    s.cc_sig_ok = 0;
+    s.cc_vol = volume;
+  }
   __syncwarp();
-  // order signature: rank of every class cost among all classes (ties share a
-  // rank), 4 bits per class. Every ring algorithm below decides only by
-  // comparing class costs, so equal signatures mean identical decisions.
+  HPG_PH_END(20);
+}
+
+// order signature of the staged class costs (computed on first use): rank of
+// every class cost among all classes (ties share a rank), 4 bits per class.
+// Every ring algorithm below decides only by comparing class costs, so equal
+// signatures mean identical decisions. Warp-collective.
+__device__ __noinline__ unsigned long long cc_signature(const DevProblem& P, Ws& s) {
+  const int lane = threadIdx.x & 31;
+  if (s.cc_sig_ok) return s.cc_sig;
   unsigned long long sig = 0;
   if (P.n_classes <= 16 && lane < P.n_classes) {
     int rank = 0;
@@ -417,12 +429,13 @@ __device__ __forceinline__ void class_costs(const DevProblem& P, Ws& s, double v
     sig = static_cast<unsigned long long>(rank) << (4 * lane);
   }
   for (int o = 16; o > 0; o >>= 1) sig |= __shfl_xor_sync(kFull, sig, o);
+  __syncwarp();
   if (lane == 0) {
     s.cc_sig = sig;
-    s.cc_vol = volume;
+    s.cc_sig_ok = 1;
   }
   __syncwarp();
-  HPG_PH_END(20);
+  return sig;
 }
 
 __device__ __forceinline__ double ecost(const DevProblem& P, const Ws& s, int a, int b) {
@@ -449,12 +462,12 @@ struct RingKey {
 // volume bits (the slot stores the value). Warp-collective.
 constexpr unsigned long long kSigMode = 1ull << 63;
 
-__device__ __forceinline__ RingKey ring_key(const DevProblem& P, const Ws& s,
+__device__ __noinline__ RingKey ring_key(const DevProblem& P, Ws& s,
                                             const uint8_t* devs, int n) {
   const int lane = threadIdx.x & 31;
   RingKey k;
   const bool sig = P.n_classes <= 16;
-  k.k2 = sig ? s.cc_sig : static_cast<unsigned long long>(__double_as_longlong(s.cc_vol));
+  k.k2 = sig ? cc_signature(P, s) : static_cast<unsigned long long>(__double_as_longlong(s.cc_vol));
   const unsigned long long mode = sig ? kSigMode : 0ull;
   if (n <= 8) {
     unsigned long long p = 0;
@@ -500,7 +513,7 @@ __device__ __forceinline__ bool ring_payload_of(const DevProblem& P, const Ws& s
 }
 
 // lane 0 probes; result broadcast. Returns true and sets v on a hit.
-__device__ __forceinline__ bool ring_lookup(const DevProblem& P, const RingKey& k, double& v) {
+__device__ __noinline__ bool ring_lookup(const DevProblem& P, const RingKey& k, double& v) {
   const int lane = threadIdx.x & 31;
   int hit = 0;
   double val = 0.0;
@@ -525,7 +538,7 @@ __device__ __forceinline__ bool ring_lookup(const DevProblem& P, const RingKey& 
   return hit != 0;
 }
 
-__device__ __forceinline__ void ring_insert(const DevProblem& P, const RingKey& k, double v) {
+__device__ __noinline__ void ring_insert(const DevProblem& P, const RingKey& k, double v) {
   if ((threadIdx.x & 31) != 0 || !P.ring_cache) return;
   const unsigned long long h = (k.k1 ^ mix64d(k.k2 ^ k.k3)) & P.ring_mask;
   for (int pr = 0; pr < 8; ++pr) {
@@ -944,6 +957,54 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
     class_costs(P, s, cv_tp);
     if (tp == 2) {
       for (int c = lane; c < ncell; c += 32) s.rtp[cell0 + c] = ecost(P, s, dv[c * 2], dv[c * 2 + 1]);
+    } else if (tp <= 8) {
+      // all cells' ring bounds at once, one lane per (cell, vertex): UB = the
+      // identity tour's largest edge, LB = the largest 2nd-cheapest incident
+      // edge; LB == UB settles the exact ring (ring_small's fast path). Costs
+      // are >= 0, so their bit patterns order like the values (64-bit
+      // atomicMax in the c_comp/c_tp scratch, free until task_cost's cells).
+      unsigned long long* ubb = reinterpret_cast<unsigned long long*>(s.c_comp);
+      unsigned long long* lbb = reinterpret_cast<unsigned long long*>(s.c_tp);
+      for (int c = lane; c < ncell; c += 32) ubb[c] = lbb[c] = 0ull;
+      __syncwarp();
+      for (int it = lane; it < ncell * tp; it += 32) {
+        const int c = it / tp, v = it - (it / tp) * tp;
+        const uint8_t* r = dv + c * tp;
+        const double ub = ecost(P, s, r[v], r[v + 1 < tp ? v + 1 : 0]);
+        double m1 = kInf, m2 = kInf;
+        for (int u = 0; u < tp; ++u) {
+          if (u == v) continue;
+          const double x = ecost(P, s, r[v], r[u]);
+          if (x < m1) {
+            m2 = m1;
+            m1 = x;
+          } else if (x < m2) {
+            m2 = x;
+          }
+        }
+        atomicMax(&ubb[c], static_cast<unsigned long long>(__double_as_longlong(ub)));
+        atomicMax(&lbb[c], static_cast<unsigned long long>(__double_as_longlong(m2)));
+      }
+      __syncwarp();
+      unsigned open = 0;  // cells left to the exact search (rare)
+      for (int c0 = 0; c0 < ncell; c0 += 32) {
+        const int c = c0 + lane;
+        bool o = false;
+        if (c < ncell) {
+          if (ubb[c] == lbb[c]) {
+            s.rtp[cell0 + c] = __longlong_as_double(static_cast<long long>(ubb[c]));
+          } else {
+            o = true;
+          }
+        }
+        open = __ballot_sync(kFull, o);
+        while (open) {
+          const int cc = c0 + __ffs(open) - 1;
+          open &= open - 1;
+          const double r = ring_bottleneck(P, s, dv + cc * tp, tp, cv_tp);
+          if (lane == 0) s.rtp[cell0 + cc] = r;
+        }
+      }
     } else {
       for (int c = 0; c < ncell; ++c) {
         const double r = ring_bottleneck(P, s, dv + c * tp, tp, cv_tp);
@@ -958,15 +1019,24 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
     HPG_PH_BEGIN(14);
     const double cv_pp = pp_comm_volume(tk.precision_bytes, P.mbs, seq_total, tk.h1);
     class_costs(P, s, cv_pp);
-    for (int c = lane; c < ncell; c += 32) {
-      const int j = c % pp;
-      if (j + 1 < pp) {
+    const int tt = tp * tp;
+    if (tt <= 4) {
+      for (int c = lane; c < ncell; c += 32) {
+        if (c % pp + 1 >= pp) continue;
         double best = kInf;
-        const uint8_t* a = dv + c * tp;
-        const uint8_t* b = dv + (c + 1) * tp;
-        for (int x = 0; x < tp; ++x)
-          for (int y = 0; y < tp; ++y) best = smin(best, ecost(P, s, a[x], b[y]));
+        for (int xy = 0; xy < tt; ++xy)
+          best = smin(best, ecost(P, s, dv[c * tp + xy / tp], dv[(c + 1) * tp + xy % tp]));
         s.ppp[cell0 + c] = best;
+      }
+    } else {
+      // cheapest pair per (cell, next stage): the warp over the tp x tp pairs
+      for (int c = 0; c < ncell; ++c) {
+        if (c % pp + 1 >= pp) continue;
+        double best = kInf;
+        for (int xy = lane; xy < tt; xy += 32)
+          best = smin(best, ecost(P, s, dv[c * tp + xy / tp], dv[(c + 1) * tp + xy % tp]));
+        best = warp_min(best);
+        if (lane == 0) s.ppp[cell0 + c] = best;
       }
     }
     __syncwarp();
