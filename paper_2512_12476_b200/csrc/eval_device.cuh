@@ -562,37 +562,43 @@ __device__ __noinline__ void ring_insert(const DevProblem& P, const RingKey& k, 
 // of maxes of the same doubles, so any exact method returns identical bits:
 // bounds first (LB = max over vertices of the 2nd-cheapest incident edge,
 // UB = identity tour), then a lane-parallel DFS over 2-vertex prefixes.
+// ub_known >= 0: the caller already has UB (and knows LB < UB).
 __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint8_t* devs, int n,
-                                          double volume) {
+                                          double ub_known) {
   const int lane = threadIdx.x & 31;
   __syncwarp();
   for (int e = lane; e < n * n; e += 32) s.rm[e] = ecost(P, s, devs[e / n], devs[e % n]);
   __syncwarp();
   const double* rm = s.rm;
   // lane v: its identity-tour edge (UB) and its 2nd-cheapest incident edge (LB)
-  double ub = 0.0, lb = 0.0;
-  if (lane < n) {
-    ub = rm[lane * n + (lane + 1) % n];
-    double m1 = kInf, m2 = kInf;
-    for (int u = 0; u < n; ++u) {
-      if (u == lane) continue;
-      const double c = rm[lane * n + u];
-      if (c < m1) {
-        m2 = m1;
-        m1 = c;
-      } else if (c < m2) {
-        m2 = c;
+  double ub = ub_known, lb = 0.0;
+  if (ub_known < 0.0) {
+    ub = 0.0;
+    if (lane < n) {
+      ub = rm[lane * n + (lane + 1) % n];
+      double m1 = kInf, m2 = kInf;
+      for (int u = 0; u < n; ++u) {
+        if (u == lane) continue;
+        const double c = rm[lane * n + u];
+        if (c < m1) {
+          m2 = m1;
+          m1 = c;
+        } else if (c < m2) {
+          m2 = c;
+        }
       }
+      lb = m2;
     }
-    lb = m2;
+    ub = warp_max(ub);
+    lb = warp_max(lb);
+    if (ub == lb) return ub;
   }
-  ub = warp_max(ub);
-  lb = warp_max(lb);
-  if (ub == lb) return ub;
-  (void)volume;
-  const RingKey key = ring_key(P, s, devs, n);
-  double cached;
-  if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
+  RingKey key;
+  if (P.ring_cache) {
+    key = ring_key(P, s, devs, n);
+    double cached;
+    if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
+  }
   double best = ub;
   const int m = n - 1;
   const int nprefix = m * (m - 1);
@@ -642,7 +648,7 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
   }
   best = warp_min(best);
   double stored;
-  if (ring_payload_of(P, s, key, best, stored)) ring_insert(P, key, stored);
+  if (P.ring_cache && ring_payload_of(P, s, key, best, stored)) ring_insert(P, key, stored);
   return best;
 }
 
@@ -871,7 +877,8 @@ __device__ inline double ring_bottleneck_impl(const DevProblem& P, Ws& s, const 
                                               int n, double volume) {
   if (n <= 1) return 0.0;
   if (n == 2) return ecost(P, s, devs[0], devs[1]);
-  if (n <= 8) return ring_small(P, s, devs, n, volume);
+  if (n <= 8) return ring_small(P, s, devs, n, -1.0);
+  if (!P.ring_cache) return ring_heuristic(P, s, devs, n);
   const RingKey key = ring_key(P, s, devs, n);
   double v;
   if (ring_lookup(P, key, v)) return ring_payload_value(s, key, v);
@@ -1001,7 +1008,8 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
         while (open) {
           const int cc = c0 + __ffs(open) - 1;
           open &= open - 1;
-          const double r = ring_bottleneck(P, s, dv + cc * tp, tp, cv_tp);
+          const double ub = __longlong_as_double(static_cast<long long>(ubb[cc]));
+          const double r = ring_small(P, s, dv + cc * tp, tp, ub);
           if (lane == 0) s.rtp[cell0 + cc] = r;
         }
       }

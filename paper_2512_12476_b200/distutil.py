@@ -38,3 +38,22 @@ def sum_over_ranks(x: float) -> float:
 def shard_of(run_index: int, world: int) -> int:
     """owner rank of a lockstep run (mirror of search.cpp's round-robin deal)"""
     return run_index % world
+
+
+def sweep_range(total: int, rank: int, world: int):
+    """contiguous plan-index shard [k0, k0 + n) of a sweep over `total` plans
+    (independent units, no data-path collective)"""
+    k0 = total * rank // world
+    return k0, total * (rank + 1) // world - k0
+
+
+def merge_argmin(best_cost: float, best_k: int, n_feasible: int):
+    """global (min cost, lowest k) over the ranks' shard results; one
+    all-gather of 24 B per rank. An empty shard reports best_cost = inf."""
+    t = torch.tensor([best_cost, float(best_k), float(n_feasible)], dtype=torch.float64,
+                     device=_dev())
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    rows = [(float(o[0]), int(o[1]), int(o[2])) for o in (x.cpu() for x in out)]
+    best = min(rows, key=lambda r: (r[0], r[1]))
+    return best[0], best[1], sum(r[2] for r in rows)

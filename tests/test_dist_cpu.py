@@ -1,5 +1,6 @@
 """world_size-2 gloo tests (CPU) of the multi-process plumbing the sharded
-search and bench.py use: id broadcast, max/sum over ranks, run ownership."""
+search and bench.py use: id broadcast, max/sum over ranks, run ownership,
+sweep shards and the argmin merge."""
 import os
 import socket
 
@@ -28,7 +29,11 @@ def _worker(rank, world, port, q):
     mx = distutil.max_over_ranks(10.0 * (rank + 1))
     sm = distutil.sum_over_ranks(1.0)
     owned = [r for r in range(10) if distutil.shard_of(r, world) == rank]
-    q.put((rank, got == bytes(range(128)), mx, sm, owned))
+    # sweep sharding: contiguous ranges, argmin merged by (cost, lowest k)
+    k0, n = distutil.sweep_range(1001, rank, world)
+    fake = {0: (5.0, 17, 3), 1: (5.0, 600, 4)}[rank]  # tie on cost -> lowest k wins
+    merged = distutil.merge_argmin(*fake)
+    q.put((rank, got == bytes(range(128)), mx, sm, owned, (k0, n), merged))
     dist.destroy_process_group()
 
 
@@ -47,6 +52,8 @@ def test_gloo_world2_plumbing():
     owned = sorted(i for r in res for i in r[4])
     assert owned == list(range(10))            # every run has exactly one owner
     assert res[0][4] == [0, 2, 4, 6, 8]
+    assert [r[5] for r in res] == [(0, 500), (500, 501)]   # covers [0, 1001) exactly once
+    assert all(r[6] == (5.0, 17, 7) for r in res)
 
 
 @pytest.mark.gpu
