@@ -32,7 +32,7 @@ extern "C" {
 #define HPG_INFEASIBLE 4
 #define HPG_INTERNAL 5
 
-#define HPG_ABI_VERSION 1
+#define HPG_ABI_VERSION 2
 
 /* ---- problem: workflow + topology (workflow.hpp:67-77, topology.hpp:24-104) ---- */
 
@@ -150,6 +150,7 @@ typedef struct {
    * each as a per-task group index (n_tg_override * T entries) */
   int32_t n_tg_override;
   const int32_t* tg_override;
+  double exhaustive_cap;   /* exhaustive_search raw-space cap (search.hpp:35) */
 } hpg_knobs;
 
 typedef struct hpg_ctx hpg_ctx;
@@ -212,6 +213,19 @@ int hpg_search_dist(hpg_ctx* ctx, const hpg_knobs* knobs, int rank, int world,
 int hpg_ga_search(hpg_ctx* ctx, const int32_t* task_group, int32_t n_groups,
                   const int32_t* gpu_counts, int64_t budget_slice, uint64_t rng_seed,
                   const hpg_knobs* knobs, hpg_search_result** out, char* err, size_t errlen);
+
+/* exhaustive_search (search.hpp:137-150, search.cpp:884-1031): every task
+ * grouping x composition x layout x device assignment, deduplicated by
+ * identical-device symmetry, evaluated on the device. Throws (HPG_INPUT) when
+ * exhaustive_space_estimate exceeds knobs->exhaustive_cap. The result's
+ * info.consumed = ExhaustiveResult::explored (unique plans evaluated),
+ * info.budget = raw candidates enumerated; plan/breakdown as for a search
+ * (HPG_INFEASIBLE from hpg_result_plan when no plan fits memory). */
+int hpg_exhaustive(hpg_ctx* ctx, const hpg_knobs* knobs, hpg_search_result** out, char* err,
+                   size_t errlen);
+/* exhaustive_space_estimate (search.hpp:153-155, search.cpp:851-882) */
+int hpg_exhaustive_estimate(hpg_ctx* ctx, const hpg_knobs* knobs, double* estimate, char* err,
+                            size_t errlen);
 
 /* SearchResult / SearchState accessors (search.hpp:79-111) */
 typedef struct {

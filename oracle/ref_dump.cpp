@@ -12,6 +12,7 @@
 //   fuzz SEED N OUT                      acceptance-#1-style random instances
 //   search WF TOPO BUDGET SEED OUT [knobs.json]   nested_sha_search + survivor replay
 //   searchfuzz SEED N OUT                tiny random searches (acceptance #3/#4 style)
+//   exhaustive SEED N OUT                exhaustive_search goldens (acceptance #2 + fuzz)
 //   sweep WF TOPO SEED K0 COUNT OUT      config-5 generator
 //   time_search WF TOPO BUDGET SEED [knobs.json]  one timed search, JSON line
 //   time_sweep WF TOPO SEED K0 COUNT THREADS      timed sweep sample, JSON line
@@ -19,6 +20,7 @@
 #include <chrono>
 #include <cinttypes>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <functional>
@@ -848,6 +850,156 @@ int cmd_searchfuzz(std::uint64_t seed, int n, const std::string& out) {
   return all_ok ? 0 : 1;
 }
 
+// ---- exhaustive_search goldens (search.cpp:837-1031; acceptance #2) ----
+
+json exh_record(const std::string& name, const WorkflowGraph& wf, const DeviceTopology& topo,
+                const SearchKnobs& k) {
+  json r;
+  r["name"] = name;
+  r["workflow"] = workflow_json(wf);
+  r["topology"] = topology_json(topo);
+  r["knobs"] = knobs_json(k);
+  r["exhaustive_cap"] = hx(k.exhaustive_cap);
+  r["estimate"] = hx(exhaustive_space_estimate(wf, topo, k));
+  try {
+    const auto t0 = std::chrono::steady_clock::now();
+    const ExhaustiveResult ex = exhaustive_search(wf, topo, k);
+    if (std::getenv("HPG_REF_TIMING"))  // timing probes only, not in the goldens
+      r["ref_wall_s"] =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r["explored"] = ex.explored;
+    r["cost"] = hx(ex.cost);
+    r["has_plan"] = ex.plan.has_value();
+    if (ex.plan) {
+      r["plan"] = plan_json(*ex.plan, topo);
+      r["breakdown"] = breakdown_json(ex.breakdown);
+    }
+  } catch (const InputError& e) {
+    r["error"] = e.what();
+  }
+  return r;
+}
+
+// two regions x two single-GPU nodes (the level-5 swap / SHA test fixture shape)
+DeviceTopology two_region_pairs() {
+  std::vector<Device> devs(4);
+  for (int i = 0; i < 4; ++i) {
+    Device& d = devs[i];
+    d.id = "dev-" + std::to_string(i);
+    d.gpu_model = "synthetic";
+    d.comp_tflops = 10;
+    d.mem_gb = 640;
+    d.hbm_gbps = 1000;
+    d.intra_node_gbps = 600;
+    d.region = i < 2 ? "east" : "west";
+    d.node = d.region + "-n" + std::to_string(i % 2);
+  }
+  return DeviceTopology::make(devs, {{"east", "west", 50.0, 1.0}}, TopologyDefaults{0.05, 100.0});
+}
+
+int cmd_exhaustive(std::uint64_t seed, int n_fuzz, const std::string& out) {
+  json recs = json::array();
+  auto quiet = [](std::int64_t budget, std::uint64_t s) {
+    SearchKnobs k;
+    k.budget = budget;
+    k.seed = s;
+    k.balance_data = false;
+    k.balance_layers = false;
+    return k;
+  };
+  // acceptance #2's twenty instances (acceptance.cpp:116-141)
+  for (int i = 0; i < 20; ++i) {
+    Rng rng(5000 + i);
+    std::map<int, ModelSpec> models;
+    if (i % 4 == 0) {
+      models[6] = testutil::tiny_model(8, 16, 2 + i % 3);
+    } else if (i % 4 == 1) {
+      models[2] = testutil::tiny_model(8, 16, 2);
+      models[6] = testutil::tiny_model(8, 16, 4);
+    } else if (i % 4 == 2) {
+      models[1] = testutil::tiny_model(8, 16, 2);
+      models[6] = testutil::tiny_model(8, 16, 2);
+    } else {
+      models[2] = testutil::tiny_model(8, 16, 2);
+      models[3] = testutil::tiny_model(16, 32, 2);
+    }
+    const auto wf = testutil::subset_workflow_models(
+        models, testutil::tiny_batch(4, 1, 8, 4, 1),
+        i % 2 == 0 ? RunMode::kSync : RunMode::kAsync, 0.25);
+    const int n_devices = 2 + static_cast<int>(rng.bounded(3));
+    const DeviceTopology topo = i % 3 == 0
+                                    ? testutil::uniform_topology(n_devices, 1e13, 1e12, 64.0, 2)
+                                    : testutil::random_topology(rng, 4);
+    recs.push_back(exh_record("acc2_" + std::to_string(i), wf, topo, quiet(0, 0)));
+  }
+  // test_search.cpp:284-320 shapes, the two-region fixture, the cap guard
+  recs.push_back(exh_record(
+      "one_task_one_device",
+      testutil::subset_workflow({2}, testutil::tiny_model(4, 8, 2), testutil::tiny_batch()),
+      testutil::uniform_topology(1, 1e13, 1e12, 64.0, 1), quiet(0, 0)));
+  recs.push_back(exh_record(
+      "train_two_same_node",
+      testutil::subset_workflow({6}, testutil::tiny_model(4, 8, 2), testutil::tiny_batch()),
+      testutil::uniform_topology(2, 1e13, 1e12, 64.0, 2), quiet(0, 0)));
+  recs.push_back(exh_record("cap_guard",
+                            testutil::subset_workflow({1, 2, 6}, testutil::tiny_model(4, 8, 2),
+                                                      testutil::tiny_batch()),
+                            testutil::uniform_topology(16, 1e13, 1e12, 64.0, 8), quiet(0, 0)));
+  recs.push_back(exh_record(
+      "two_region_train",
+      testutil::subset_workflow({6}, testutil::tiny_model(8, 16, 2),
+                                testutil::tiny_batch(8, 1, 16, 0, 1)),
+      two_region_pairs(), quiet(0, 0)));
+  {
+    std::map<int, ModelSpec> models{{2, testutil::tiny_model(8, 16, 2)},
+                                    {6, testutil::tiny_model(8, 16, 4)}};
+    recs.push_back(exh_record("two_region_pair",
+                              testutil::subset_workflow_models(
+                                  models, testutil::tiny_batch(4, 1, 8, 0, 1), RunMode::kSync, 0.0),
+                              two_region_pairs(), quiet(0, 0)));
+  }
+  // fuzz: random workflows on small random / uniform / duplicated-type pools
+  Rng rng(seed);
+  for (int i = 0; i < n_fuzz; ++i) {
+    WorkflowGraph wf = random_workflow(rng);
+    DeviceTopology topo;
+    const int shape = static_cast<int>(rng.bounded(3));
+    if (shape == 0) {
+      topo = testutil::random_topology(rng, 5);
+    } else if (shape == 1) {
+      topo = testutil::uniform_topology(1 + static_cast<int>(rng.bounded(6)),
+                                        rng.uniform(1e12, 4e14), rng.uniform(1e11, 3e12),
+                                        rng.uniform(8.0, 96.0), 1 + static_cast<int>(rng.bounded(4)));
+    } else {
+      // two device types over two nodes (symmetry classes with repeats)
+      const int n = 2 + static_cast<int>(rng.bounded(5));
+      std::vector<Device> devs(n);
+      for (int d = 0; d < n; ++d) {
+        Device& x = devs[d];
+        x.id = "g" + std::to_string(d);
+        const bool big = rng.bounded(2) == 0;
+        x.gpu_model = big ? "big" : "small";
+        x.comp_tflops = big ? 312.0 : 181.0;
+        x.mem_gb = big ? 80.0 : 48.0;
+        x.hbm_gbps = big ? 2039.0 : 864.0;
+        x.intra_node_gbps = big ? 600.0 : 64.0;
+        x.region = "r0";
+        x.node = "n" + std::to_string(rng.bounded(2));
+      }
+      topo = DeviceTopology::make(devs, {}, TopologyDefaults{0.1, 100.0});
+    }
+    SearchKnobs k = quiet(0, 0);
+    k.recompute = rng.bounded(2) == 0;
+    if (rng.bounded(4) == 0) k.reshard_override = rng.uniform(0.0, 2.0);
+    if (rng.bounded(4) == 0) k.sync_override = rng.uniform(0.0, 2.0);
+    if (rng.bounded(3) == 0) k.exhaustive_cap = 1e4 * (1 + static_cast<double>(rng.bounded(100)));
+    recs.push_back(exh_record("fuzz_" + std::to_string(i), wf, topo, k));
+  }
+  write_file(out, json{{"records", recs}}.dump() + "\n");
+  std::printf("wrote %zu exhaustive records to %s\n", recs.size(), out.c_str());
+  return 0;
+}
+
 struct SweepStats {
   std::uint64_t feasible = 0;
   double best = std::numeric_limits<double>::infinity();
@@ -989,6 +1141,7 @@ int main(int argc, char** argv) {
       return cmd_search(arg(2), arg(3), std::stoll(arg(4)), std::stoull(arg(5)), arg(6),
                         argc > 7 ? argv[7] : "");
     if (cmd == "searchfuzz") return cmd_searchfuzz(std::stoull(arg(2)), std::stoi(arg(3)), arg(4));
+    if (cmd == "exhaustive") return cmd_exhaustive(std::stoull(arg(2)), std::stoi(arg(3)), arg(4));
     if (cmd == "sweep")
       return cmd_sweep(arg(2), arg(3), std::stoull(arg(4)), std::stoull(arg(5)),
                        std::stoull(arg(6)), arg(7));

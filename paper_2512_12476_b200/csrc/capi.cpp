@@ -79,6 +79,7 @@ void hpg_knobs_default(hpg_knobs* k) {
   k->sync_override = -1.0;
   k->n_tg_override = 0;
   k->tg_override = nullptr;
+  k->exhaustive_cap = 1e6;
 }
 
 int hpg_create(const hpg_problem* problem, int cuda_device, hpg_ctx** out, char* err,

@@ -310,6 +310,26 @@ int hpg_ga_search(hpg_ctx* ctx, const int32_t* task_group, int32_t n_groups,
   });
 }
 
+int hpg_exhaustive(hpg_ctx* ctx, const hpg_knobs* knobs, hpg_search_result** out, char* err,
+                   size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl || !knobs || !out) throw UsageError("hpg_exhaustive: null argument");
+    *out = nullptr;
+    Ctx& C = *ctx->impl;
+    *out = wrap(exhaustive_search(C, knobs_from_c(C.prob, *knobs)), C.prob);
+  });
+}
+
+int hpg_exhaustive_estimate(hpg_ctx* ctx, const hpg_knobs* knobs, double* estimate, char* err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl || !knobs || !estimate)
+      throw UsageError("hpg_exhaustive_estimate: null argument");
+    Ctx& C = *ctx->impl;
+    *estimate = exhaustive_space_estimate(C.prob, knobs_from_c(C.prob, *knobs));
+  });
+}
+
 int hpg_result_info(const hpg_search_result* r, hpg_search_info* info) {
   if (!r || !info) return HPG_USAGE;
   const SearchOut& o = r->out;
@@ -417,7 +437,7 @@ int hpg_result_plan(const hpg_search_result* r, hpg_plan_table* plan, int32_t* g
   if (groups_flat) std::copy(r->groups_flat.begin(), r->groups_flat.end(), groups_flat);
   if (estimated_cost_s) *estimated_cost_s = r->out.est_cost;
   if (prov_seed) *prov_seed = r->out.seed;
-  if (prov_budget) *prov_budget = r->out.consumed;
+  if (prov_budget) *prov_budget = r->out.prov_budget >= 0 ? r->out.prov_budget : r->out.consumed;
   return HPG_OK;
 }
 

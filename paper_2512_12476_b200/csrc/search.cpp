@@ -62,6 +62,7 @@ Knobs knobs_from_c(const Problem& P, const hpg_knobs& k) {
   o.recompute = k.recompute != 0;
   o.reshard_override = k.reshard_override;
   o.sync_override = k.sync_override;
+  o.exhaustive_cap = k.exhaustive_cap;
   // parse_knobs_json validation (search.cpp:75-83)
   if (o.population < 1 || o.swap_pair_sample < 0 || o.gg_arm_cap < 1)
     throw InputError("knobs: population and gg_arm_cap must be >= 1");

@@ -38,6 +38,7 @@ struct Knobs {
   bool recompute = true;
   double reshard_override = -1.0;
   double sync_override = -1.0;
+  double exhaustive_cap = 1e6;
   bool has_tg_override = false;
   std::vector<std::vector<std::vector<int>>> tg_override;  // groups of task slots
   DevCostConfig cost_config() const;  // SearchKnobs::cost_config (search.cpp:38-44)
@@ -72,6 +73,7 @@ struct SearchOut {
   Grouping plan_groups;
   std::vector<int> plan_counts;
   double est_cost = -1.0;
+  int64_t prov_budget = -1;      // plan provenance budget; -1 = consumed
   std::vector<double> per_task;  // T*7
   double reshard_s = 0, sync_s = 0, e2e = 0;
   bool feasible = true;
@@ -84,6 +86,11 @@ struct SearchOut {
 SearchOut nested_sha_search(Ctx& ctx, const Knobs& k, Dist* dist);
 SearchOut ga_search(Ctx& ctx, const Grouping& tg, const std::vector<int>& counts, int64_t slice,
                     uint64_t seed, const Knobs& k);
+// exhaustive_search / exhaustive_space_estimate (search.cpp:837-1031) on the
+// device; SearchOut.consumed = unique plans evaluated (ExhaustiveResult::
+// explored), SearchOut.budget = raw candidates enumerated
+SearchOut exhaustive_search(Ctx& ctx, const Knobs& k);
+double exhaustive_space_estimate(const Problem& P, const Knobs& k);
 
 // enumerations (search.cpp:97-150, combinatorics.cpp:10-146)
 std::vector<Grouping> enumerate_task_groupings(const Problem& P, bool adjacent);

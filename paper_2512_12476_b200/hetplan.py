@@ -131,7 +131,8 @@ class _Knobs(C.Structure):
                 ("balance_data", C.c_int32), ("balance_layers", C.c_int32),
                 ("balance_seqlen", C.c_int32), ("recompute", C.c_int32),
                 ("reshard_override", C.c_double), ("sync_override", C.c_double),
-                ("n_tg_override", C.c_int32), ("tg_override", C.POINTER(C.c_int32))]
+                ("n_tg_override", C.c_int32), ("tg_override", C.POINTER(C.c_int32)),
+                ("exhaustive_cap", C.c_double)]
 
 
 class _SearchInfo(C.Structure):
@@ -163,7 +164,7 @@ EXPORTED_SYMBOLS = [
     "hpg_result_info", "hpg_result_b_m", "hpg_result_trace", "hpg_result_arms",
     "hpg_result_halvings", "hpg_result_survivor_sizes", "hpg_result_survivors",
     "hpg_result_plan", "hpg_result_breakdown", "hpg_result_free", "hpg_sweep",
-    "hpg_sweep_resident",
+    "hpg_sweep_resident", "hpg_exhaustive", "hpg_exhaustive_estimate",
 ]
 
 
@@ -198,6 +199,8 @@ def load_library(path: str = LIB_PATH):
                                       P(C.c_void_p), E, L]),
         "hpg_ga_search": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int32, P(C.c_int32),
                                     C.c_int64, C.c_uint64, P(_Knobs), P(C.c_void_p), E, L]),
+        "hpg_exhaustive": (C.c_int, [C.c_void_p, P(_Knobs), P(C.c_void_p), E, L]),
+        "hpg_exhaustive_estimate": (C.c_int, [C.c_void_p, P(_Knobs), P(C.c_double), E, L]),
         "hpg_result_info": (C.c_int, [C.c_void_p, P(_SearchInfo)]),
         "hpg_result_b_m": (C.c_int, [C.c_void_p, P(C.c_int64)]),
         "hpg_result_trace": (C.c_int, [C.c_void_p, P(C.c_int64), P(C.c_double)]),
@@ -399,6 +402,7 @@ class SearchKnobs:
     recompute: bool = True
     reshard_override: float = -1.0
     sync_override: float = -1.0
+    exhaustive_cap: float = 1e6
 
     @staticmethod
     def from_json(obj: dict) -> "SearchKnobs":
@@ -642,6 +646,7 @@ class Engine:
         kn.balance_data, kn.balance_layers = int(k.balance_data), int(k.balance_layers)
         kn.balance_seqlen, kn.recompute = int(k.balance_seqlen), int(k.recompute)
         kn.reshard_override, kn.sync_override = k.reshard_override, k.sync_override
+        kn.exhaustive_cap = k.exhaustive_cap
         keep = None
         if tg_override:
             ids = self.wf.task_ids
@@ -691,6 +696,26 @@ class Engine:
                                     C.byref(kn), C.byref(r), err, 1024)
         _raise(rc, err)
         return SearchResult(self, r)
+
+    # ---- exhaustive oracle (search.hpp:137-155) ----
+
+    def exhaustive_search(self, knobs: SearchKnobs) -> "SearchResult":
+        """exhaustive_search on the device; result.info["consumed"] = explored
+        (unique plans evaluated), result.info["budget"] = raw candidates."""
+        kn, keep = self._knobs(knobs)
+        r = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = self.lib.hpg_exhaustive(self._h, C.byref(kn), C.byref(r), err, 1024)
+        _raise(rc, err)
+        return SearchResult(self, r)
+
+    def exhaustive_space_estimate(self, knobs: SearchKnobs) -> float:
+        kn, keep = self._knobs(knobs)
+        est = C.c_double()
+        err = C.create_string_buffer(1024)
+        _raise(self.lib.hpg_exhaustive_estimate(self._h, C.byref(kn), C.byref(est), err, 1024),
+               err)
+        return est.value
 
     # ---- config-5 sweep ----
 

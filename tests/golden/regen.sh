@@ -1,0 +1,32 @@
+#!/usr/bin/env bash
+# Regenerates every golden fixture in tests/golden/ from the UNMODIFIED
+# reference planner (compiled from /root/reference by oracle/Makefile into
+# oracle/_ref/ref_dump). Runs in the build container only (needs
+# /root/reference); the GPU box uses the committed JSON.
+set -euo pipefail
+cd "$(dirname "$0")/../.."
+make -C oracle ref
+R=oracle/_ref/ref_dump
+G=tests/golden
+KNOBS=/root/reference/proj/samples/knobs.json
+for c in c1 c2; do
+  $R evalplans fixtures/$c.workflow.json fixtures/$c.topology.json 42 60 $G/evalplans_$c.json
+done
+for c in c3 c4; do
+  $R evalplans fixtures/$c.workflow.json fixtures/$c.topology.json 42 24 $G/evalplans_$c.json
+done
+$R fuzz 20251018 250 $G/fuzz_eval.json
+$R search fixtures/c1.workflow.json fixtures/c1.topology.json 1000 42 $G/search_c1_b1000.json $KNOBS
+$R search fixtures/c2.workflow.json fixtures/c2.topology.json 1000 42 $G/search_c2_b1000.json $KNOBS
+$R searchfuzz 777 60 $G/searchfuzz.json
+$R sweep fixtures/c4.workflow.json fixtures/c4.topology.json 42 0 2000 $G/sweep_c4.json
+$R exhaustive 4242 40 $G/exhaustive.json
+python3 - <<'PY'
+import json, subprocess
+out = {}
+for seed in ("42", "0", "18446744073709551615", "20251018"):
+    r = subprocess.run(["oracle/_ref/ref_dump", "rngpin", seed], capture_output=True, text=True,
+                       check=True)
+    out[seed] = r.stdout.strip().splitlines()
+json.dump(out, open("tests/golden/rng_pin.json", "w"), indent=1)
+PY

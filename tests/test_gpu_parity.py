@@ -173,3 +173,45 @@ def test_sweep_c4_bit_exact():
     assert out["n_feasible"] == g["n_feasible"]
     if g["n_feasible"]:
         assert out["best_k"] == g["best_k"] and same(out["best_cost"], hx(g["best"]))
+
+
+def test_exhaustive_identical():
+    """exhaustive_search on the device vs the reference (acceptance #2's twenty
+    instances, test_search.cpp's tiny cases, the cap guard and 40 random
+    pools): explored count, estimate, chosen plan, cost bits and breakdown,
+    or the identical InputError when the estimate exceeds the cap."""
+    from paper_2512_12476_b200 import InputError, SearchKnobs
+    g = load("exhaustive.json")
+    bad = []
+    for r in g["records"]:
+        obj = dict(r["knobs"])
+        obj["exhaustive_cap"] = r["exhaustive_cap"]
+        knobs = SearchKnobs.from_json(obj)
+        with _engine(r["workflow"], r["topology"]) as eng:
+            est = eng.exhaustive_space_estimate(knobs)
+            if not same(est, hx(r["estimate"])):
+                bad.append(f"{r['name']}: estimate {est!r} != {hx(r['estimate'])!r}")
+            if "error" in r:
+                try:
+                    eng.exhaustive_search(knobs)
+                    bad.append(f"{r['name']}: expected InputError")
+                except InputError as e:
+                    if r["error"] not in str(e):
+                        bad.append(f"{r['name']}: error {e} != {r['error']}")
+                continue
+            res = eng.exhaustive_search(knobs)
+        if res.info["consumed"] != r["explored"]:
+            bad.append(f"{r['name']}: explored {res.info['consumed']} != {r['explored']}")
+        if bool(res.plan) != bool(r["has_plan"]):
+            bad.append(f"{r['name']}: has_plan {bool(res.plan)}")
+            continue
+        if res.plan:
+            bad += _check_plan_eq(res.plan, r["plan"], r["name"])
+            bad += check_breakdown(res.breakdown, r["breakdown"], r["name"])
+            if not same(res.breakdown["end_to_end_s"], hx(r["cost"])):
+                bad.append(f"{r['name']}: cost {res.breakdown['end_to_end_s']!r}")
+            if not same(res.plan["estimated_cost_s"], hx(r["plan"]["estimated_cost_s"])):
+                bad.append(f"{r['name']}: estimated_cost_s")
+            if res.plan["provenance"]["budget"] != r["plan"]["provenance"]["budget"]:
+                bad.append(f"{r['name']}: provenance budget")
+    assert not bad, "\n".join(bad[:30])
