@@ -140,6 +140,7 @@ enum EvalMode : int32_t {
   kModeBalanceData = 3,  // balance_data (balance.cpp:37-56) only
   kModeBalanceLayers = 4,  // balance_layers (balance.cpp:81-167) only
   kModeChain = 5,        // balance_data -> balance_layers -> e2e, no C3 gate
+  kModeSkip = 6,         // no plan in this slot: result {cost -1, flags 0}
 };
 
 // Per-plan result slot.

@@ -180,6 +180,11 @@ struct Ctx {
   DevBuf<double> d_scratch;  // per-CTA global scratch of eval_kernel
   DevBuf<uint8_t> d_ring;    // device-wide ring memo (RingSlot table)
   DevBuf<uint8_t> d_xch_send, d_xch_recv;  // multi-GPU record exchange
+  // exhaustive_search block buffers (keys, dedup table, slots, records, ...)
+  DevBuf<uint8_t> d_exh_keys, d_exh_recs;
+  DevBuf<unsigned long long> d_exh_table, d_exh_slot, d_exh_count;
+  DevBuf<EvalResult> d_exh_res;
+  DevBuf<uint8_t> d_exh_part;
   Dist dist;                               // world 1 until hpg_search_dist attaches
   int64_t max_nl = 1;
   // sweep

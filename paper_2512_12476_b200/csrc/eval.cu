@@ -642,6 +642,10 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
     const int64_t rec_at = off ? off[p] : static_cast<int64_t>(p) * stride;
     const uint8_t* rec = recs + rec_at;
     const int mode = modes ? modes[p] : uniform_mode;
+    if (mode == kModeSkip) {
+      if (lane == 0) res[p] = EvalResult{-1.0, 0.0, 0.0, 0, 0};
+      continue;
+    }
     long long* prof = g_plan_prof ? g_plan_prof + kPlanProfSlots * static_cast<int64_t>(p) : nullptr;
     if (prof && lane == 0) {
       s.prof = prof;

@@ -91,15 +91,19 @@ __global__ void exh_insert_kernel(ExhBlock B, uint64_t n, const uint8_t* __restr
 }
 
 // first occurrences -> compact plan records (unit weights, make_layout split)
+// in their own slot; every other slot is marked skip
 __global__ void exh_rep_kernel(ExhBlock B, uint64_t n, const unsigned long long* __restrict__ table,
                                const unsigned long long* __restrict__ slot,
-                               uint8_t* __restrict__ recs, unsigned long long* __restrict__ ridx,
+                               uint8_t* __restrict__ recs, int32_t* __restrict__ modes,
                                unsigned long long* __restrict__ count) {
   const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool rep = idx < n && table[slot[idx]] == idx;
+  const unsigned ballot = __ballot_sync(0xffffffffu, rep);
+  if ((threadIdx.x & 31) == 0 && ballot) atomicAdd(count, static_cast<unsigned long long>(__popc(ballot)));
   if (idx >= n) return;
-  if (table[slot[idx]] != idx) return;
-  const unsigned long long pos = atomicAdd(count, 1ull);
-  ridx[pos] = idx;
+  modes[idx] = rep ? kModeE2E : kModeSkip;
+  if (!rep) return;
+  const uint64_t pos = idx;
   int oi[kMaxTasks];
   uint8_t devs[kMaxTasks * kExhMaxDevices];
   exh_decode(B, idx, oi, devs);
@@ -129,8 +133,7 @@ __global__ void exh_rep_kernel(ExhBlock B, uint64_t n, const unsigned long long*
 }
 
 // argmin over memory-feasible representatives by (cost, raw index)
-__global__ void exh_reduce_kernel(const EvalResult* __restrict__ res,
-                                  const unsigned long long* __restrict__ ridx, int64_t n,
+__global__ void exh_reduce_kernel(const EvalResult* __restrict__ res, int64_t n,
                                   ExhPartial* __restrict__ out) {
   double best = kInf;
   unsigned long long bi = ~0ull;
@@ -138,7 +141,7 @@ __global__ void exh_reduce_kernel(const EvalResult* __restrict__ res,
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const EvalResult r = res[i];
     if (!(r.flags & kResFeasIn)) continue;
-    const unsigned long long k = ridx[i];
+    const unsigned long long k = static_cast<unsigned long long>(i);
     if (r.cost < best || (r.cost == best && k < bi)) {
       best = r.cost;
       bi = k;
@@ -189,18 +192,17 @@ cudaError_t launch_exh_insert(const ExhBlock& B, uint64_t n, const uint8_t* d_ke
 }
 
 cudaError_t launch_exh_reps(const ExhBlock& B, uint64_t n, const unsigned long long* d_table,
-                            const unsigned long long* d_slot, uint8_t* d_recs,
-                            unsigned long long* d_ridx, unsigned long long* d_count,
-                            cudaStream_t st) {
+                            const unsigned long long* d_slot, uint8_t* d_recs, int32_t* d_modes,
+                            unsigned long long* d_count, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
-  dev::exh_rep_kernel<<<blocks_for(n, 128), 128, 0, st>>>(B, n, d_table, d_slot, d_recs, d_ridx,
+  dev::exh_rep_kernel<<<blocks_for(n, 128), 128, 0, st>>>(B, n, d_table, d_slot, d_recs, d_modes,
                                                           d_count);
   return cudaGetLastError();
 }
 
-cudaError_t launch_exh_reduce(const EvalResult* d_res, const unsigned long long* d_ridx,
-                              int64_t n, ExhPartial* d_out, int blocks, cudaStream_t st) {
-  dev::exh_reduce_kernel<<<blocks, 256, 0, st>>>(d_res, d_ridx, n, d_out);
+cudaError_t launch_exh_reduce(const EvalResult* d_res, int64_t n, ExhPartial* d_out, int blocks,
+                              cudaStream_t st) {
+  dev::exh_reduce_kernel<<<blocks, 256, 0, st>>>(d_res, n, d_out);
   return cudaGetLastError();
 }
 

@@ -13,12 +13,14 @@
 //   exh_key_kernel     index -> candidate -> canonical key bytes
 //   exh_insert_kernel  open-addressing table keyed by the exact key bytes,
 //                      slot value = min index (the first occurrence)
-//   exh_rep_kernel     first occurrences -> compact plan records
+//   exh_rep_kernel     first occurrences -> compact plan records at their
+//                      index (mode e2e), the others -> mode skip
 //   eval_kernel        end_to_end_cost + check_memory (mode e2e)
 //   exh_reduce_kernel  argmin over memory-feasible representatives by
 //                      (cost, index) = the reference's strict-< first minimum
 // Keys never collide across blocks (the layouts pin the composition), so a
-// block is deduplicated on its own.
+// block is deduplicated on its own. Blocks are queued back to back on one
+// stream (buffers reused in stream order) with a single host sync at the end.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -109,10 +111,9 @@ cudaError_t launch_exh_insert(const ExhBlock& B, uint64_t n, const uint8_t* d_ke
                               unsigned long long* d_table, uint64_t mask,
                               unsigned long long* d_slot, cudaStream_t st);
 cudaError_t launch_exh_reps(const ExhBlock& B, uint64_t n, const unsigned long long* d_table,
-                            const unsigned long long* d_slot, uint8_t* d_recs,
-                            unsigned long long* d_ridx, unsigned long long* d_count,
-                            cudaStream_t st);
-cudaError_t launch_exh_reduce(const EvalResult* d_res, const unsigned long long* d_ridx,
-                              int64_t n, ExhPartial* d_out, int blocks, cudaStream_t st);
+                            const unsigned long long* d_slot, uint8_t* d_recs, int32_t* d_modes,
+                            unsigned long long* d_count, cudaStream_t st);
+cudaError_t launch_exh_reduce(const EvalResult* d_res, int64_t n, ExhPartial* d_out, int blocks,
+                              cudaStream_t st);
 
 }  // namespace hpg

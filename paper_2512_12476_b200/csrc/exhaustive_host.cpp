@@ -111,25 +111,20 @@ SearchOut exhaustive_search(Ctx& ctx, const Knobs& K) {
   cv.n_tasks = T;
   cv.max_w = cv.max_sl = cv.max_slots = cv.max_cells = cv.max_dpk = T * n;
   const int64_t stride = (80 + T * n + 7) & ~int64_t(7);
-  const int red_blocks = 2 * ctx.n_sm;
-  DevBuf<uint8_t> keys, recs;
-  DevBuf<unsigned long long> table, slot, ridx, count;
-  DevBuf<EvalResult> res;
-  DevBuf<ExhPartial> part;
-  part.reserve(red_blocks);
-  count.reserve(1);
-  std::vector<ExhPartial> hp(red_blocks);
-  cudaStream_t st = ctx.stream;
-
+  // ---- pass 1: the blocks, in enumeration order ----
+  struct BlockRef {
+    ExhBlock B;
+    const Grouping* tg;
+    std::vector<int> comp;
+    int part_off, part_n;
+  };
+  std::vector<BlockRef> blocks;
   SearchOut S;
   const auto tgs = enumerate_task_groupings(P, false);
   S.task_groupings = static_cast<int64_t>(tgs.size());
-  int64_t explored = 0, raw_total = 0;
-  double best = kInf;
-  ExhBlock best_block{};
-  uint64_t best_idx = 0;
-  Grouping best_tg;
-  std::vector<int> best_comp;
+  int64_t raw_total = 0;
+  uint64_t max_raw = 0;
+  int key_max = 8, parts = 0;
   for (const Grouping& tg : tgs) {
     const int k = static_cast<int>(tg.size());
     if (k > n) continue;
@@ -177,84 +172,113 @@ SearchOut exhaustive_search(Ctx& ctx, const Knobs& K) {
       B.key_bytes = (kb + 7) & ~7;
       B.rec_stride = static_cast<int32_t>(stride);
       raw_total += static_cast<int64_t>(B.raw);
-
-      // ---- device pipeline for the block ----
-      const uint64_t R = B.raw;
-      uint64_t H = 1;
-      while (H < 2 * R) H <<= 1;
-      keys.reserve(R * B.key_bytes);
-      table.reserve(H);
-      slot.reserve(R);
-      recs.reserve(R * stride);
-      ridx.reserve(R);
-      res.reserve(R);
-      cuda_check(cudaMemsetAsync(table.p, 0xff, H * 8, st), "memset table");
-      cuda_check(cudaMemsetAsync(count.p, 0, 8, st), "memset count");
-      cuda_check(launch_exh_keys(B, R, keys.p, st), "exh_key_kernel");
-      cuda_check(launch_exh_insert(B, R, keys.p, table.p, H - 1, slot.p, st), "exh_insert_kernel");
-      cuda_check(launch_exh_reps(B, R, table.p, slot.p, recs.p, ridx.p, count.p, st),
-                 "exh_rep_kernel");
-      unsigned long long nrep = 0;
-      cuda_check(cudaMemcpyAsync(&nrep, count.p, 8, cudaMemcpyDeviceToHost, st), "D2H count");
-      cuda_check(cudaStreamSynchronize(st), "exhaustive block");
-      ctx.launches += 3;
-      int grid = 0;
-      cuda_check(eval_grid(cv, static_cast<int>(nrep), ctx.n_sm, grid), "eval occupancy");
-      const int64_t scratch = eval_scratch_doubles(n, ctx.max_nl);
-      ctx.d_scratch.reserve(static_cast<size_t>(std::max(grid, 32 * ctx.n_sm)) * scratch);
-      cuda_check(launch_eval(ctx.dprob, cfg, cv, 0, recs.p, nullptr, nullptr, kModeE2E,
-                             static_cast<int>(nrep), stride, nullptr, res.p, nullptr, nullptr,
-                             ctx.d_scratch.p, scratch, grid, st),
-                 "eval_kernel");
-      cuda_check(launch_exh_reduce(res.p, ridx.p, static_cast<int64_t>(nrep), part.p, red_blocks,
-                                   st),
-                 "exh_reduce_kernel");
-      cuda_check(cudaMemcpyAsync(hp.data(), part.p, sizeof(ExhPartial) * red_blocks,
-                                 cudaMemcpyDeviceToHost, st),
-                 "D2H partials");
-      cuda_check(cudaStreamSynchronize(st), "exhaustive eval");
-      ctx.launches += 2;
-      ++ctx.eval_launches;
-      ctx.plans_evaluated += static_cast<int64_t>(nrep);
-      explored += static_cast<int64_t>(nrep);
-      ExhPartial bb{kInf, ~0ull};
-      for (const ExhPartial& p : hp)
-        if (p.best < bb.best || (p.best == bb.best && p.best_idx < bb.best_idx)) bb = p;
-      // blocks arrive in enumeration order: strict < keeps the first minimum
-      if (bb.best_idx != ~0ull && bb.best < best) {
-        best = bb.best;
-        best_block = B;
-        best_idx = bb.best_idx;
-        best_tg = tg;
-        best_comp = comp;
-      }
+      max_raw = std::max(max_raw, B.raw);
+      key_max = std::max(key_max, B.key_bytes);
+      const int pn = static_cast<int>(
+          std::min<uint64_t>(static_cast<uint64_t>(2 * ctx.n_sm), (B.raw + 1023) / 1024));
+      blocks.push_back({B, &tg, comp, parts, std::max(1, pn)});
+      parts += std::max(1, pn);
+    }
+  }
+  // ---- pass 2: every block queued back to back on the context stream ----
+  // (buffers live in the context; stream order makes their reuse safe)
+  uint64_t H = 1;
+  while (H < 2 * std::max<uint64_t>(max_raw, 1)) H <<= 1;
+  DevBuf<uint8_t>& keys = ctx.d_exh_keys;
+  DevBuf<uint8_t>& recs = ctx.d_exh_recs;
+  DevBuf<unsigned long long>& table = ctx.d_exh_table;
+  DevBuf<unsigned long long>& slot = ctx.d_exh_slot;
+  DevBuf<unsigned long long>& counts = ctx.d_exh_count;
+  DevBuf<EvalResult>& res = ctx.d_exh_res;
+  keys.reserve(max_raw * key_max);
+  table.reserve(H);
+  slot.reserve(max_raw);
+  recs.reserve(max_raw * stride);
+  res.reserve(max_raw);
+  ctx.d_modes.reserve(max_raw);
+  counts.reserve(blocks.size() + 1);
+  ctx.d_exh_part.reserve(sizeof(ExhPartial) * (parts + 1));
+  ExhPartial* part_p = reinterpret_cast<ExhPartial*>(ctx.d_exh_part.p);
+  const int64_t scratch = eval_scratch_doubles(n, ctx.max_nl);
+  ctx.d_scratch.reserve(static_cast<size_t>(32 * ctx.n_sm) * scratch);
+  cudaStream_t st = ctx.stream;
+  cuda_check(cudaMemsetAsync(counts.p, 0, 8 * (blocks.size() + 1), st), "memset counts");
+  for (size_t bi = 0; bi < blocks.size(); ++bi) {
+    const ExhBlock& B = blocks[bi].B;
+    const uint64_t R = B.raw;
+    uint64_t h = 1;
+    while (h < 2 * R) h <<= 1;
+    cuda_check(cudaMemsetAsync(table.p, 0xff, h * 8, st), "memset table");
+    cuda_check(launch_exh_keys(B, R, keys.p, st), "exh_key_kernel");
+    cuda_check(launch_exh_insert(B, R, keys.p, table.p, h - 1, slot.p, st), "exh_insert_kernel");
+    cuda_check(launch_exh_reps(B, R, table.p, slot.p, recs.p, ctx.d_modes.p, counts.p + bi, st),
+               "exh_rep_kernel");
+    int grid = 0;
+    cuda_check(eval_grid(cv, static_cast<int>(R), ctx.n_sm, grid), "eval occupancy");
+    cuda_check(launch_eval(ctx.dprob, cfg, cv, 0, recs.p, nullptr, ctx.d_modes.p, 0,
+                           static_cast<int>(R), stride, nullptr, res.p, nullptr, nullptr,
+                           ctx.d_scratch.p, scratch, grid, st),
+               "eval_kernel");
+    cuda_check(launch_exh_reduce(res.p, static_cast<int64_t>(R), part_p + blocks[bi].part_off,
+                                 blocks[bi].part_n, st),
+               "exh_reduce_kernel");
+    ctx.launches += 5;
+    ++ctx.eval_launches;
+    ctx.plans_evaluated += static_cast<int64_t>(R);
+  }
+  std::vector<unsigned long long> hc(blocks.size() + 1);
+  std::vector<ExhPartial> hp(parts + 1);
+  cuda_check(cudaMemcpyAsync(hc.data(), counts.p, 8 * hc.size(), cudaMemcpyDeviceToHost, st),
+             "D2H counts");
+  if (parts)
+    cuda_check(cudaMemcpyAsync(hp.data(), part_p, sizeof(ExhPartial) * parts,
+                               cudaMemcpyDeviceToHost, st),
+               "D2H partials");
+  cuda_check(cudaStreamSynchronize(st), "exhaustive");
+  // ---- merge: blocks in enumeration order, strict < keeps the first minimum ----
+  int64_t explored = 0;
+  double best = kInf;
+  int best_block = -1;
+  uint64_t best_idx = 0;
+  for (size_t bi = 0; bi < blocks.size(); ++bi) {
+    explored += static_cast<int64_t>(hc[bi]);
+    ExhPartial bb{kInf, ~0ull};
+    for (int q = 0; q < blocks[bi].part_n; ++q) {
+      const ExhPartial& p = hp[blocks[bi].part_off + q];
+      if (p.best < bb.best || (p.best == bb.best && p.best_idx < bb.best_idx)) bb = p;
+    }
+    if (bb.best_idx != ~0ull && bb.best < best) {
+      best = bb.best;
+      best_block = static_cast<int>(bi);
+      best_idx = bb.best_idx;
     }
   }
   S.consumed = explored;
   S.budget = raw_total;
-  if (best < kInf) {
+  if (best_block >= 0) {
+    const ExhBlock& BB = blocks[best_block].B;
     int oi[kMaxTasks];
     uint8_t devs[kMaxTasks * kExhMaxDevices];
-    exh_decode(best_block, best_idx, oi, devs);
+    exh_decode(BB, best_idx, oi, devs);
     int dp[kMaxTasks], pp[kMaxTasks], tp[kMaxTasks];
     for (int p = 0; p < T; ++p) {
-      const int s = best_block.order[p];
-      dp[s] = best_block.opt[p][oi[p]][0];
-      pp[s] = best_block.opt[p][oi[p]][1];
-      tp[s] = best_block.opt[p][oi[p]][2];
+      const int s = BB.order[p];
+      dp[s] = BB.opt[p][oi[p]][0];
+      pp[s] = BB.opt[p][oi[p]][1];
+      tp[s] = BB.opt[p][oi[p]][2];
     }
     Cand c;
     init_cand(c, T, dp, pp, tp, P);
-    c.ng = static_cast<int>(best_tg.size());
+    c.ng = static_cast<int>(blocks[best_block].tg->size());
     for (int p = 0; p < T; ++p) {
-      const int s = best_block.order[p];
-      const int m = best_block.comp[best_block.grp[p]];
+      const int s = BB.order[p];
+      const int m = BB.comp[BB.grp[p]];
       for (int i = 0; i < m; ++i) c.dev()[c.o.dev[s] + i] = devs[p * n + i];
     }
     S.has_plan = true;
     S.plan = std::move(c);
-    S.plan_groups = best_tg;
-    S.plan_counts = best_comp;
+    S.plan_groups = *blocks[best_block].tg;
+    S.plan_counts = blocks[best_block].comp;
     Batch b;
     b.cands.push_back(&S.plan);
     b.modes.push_back(kModeE2E);
