@@ -13,6 +13,7 @@
 //   search WF TOPO BUDGET SEED OUT [knobs.json]   nested_sha_search + survivor replay
 //   searchfuzz SEED N OUT                tiny random searches (acceptance #3/#4 style)
 //   exhaustive SEED N OUT                exhaustive_search goldens (acceptance #2 + fuzz)
+//   cli OUT                              reference CLI (cmd_plan/estimate/compare/scenario)
 //   sweep WF TOPO SEED K0 COUNT OUT      config-5 generator
 //   time_search WF TOPO BUDGET SEED [knobs.json]  one timed search, JSON line
 //   time_sweep WF TOPO SEED K0 COUNT THREADS      timed sweep sample, JSON line
@@ -25,6 +26,7 @@
 #include <fstream>
 #include <functional>
 #include <numeric>
+#include <optional>
 #include <set>
 #include <sstream>
 #include <string>
@@ -34,6 +36,7 @@
 #include "json.hpp"
 
 #include "hetplan/balance.hpp"
+#include "hetplan/cli.hpp"
 #include "hetplan/combinatorics.hpp"
 #include "hetplan/cost_model.hpp"
 #include "hetplan/errors.hpp"
@@ -1000,6 +1003,158 @@ int cmd_exhaustive(std::uint64_t seed, int n_fuzz, const std::string& out) {
   return 0;
 }
 
+// ---- CLI goldens: the reference's own cmd_* (cli.cpp:76-283) on fixed
+// command lines; paths relative to the repo root, {tmp} = a scratch dir ----
+
+std::string subst_tmp(std::string s, const std::string& tmp) {
+  for (size_t p = s.find(tmp); p != std::string::npos; p = s.find(tmp, p)) {
+    s.replace(p, tmp.size(), "{tmp}");
+    p += 5;
+  }
+  return s;
+}
+
+int cmd_cli(const std::string& out_path) {
+  char tmpl[] = "/tmp/hpg_cli_XXXXXX";
+  const std::string tmp = mkdtemp(tmpl);
+  json cases = json::array();
+  auto file_text = [&](const std::string& path) {
+    std::ifstream in(path);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    return subst_tmp(ss.str(), tmp);
+  };
+  auto record = [&](const std::string& name, const std::vector<std::string>& argv, int rc,
+                    const std::string& out, const std::string& err,
+                    const std::vector<std::string>& files) {
+    json c;
+    c["name"] = name;
+    c["args"] = argv;
+    c["rc"] = rc;
+    c["stdout"] = subst_tmp(out, tmp);
+    c["stderr"] = subst_tmp(err, tmp);
+    json f = json::object();
+    for (const auto& fn : files) f[fn] = file_text(tmp + "/" + fn);
+    c["files"] = f;
+    cases.push_back(c);
+  };
+  const std::string K = "tests/golden/cli/knobs.json";
+  auto fx = [](const std::string& c, const char* kind) {
+    return "fixtures/" + c + "." + kind + ".json";
+  };
+  auto plan = [&](const std::string& name, const std::string& cfg, const std::string& knobs,
+                  std::optional<std::int64_t> budget, std::optional<std::uint64_t> seed,
+                  const std::string& out_file, const std::string& format) {
+    PlanArgs a;
+    a.workflow_path = fx(cfg, "workflow");
+    a.topology_path = fx(cfg, "topology");
+    a.knobs_path = knobs;
+    a.out_path = tmp + "/" + out_file;
+    a.budget = budget;
+    a.seed = seed;
+    a.format = format;
+    std::ostringstream o, e;
+    const int rc = cmd_plan(a, o, e);
+    std::vector<std::string> argv = {"plan", "--workflow", a.workflow_path, "--topology",
+                                     a.topology_path};
+    if (!knobs.empty()) argv.insert(argv.end(), {"--knobs", knobs});
+    if (budget) argv.insert(argv.end(), {"--budget", std::to_string(*budget)});
+    if (seed) argv.insert(argv.end(), {"--seed", std::to_string(*seed)});
+    argv.insert(argv.end(), {"--out", "{tmp}/" + out_file, "--format", format});
+    record(name, argv, rc, o.str(), e.str(), rc == 0 ? std::vector<std::string>{out_file}
+                                                     : std::vector<std::string>{});
+  };
+  plan("plan_c1_json", "c1", "", 1000, 42, "p1.json", "json");
+  plan("plan_c1_text", "c1", K, std::nullopt, 7, "p2.json", "text");
+  plan("plan_c2_knobs", "c2", K, 300, 11, "p3.json", "json");
+  auto estimate = [&](const std::string& name, const std::string& cfg, const std::string& pfile,
+                      const std::string& knobs, const std::string& format) {
+    EstimateArgs a;
+    a.plan_path = tmp + "/" + pfile;
+    a.workflow_path = fx(cfg, "workflow");
+    a.topology_path = fx(cfg, "topology");
+    a.knobs_path = knobs;
+    a.format = format;
+    std::ostringstream o, e;
+    const int rc = cmd_estimate(a, o, e);
+    std::vector<std::string> argv = {"estimate", "--plan", "{tmp}/" + pfile, "--workflow",
+                                     a.workflow_path, "--topology", a.topology_path};
+    if (!knobs.empty()) argv.insert(argv.end(), {"--knobs", knobs});
+    argv.insert(argv.end(), {"--format", format});
+    record(name, argv, rc, o.str(), e.str(), {});
+  };
+  estimate("estimate_json", "c1", "p1.json", "", "json");
+  estimate("estimate_text_knobs", "c1", "p2.json", K, "text");
+  estimate("estimate_missing_plan", "c1", "nope.json", "", "json");
+  {
+    // a plan file naming an unknown device
+    std::string t = file_text(tmp + "/p1.json");
+    const auto pos = t.find("\"a100-00\"");
+    if (pos != std::string::npos) t.replace(pos, 9, "\"zz-99\"");
+    std::ofstream(tmp + "/bad.json") << subst_tmp(t, "{tmp}");
+    estimate("estimate_unknown_device", "c1", "bad.json", "", "json");
+  }
+  auto compare = [&](const std::string& name, const std::vector<std::string>& pfiles,
+                     const std::string& knobs, const std::string& format) {
+    CompareArgs a;
+    for (const auto& p : pfiles) a.plan_paths.push_back(tmp + "/" + p);
+    a.workflow_path = fx("c1", "workflow");
+    a.topology_path = fx("c1", "topology");
+    a.knobs_path = knobs;
+    a.format = format;
+    std::ostringstream o, e;
+    const int rc = cmd_compare(a, o, e);
+    std::vector<std::string> argv = {"compare"};
+    for (const auto& p : pfiles) argv.push_back("{tmp}/" + p);
+    argv.insert(argv.end(), {"--workflow", a.workflow_path, "--topology", a.topology_path});
+    if (!knobs.empty()) argv.insert(argv.end(), {"--knobs", knobs});
+    argv.insert(argv.end(), {"--format", format});
+    record(name, argv, rc, o.str(), e.str(), {});
+  };
+  compare("compare_json", {"p2.json", "p1.json"}, "", "json");
+  compare("compare_text", {"p1.json", "p2.json", "p1.json"}, K, "text");
+  compare("compare_one_plan", {"p1.json"}, "", "json");
+  auto scenario = [&](const std::string& name, int id, const std::string& gpus,
+                      std::optional<std::uint64_t> seed, int node_size,
+                      const std::string& edge, const std::string& out_file) {
+    ScenarioArgs a;
+    a.scenario_id = id;
+    a.gpus = gpus;
+    a.seed = seed;
+    a.out_path = tmp + "/" + out_file;
+    a.node_size = node_size;
+    a.edge_gpus = edge;
+    std::ostringstream o, e;
+    const int rc = cmd_scenario(a, o, e);
+    std::vector<std::string> argv = {"scenario", "--id", std::to_string(id)};
+    if (!gpus.empty()) argv.insert(argv.end(), {"--gpus", gpus});
+    if (seed) argv.insert(argv.end(), {"--seed", std::to_string(*seed)});
+    argv.insert(argv.end(), {"--out", "{tmp}/" + out_file, "--node-size",
+                             std::to_string(node_size), "--edge-gpus", edge});
+    record(name, argv, rc, o.str(), e.str(), rc == 0 ? std::vector<std::string>{out_file}
+                                                     : std::vector<std::string>{});
+  };
+  scenario("scenario1_default", 1, "", 3, 8, "L4", "s1.json");
+  scenario("scenario1_mixed", 1, "6xA100,3xL4,5xL40S", 3, 4, "L4", "s1b.json");
+  scenario("scenario2_edges", 2, "8xA100,8xL40S,4xL4", 9, 8, "L4,L40S", "s2.json");
+  scenario("scenario3", 3, "", 11, 8, "L4", "s3.json");
+  scenario("scenario4", 4, "10xL40S,6xA100", 5, 8, "L4", "s4.json");
+  scenario("scenario_bad_inventory", 1, "24A100", 1, 8, "L4", "sx.json");
+  scenario("scenario_unknown_model", 1, "4xH200", 1, 8, "L4", "sx.json");
+  scenario("scenario_bad_id", 9, "", 1, 8, "L4", "sx.json");
+  {
+    PlanArgs a;  // usage error: no topology
+    a.workflow_path = fx("c1", "workflow");
+    std::ostringstream o, e;
+    const int rc = cmd_plan(a, o, e);
+    record("plan_missing_topology", {"plan", "--workflow", a.workflow_path, "--seed", "1"}, rc,
+           o.str(), e.str(), {});
+  }
+  write_file(out_path, json{{"cases", cases}}.dump(1) + "\n");
+  std::printf("wrote %zu CLI cases to %s\n", cases.size(), out_path.c_str());
+  return 0;
+}
+
 struct SweepStats {
   std::uint64_t feasible = 0;
   double best = std::numeric_limits<double>::infinity();
@@ -1142,6 +1297,7 @@ int main(int argc, char** argv) {
                         argc > 7 ? argv[7] : "");
     if (cmd == "searchfuzz") return cmd_searchfuzz(std::stoull(arg(2)), std::stoi(arg(3)), arg(4));
     if (cmd == "exhaustive") return cmd_exhaustive(std::stoull(arg(2)), std::stoi(arg(3)), arg(4));
+    if (cmd == "cli") return cmd_cli(arg(2));
     if (cmd == "sweep")
       return cmd_sweep(arg(2), arg(3), std::stoull(arg(4)), std::stoull(arg(5)),
                        std::stoull(arg(6)), arg(7));

@@ -30,3 +30,4 @@ for seed in ("42", "0", "18446744073709551615", "20251018"):
     out[seed] = r.stdout.strip().splitlines()
 json.dump(out, open("tests/golden/rng_pin.json", "w"), indent=1)
 PY
+$R cli $G/cli/cases.json
