@@ -225,8 +225,9 @@ Plan Engine::balance_layers(const Plan& plan, const CostModelConfig& cfg) {
   return balanced(ctx_, plan, wf_, topo_, cfg, 2);
 }
 
-SearchResult Engine::nested_sha_search(const SearchKnobs& k,
-                                       const std::vector<TaskGrouping>* tg_override) {
+namespace {
+
+hpg_knobs knobs_to_c(const SearchKnobs& k) {
   hpg_knobs kn;
   hpg_knobs_default(&kn);
   kn.budget = k.budget;
@@ -244,6 +245,51 @@ SearchResult Engine::nested_sha_search(const SearchKnobs& k,
   kn.recompute = k.recompute;
   kn.reshard_override = k.reshard_override;
   kn.sync_override = k.sync_override;
+  kn.exhaustive_cap = k.exhaustive_cap;
+  return kn;
+}
+
+// the chosen plan + breakdown of a result handle (has_plan checked by caller)
+void read_plan(hpg_search_result* r, const WorkflowGraph& wf, const DeviceTopology& topo,
+               Plan& plan, CostBreakdown& bd) {
+  hpg_plan_table pt;
+  const int T = static_cast<int>(wf.tasks.size());
+  std::vector<int32_t> gflat(T);
+  double est = 0;
+  uint64_t pseed = 0;
+  int64_t pbudget = 0;
+  hpg_result_plan(r, &pt, gflat.data(), &est, &pseed, &pbudget);
+  plan.task_grouping.groups.assign(pt.n_groups[0], {});
+  for (int s_ : gflat) plan.task_grouping.groups[pt.task_group[s_]].push_back(wf.tasks[s_].id);
+  for (int g = 0; g < pt.n_groups[0]; ++g) plan.gpu_grouping.counts.push_back(pt.gpu_counts[g]);
+  for (int t = 0; t < T; ++t) {
+    ParallelLayout l;
+    l.dp = pt.dp[t];
+    l.pp = pt.pp[t];
+    l.tp = pt.tp[t];
+    l.stage_layers.assign(pt.stage_layers + pt.sl_off[t], pt.stage_layers + pt.sl_off[t] + l.pp);
+    l.replica_batch_weights.assign(pt.weights + pt.w_off[t], pt.weights + pt.w_off[t] + l.dp);
+    std::vector<std::string> ids;
+    for (int e = 0; e < l.dp * l.pp * l.tp; ++e)
+      ids.push_back(topo.device(pt.devices[pt.dev_off[t] + e]).id);
+    plan.layouts[wf.tasks[t].id] = std::move(l);
+    plan.assignment[wf.tasks[t].id] = std::move(ids);
+  }
+  plan.provenance.seed = pseed;
+  plan.provenance.budget = pbudget;
+  plan.estimated_cost_s = est;
+  std::vector<double> ptk(T * 7);
+  double rs = 0, sy = 0, e2e = 0;
+  uint8_t mf = 0;
+  hpg_result_breakdown(r, ptk.data(), &rs, &sy, &e2e, &mf);
+  bd = breakdown_of(wf, ptk.data(), rs, sy, e2e, mf != 0);
+}
+
+}  // namespace
+
+SearchResult Engine::nested_sha_search(const SearchKnobs& k,
+                                       const std::vector<TaskGrouping>* tg_override) {
+  hpg_knobs kn = knobs_to_c(k);
   std::vector<int32_t> tgo;
   if (tg_override) {
     for (const TaskGrouping& tg : *tg_override)
@@ -281,42 +327,39 @@ SearchResult Engine::nested_sha_search(const SearchKnobs& k,
     s.halvings.push_back(HalvingEvent{hl[i], static_cast<size_t>(hb[i]),
                                       static_cast<size_t>(ha[i]), hw[i], he[i]});
   if (info.has_plan) {
-    hpg_plan_table pt;
-    const int T = static_cast<int>(wf_.tasks.size());
-    std::vector<int32_t> gflat(T);
-    double est = 0;
-    uint64_t pseed = 0;
-    int64_t pbudget = 0;
-    hpg_result_plan(r, &pt, gflat.data(), &est, &pseed, &pbudget);
     Plan plan;
-    plan.task_grouping.groups.assign(pt.n_groups[0], {});
-    for (int s_ : gflat) plan.task_grouping.groups[pt.task_group[s_]].push_back(wf_.tasks[s_].id);
-    for (int g = 0; g < pt.n_groups[0]; ++g) plan.gpu_grouping.counts.push_back(pt.gpu_counts[g]);
-    for (int t = 0; t < T; ++t) {
-      ParallelLayout l;
-      l.dp = pt.dp[t];
-      l.pp = pt.pp[t];
-      l.tp = pt.tp[t];
-      l.stage_layers.assign(pt.stage_layers + pt.sl_off[t], pt.stage_layers + pt.sl_off[t] + l.pp);
-      l.replica_batch_weights.assign(pt.weights + pt.w_off[t], pt.weights + pt.w_off[t] + l.dp);
-      std::vector<std::string> ids;
-      for (int e = 0; e < l.dp * l.pp * l.tp; ++e)
-        ids.push_back(topo_.device(pt.devices[pt.dev_off[t] + e]).id);
-      plan.layouts[wf_.tasks[t].id] = std::move(l);
-      plan.assignment[wf_.tasks[t].id] = std::move(ids);
-    }
-    plan.provenance.seed = pseed;
-    plan.provenance.budget = pbudget;
-    plan.estimated_cost_s = est;
-    std::vector<double> ptk(T * 7);
-    double rs = 0, sy = 0, e2e = 0;
-    uint8_t mf = 0;
-    hpg_result_breakdown(r, ptk.data(), &rs, &sy, &e2e, &mf);
-    out.breakdown = breakdown_of(wf_, ptk.data(), rs, sy, e2e, mf != 0);
+    read_plan(r, wf_, topo_, plan, out.breakdown);
     out.plan = std::move(plan);
   }
   hpg_result_free(r);
   return out;
+}
+
+ExhaustiveResult Engine::exhaustive_search(const SearchKnobs& k) {
+  const hpg_knobs kn = knobs_to_c(k);
+  hpg_search_result* r = nullptr;
+  char err[1024];
+  check(hpg_exhaustive(ctx_, &kn, &r, err, sizeof(err)), err);
+  hpg_search_info info;
+  hpg_result_info(r, &info);
+  ExhaustiveResult out;
+  out.explored = info.consumed;
+  if (info.has_plan) {
+    Plan plan;
+    read_plan(r, wf_, topo_, plan, out.breakdown);
+    out.cost = out.breakdown.end_to_end_s;
+    out.plan = std::move(plan);
+  }
+  hpg_result_free(r);
+  return out;
+}
+
+double Engine::exhaustive_space_estimate(const SearchKnobs& k) {
+  const hpg_knobs kn = knobs_to_c(k);
+  double est = 0;
+  char err[1024];
+  check(hpg_exhaustive_estimate(ctx_, &kn, &est, err, sizeof(err)), err);
+  return est;
 }
 
 CostBreakdown end_to_end_cost(const Plan& plan, const WorkflowGraph& wf,
@@ -330,6 +373,12 @@ SearchResult nested_sha_search(const WorkflowGraph& wf, const DeviceTopology& to
                                const std::vector<TaskGrouping>* tg_override) {
   Engine e(wf, topo);
   return e.nested_sha_search(knobs, tg_override);
+}
+
+ExhaustiveResult exhaustive_search(const WorkflowGraph& wf, const DeviceTopology& topo,
+                                   const SearchKnobs& knobs) {
+  Engine e(wf, topo);
+  return e.exhaustive_search(knobs);
 }
 
 }  // namespace hetplan::b200

@@ -43,6 +43,9 @@ class Engine {
   // nested_sha_search (search.hpp:115-118)
   SearchResult nested_sha_search(const SearchKnobs& knobs,
                                  const std::vector<TaskGrouping>* tg_override = nullptr);
+  // exhaustive_search / exhaustive_space_estimate (search.hpp:137-155)
+  ExhaustiveResult exhaustive_search(const SearchKnobs& knobs);
+  double exhaustive_space_estimate(const SearchKnobs& knobs);
 
  private:
   const WorkflowGraph& wf_;
@@ -57,5 +60,7 @@ CostBreakdown end_to_end_cost(const Plan& plan, const WorkflowGraph& wf,
 SearchResult nested_sha_search(const WorkflowGraph& wf, const DeviceTopology& topo,
                                const SearchKnobs& knobs,
                                const std::vector<TaskGrouping>* tg_override = nullptr);
+ExhaustiveResult exhaustive_search(const WorkflowGraph& wf, const DeviceTopology& topo,
+                                   const SearchKnobs& knobs);
 
 }  // namespace hetplan::b200

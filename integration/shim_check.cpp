@@ -6,11 +6,13 @@
 // Cases: the reference acceptance criteria #7 (mixed pool vs 24xA100, B=5000)
 // and #10 (desk-scale, B=1000) (proj/tests/acceptance.cpp:379-420, 552-588),
 // the survey configs c1..c4 at B=1000, and 200 random plans per config for
-// end_to_end_cost. Equality = byte-identical serialize_plan(plan, &breakdown)
+// end_to_end_cost, and exhaustive_search on acceptance #2's twenty instances.
+// Equality = byte-identical serialize_plan(plan, &breakdown)
 // plus identical SearchState (b_m, trace, arms, halvings).
 #include <chrono>
 #include <cstdio>
 #include <fstream>
+#include <map>
 #include <sstream>
 #include <string>
 
@@ -100,6 +102,57 @@ int run_costs(const char* name, const WorkflowGraph& wf, const DeviceTopology& t
   return bad ? 1 : 0;
 }
 
+// exhaustive_search on acceptance #2's twenty instances (acceptance.cpp:116-141)
+int run_exhaustive() {
+  int bad = 0, n = 0;
+  double ref_s = 0, gpu_s = 0;
+  for (int i = 0; i < 20; ++i) {
+    Rng rng(5000 + i);
+    std::map<int, ModelSpec> models;
+    if (i % 4 == 0) {
+      models[6] = testutil::tiny_model(8, 16, 2 + i % 3);
+    } else if (i % 4 == 1) {
+      models[2] = testutil::tiny_model(8, 16, 2);
+      models[6] = testutil::tiny_model(8, 16, 4);
+    } else if (i % 4 == 2) {
+      models[1] = testutil::tiny_model(8, 16, 2);
+      models[6] = testutil::tiny_model(8, 16, 2);
+    } else {
+      models[2] = testutil::tiny_model(8, 16, 2);
+      models[3] = testutil::tiny_model(16, 32, 2);
+    }
+    const auto wf = testutil::subset_workflow_models(
+        models, testutil::tiny_batch(4, 1, 8, 4, 1), i % 2 == 0 ? RunMode::kSync : RunMode::kAsync,
+        0.25);
+    const int n_devices = 2 + static_cast<int>(rng.bounded(3));
+    const DeviceTopology topo = i % 3 == 0
+                                    ? testutil::uniform_topology(n_devices, 1e13, 1e12, 64.0, 2)
+                                    : testutil::random_topology(rng, 4);
+    SearchKnobs k;
+    k.balance_data = false;
+    k.balance_layers = false;
+    const double t0 = now();
+    const ExhaustiveResult ref = exhaustive_search(wf, topo, k);
+    const double t1 = now();
+    b200::Engine eng(wf, topo);
+    const ExhaustiveResult gpu = eng.exhaustive_search(k);
+    const double t2 = now();
+    ref_s += t1 - t0;
+    gpu_s += t2 - t1;
+    ++n;
+    const bool ok = ref.explored == gpu.explored && ref.cost == gpu.cost &&
+                    ref.plan.has_value() == gpu.plan.has_value() &&
+                    (!ref.plan || serialize_plan(*ref.plan, &ref.breakdown) ==
+                                      serialize_plan(*gpu.plan, &gpu.breakdown));
+    if (!ok) ++bad;
+  }
+  std::printf("{\"case\": \"exhaustive_search acceptance#2 x%d\", \"ok\": %s, \"mismatches\": %d, "
+              "\"ref_s\": %.4f, \"b200_s_incl_staging\": %.4f}\n",
+              n, bad ? "false" : "true", bad, ref_s, gpu_s);
+  std::fflush(stdout);
+  return bad ? 1 : 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -127,5 +180,6 @@ int main(int argc, char** argv) {
     failures += run_search(c, wf, topo, k);
     failures += run_costs(c, wf, topo);
   }
+  failures += run_exhaustive();
   return failures;
 }
