@@ -170,6 +170,7 @@ struct Carve {
   int32_t max_cells;  // max sum dp*pp
   int32_t max_dpk;    // max sum pp*tp
   int32_t bytes;      // total dynamic smem per CTA
+  int32_t cls_smem;   // stage the link-class matrix in shared memory (small N, small waves)
 };
 
 HPG_HD int carve_round(int b) { return (b + 15) & ~15; }
@@ -185,9 +186,14 @@ HPG_HD int carve_bytes(const Carve& c) {
   return b;
 }
 
+// the link-class matrix may be staged in shared memory when it is this small
+// (latency-bound small waves: every SM starts with a cold L1)
+constexpr int kClsSmemMax = 16384;
+
 HPG_HD int carve2_bytes(const Carve& c) {
   return carve_bytes(c) + carve_round(8 * c.max_cells) + 2 * carve_round(8 * c.max_sl) +
-         carve_round(8 * c.n_dev) + carve_round(4 * c.max_sl) + carve_round(4 * c.n_dev);
+         carve_round(8 * c.n_dev) + carve_round(4 * c.max_sl) + carve_round(4 * c.n_dev) +
+         (c.cls_smem ? carve_round(c.n_dev * c.n_dev) : 0);
 }
 
 }  // namespace hpg

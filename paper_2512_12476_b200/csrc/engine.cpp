@@ -437,6 +437,8 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   const uint8_t* d_rec = ctx.d_recs.p + in_recs;
   EvalResult* d_res = reinterpret_cast<EvalResult*>(ctx.d_out.p + out_res);
   uint8_t* d_orec = want_out ? ctx.d_out.p + out_recs : nullptr;
+  // small waves are latency-bound on cold SMs: stage the class matrix in smem
+  cv.cls_smem = (n <= 2 * ctx.n_sm && P.N * P.N <= kClsSmemMax) ? 1 : 0;
   int grid = 0;
   cuda_check(eval_grid(cv, n, ctx.n_sm, grid), "eval_kernel occupancy");
   const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);

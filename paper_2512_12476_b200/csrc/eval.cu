@@ -638,6 +638,7 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
     s.dtab_stride = 0;
   }
   __syncwarp();
+  stage_link_classes(P, s);
   for (int p = blockIdx.x; p < n; p += gridDim.x) {
     const int64_t rec_at = off ? off[p] : static_cast<int64_t>(p) * stride;
     const uint8_t* rec = recs + rec_at;
@@ -778,16 +779,22 @@ cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid) {
     if (e != cudaSuccess) return e;
     configured_bytes = cv.bytes;
   }
-  static int cached_bytes = -1, cached_per_sm = 0;
+  // occupancy per dynamic-smem size (a few distinct sizes per problem)
+  static int cached_bytes[8] = {-1, -1, -1, -1, -1, -1, -1, -1}, cached_per_sm[8];
+  static int next_slot = 0;
   int per_sm = 0;
-  if (cv.bytes == cached_bytes) {
-    per_sm = cached_per_sm;
+  int hit = -1;
+  for (int i = 0; i < 8; ++i)
+    if (cached_bytes[i] == cv.bytes) hit = i;
+  if (hit >= 0) {
+    per_sm = cached_per_sm[hit];
   } else {
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::eval_kernel, 32,
                                                                   cv.bytes);
     if (e != cudaSuccess) return e;
-    cached_bytes = cv.bytes;
-    cached_per_sm = per_sm;
+    cached_bytes[next_slot] = cv.bytes;
+    cached_per_sm[next_slot] = per_sm;
+    next_slot = (next_slot + 1) & 7;
   }
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   grid = n < n_sm * per_sm ? n : n_sm * per_sm;

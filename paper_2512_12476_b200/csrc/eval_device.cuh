@@ -92,6 +92,7 @@ struct Ws {
   int32_t cc_sig_ok;
   double cc_vol;              // staged volume
   long long* prof;            // diagnostics: this plan's profile slots
+  const uint8_t* cls;         // link class matrix [N*N]: shared-memory copy or P.cls
 };
 
 // diagnostics only (HPG_PLAN_PROFILE): per-plan clock64 phase stamps and
@@ -170,6 +171,28 @@ __device__ inline void carve(Ws& s, uint8_t* base, const Carve& c) {
   s.wsave = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
   s.sl_save2 = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
   s.split_step = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
+  s.cls = c.cls_smem ? carve_ptr(p, N * N) : nullptr;  // else P.cls (stage_link_classes)
+}
+
+// Stages the N x N link-class matrix in shared memory (once per CTA): every
+// ring, pair and bridge edge cost is a lookup into it. Warp-collective.
+__device__ inline void stage_link_classes(const DevProblem& P, Ws& s) {
+  const int lane = threadIdx.x & 31;
+  const int nn = P.n_dev * P.n_dev;
+  if (!s.cls) {
+    if (lane == 0) s.cls = P.cls;
+    __syncwarp();
+    return;
+  }
+  uint8_t* dst = const_cast<uint8_t*>(s.cls);
+  if ((nn & 7) == 0 && (reinterpret_cast<uintptr_t>(P.cls) & 7) == 0) {
+    const uint2* src = reinterpret_cast<const uint2*>(P.cls);
+    uint2* d2 = reinterpret_cast<uint2*>(dst);
+    for (int i = lane; i < nn / 8; i += 32) d2[i] = src[i];
+  } else {
+    for (int i = lane; i < nn; i += 32) dst[i] = P.cls[i];
+  }
+  __syncwarp();
 }
 
 // ---- memory model (plan.cpp:160-220) ----
@@ -439,7 +462,7 @@ __device__ __noinline__ unsigned long long cc_signature(const DevProblem& P, Ws&
 }
 
 __device__ __forceinline__ double ecost(const DevProblem& P, const Ws& s, int a, int b) {
-  return s.cc[__ldg(&P.cls[a * P.n_dev + b])];
+  return s.cc[s.cls[a * P.n_dev + b]];
 }
 
 // ---- device-wide ring memo (common.hpp RingSlot) ----

@@ -477,6 +477,7 @@ struct ArmRun {
   ArmCoro coro;
   double* clock = nullptr;
   int owner = 0;  // rank that runs it (multi-GPU)
+  int64_t n_offspring = 0, n_spec_hit = 0;  // diagnostics
 };
 
 // ga_run (search.cpp:437-565) as a coroutine.
@@ -603,7 +604,9 @@ ArmCoro ga_run(ArmRun& run) {
   bool have_spec = false;
   int64_t streak = 0;
   while (run.used < slice && streak < 64) {
+    ++run.n_offspring;
     if (have_spec && same_rng(spec.start, rng)) {
+      ++run.n_spec_hit;
       std::swap(cur, spec);
     } else {
       Rng r = rng;
@@ -789,6 +792,21 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
     for (auto& [r, cnt] : owners)
       if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
     ctx.host_ms += 1e3 * (now_s() - clock);
+  }
+  static const char* spec_log = std::getenv("HPG_SPEC_LOG");  // diagnostics only
+  if (spec_log) {
+    if (FILE* f = std::fopen(spec_log, "a")) {
+      int64_t off = 0, hit = 0, used = 0;
+      for (ArmRun* r : runs) {
+        off += r->n_offspring;
+        hit += r->n_spec_hit;
+        used += r->used;
+      }
+      std::fprintf(f, "runs %zu used %lld offspring %lld spec_hits %lld waves_total %lld\n",
+                   runs.size(), static_cast<long long>(used), static_cast<long long>(off),
+                   static_cast<long long>(hit), static_cast<long long>(waves));
+      std::fclose(f);
+    }
   }
 }
 
