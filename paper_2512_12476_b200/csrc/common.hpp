@@ -171,6 +171,7 @@ struct Carve {
   int32_t max_dpk;    // max sum pp*tp
   int32_t bytes;      // total dynamic smem per CTA
   int32_t cls_smem;   // stage the link-class matrix in shared memory (small N, small waves)
+  int32_t n_warps;    // warps per CTA: warp 0 evaluates, the others help with task costs
 };
 
 HPG_HD int carve_round(int b) { return (b + 15) & ~15; }
@@ -186,14 +187,25 @@ HPG_HD int carve_bytes(const Carve& c) {
   return b;
 }
 
+// warps per CTA when a plan's task costs are spread over a team (eval_kernel)
+constexpr int kMaxTeamWarps = 4;
+
 // the link-class matrix may be staged in shared memory when it is this small
 // (latency-bound small waves: every SM starts with a cold L1)
 constexpr int kClsSmemMax = 16384;
 
+// per-warp scratch of a helper warp (cell pieces, ring scratch, class costs)
+HPG_HD int team_scratch_bytes(const Carve& c) {
+  const int N = c.n_dev;
+  return 5 * carve_round(8 * N) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
+         2 * carve_round(N);
+}
+
 HPG_HD int carve2_bytes(const Carve& c) {
   return carve_bytes(c) + carve_round(8 * c.max_cells) + 2 * carve_round(8 * c.max_sl) +
          carve_round(8 * c.n_dev) + carve_round(4 * c.max_sl) + carve_round(4 * c.n_dev) +
-         (c.cls_smem ? carve_round(c.n_dev * c.n_dev) : 0);
+         (c.cls_smem ? carve_round(c.n_dev * c.n_dev) : 0) +
+         (c.n_warps > 1 ? (c.n_warps - 1) * team_scratch_bytes(c) : 0);
 }
 
 }  // namespace hpg

@@ -439,6 +439,13 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   uint8_t* d_orec = want_out ? ctx.d_out.p + out_recs : nullptr;
   // small waves are latency-bound on cold SMs: stage the class matrix in smem
   cv.cls_smem = (n <= 2 * ctx.n_sm && P.N * P.N <= kClsSmemMax) ? 1 : 0;
+  // ... and get helper warps for the per-task costs of each plan
+  static const int team_env = [] {
+    const char* v = std::getenv("HPG_TEAM");  // diagnostics: force the team size
+    return v ? std::atoi(v) : -1;
+  }();
+  cv.n_warps = (n <= 2 * ctx.n_sm && P.T >= 2) ? std::min(kMaxTeamWarps, P.T) : 1;
+  if (team_env >= 1) cv.n_warps = std::min(team_env, kMaxTeamWarps);
   int grid = 0;
   cuda_check(eval_grid(cv, n, ctx.n_sm, grid), "eval_kernel occupancy");
   const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);

@@ -622,7 +622,41 @@ __device__ __noinline__ void balance_layers_dev(const DevProblem& P, const DevCo
   }
 }
 
-__global__ void __launch_bounds__(32)
+// helper warps (team_task_costs): wait for jobs from the lead until it exits
+__device__ __noinline__ void team_helper(const DevProblem& P, const DevCostConfig& cfg, Ws* team,
+                                         int w) {
+  const int lane = threadIdx.x & 31;
+  Ws& s = team[w];
+  const Ws& s0 = team[0];
+  const int threads = 32 * s.n_warps;
+  while (true) {
+    bar_sync(1, threads);
+    const int kind = s0.job[0], mask = s0.job[1];
+    if (kind == kJobExit) return;
+    // the lead's current plan view
+    {
+      const int32_t* hs = reinterpret_cast<const int32_t*>(&s0.h);
+      int32_t* hd = reinterpret_cast<int32_t*>(&s.h);
+      for (int i = lane; i < static_cast<int>(sizeof(RecHeader) / 4); i += 32) hd[i] = hs[i];
+      const int32_t* os = reinterpret_cast<const int32_t*>(&s0.o);
+      int32_t* od = reinterpret_cast<int32_t*>(&s.o);
+      for (int i = lane; i < static_cast<int>(sizeof(RecOffsets) / 4); i += 32) od[i] = os[i];
+      if (lane == 0) {
+        s.memo_tp_ok = s0.memo_tp_ok;
+        s.memo_pp_ok = s0.memo_pp_ok;
+        s.memo_cm_ok = s0.memo_cm_ok;
+      }
+      __syncwarp();
+    }
+    team_share(P, cfg, s, kind, mask, w);
+    bar_sync(2, threads);
+  }
+}
+
+// kTeam = 1: one warp per CTA, register-capped for occupancy (big waves, the
+// sweep); kTeam = kMaxTeam: up to four warps per plan (small waves)
+template <int kTeam>
+__global__ void __launch_bounds__(32 * kTeam, kTeam == 1 ? 16 : 2)
 eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
             const uint8_t* __restrict__ recs, const int64_t* __restrict__ off,
             const int32_t* __restrict__ modes, int32_t uniform_mode, int n, int64_t stride,
@@ -630,15 +664,34 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
             double* __restrict__ per_task, double* __restrict__ required,
             double* __restrict__ gscratch, int64_t gscratch_doubles) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ Ws s;
+  __shared__ Ws team[kTeam];
   const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    carve(s, smem, cv);
-    s.dtab = gscratch + static_cast<int64_t>(blockIdx.x) * gscratch_doubles;
-    s.dtab_stride = 0;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    Ws& l = team[0];
+    uint8_t* p = carve(l, smem, cv);
+    l.dtab = gscratch + static_cast<int64_t>(blockIdx.x) * gscratch_doubles;
+    l.dtab_stride = 0;
+    l.prof = nullptr;
+    l.team = team;
+    l.n_warps = static_cast<int32_t>(blockDim.x >> 5);
+    l.job_words[0] = l.job_words[1] = 0;
+    l.job = l.job_words;
+    const bool smem_cls = l.cls != nullptr;
+    if (!smem_cls) l.cls = P.cls;
+    for (int w = 1; w < l.n_warps; ++w) {
+      team[w] = l;
+      p = carve_team_scratch(team[w], p, cv);
+    }
   }
-  __syncwarp();
-  stage_link_classes(P, s);
+  __syncthreads();
+  if (warp == 0 && cv.cls_smem) stage_link_classes(P, team[0]);
+  __syncthreads();
+  if (warp > 0) {
+    team_helper(P, cfg, team, warp);
+    return;
+  }
+  Ws& s = team[0];
   for (int p = blockIdx.x; p < n; p += gridDim.x) {
     const int64_t rec_at = off ? off[p] : static_cast<int64_t>(p) * stride;
     const uint8_t* rec = recs + rec_at;
@@ -715,6 +768,7 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
       const bool chain = mode == kModeEvaluate || mode == kModeChain;
       const bool go = mode != kModeEvaluate || feas_in;
       if (go) {
+        team_geometry(P, cfg, s);
         bool have_cur = false, ch = false;
         E2E cur;
         if ((chain && (kb_flags & 1)) || mode == kModeBalanceData) {
@@ -750,6 +804,7 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
     if (lane == 0) res[p] = r;
     __syncwarp();
   }
+  team_exit(s);
 }
 
 }  // namespace dev
@@ -770,35 +825,45 @@ int64_t eval_scratch_doubles(int n_dev, int64_t max_nl) {
   return 4 * static_cast<int64_t>(n_dev) * (max_nl + 2);
 }
 
-cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid) {
-  cv.bytes = carve2_bytes(cv);
+namespace {
+template <int kTeam>
+cudaError_t grid_for(Carve cv, int n, int n_sm, int& grid) {
+  auto kern = dev::eval_kernel<kTeam>;
   static int configured_bytes = 0;
   if (cv.bytes > 48 * 1024 && cv.bytes > configured_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(dev::eval_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
     if (e != cudaSuccess) return e;
     configured_bytes = cv.bytes;
   }
   // occupancy per dynamic-smem size (a few distinct sizes per problem)
-  static int cached_bytes[8] = {-1, -1, -1, -1, -1, -1, -1, -1}, cached_per_sm[8];
+  static int cached_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1}, cached_per_sm[8];
   static int next_slot = 0;
-  int per_sm = 0;
-  int hit = -1;
+  const int key = cv.bytes * 8 + cv.n_warps;
+  int per_sm = 0, hit = -1;
   for (int i = 0; i < 8; ++i)
-    if (cached_bytes[i] == cv.bytes) hit = i;
+    if (cached_key[i] == key) hit = i;
   if (hit >= 0) {
     per_sm = cached_per_sm[hit];
   } else {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::eval_kernel, 32,
-                                                                  cv.bytes);
+    cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * cv.n_warps, cv.bytes);
     if (e != cudaSuccess) return e;
-    cached_bytes[next_slot] = cv.bytes;
+    cached_key[next_slot] = key;
     cached_per_sm[next_slot] = per_sm;
     next_slot = (next_slot + 1) & 7;
   }
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   grid = n < n_sm * per_sm ? n : n_sm * per_sm;
   return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid) {
+  if (cv.n_warps < 1) cv.n_warps = 1;
+  cv.bytes = carve2_bytes(cv);
+  return cv.n_warps == 1 ? grid_for<1>(cv, n, n_sm, grid)
+                         : grid_for<dev::kMaxTeam>(cv, n, n_sm, grid);
 }
 
 cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
@@ -808,10 +873,19 @@ cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
                         double* d_required, double* d_scratch, int64_t scratch_doubles,
                         int grid, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (cv.n_warps < 1) cv.n_warps = 1;
+  if (cv.n_warps > dev::kMaxTeam) return cudaErrorInvalidValue;
   cv.bytes = carve2_bytes(cv);
-  dev::eval_kernel<<<grid, 32, cv.bytes, st>>>(P, cfg, cv, kb_flags, d_recs, d_off, d_modes,
-                                               uniform_mode, n, stride, d_out, d_res, d_per_task,
-                                               d_required, d_scratch, scratch_doubles);
+  if (cv.n_warps == 1) {
+    dev::eval_kernel<1><<<grid, 32, cv.bytes, st>>>(P, cfg, cv, kb_flags, d_recs, d_off, d_modes,
+                                                    uniform_mode, n, stride, d_out, d_res,
+                                                    d_per_task, d_required, d_scratch,
+                                                    scratch_doubles);
+  } else {
+    dev::eval_kernel<dev::kMaxTeam><<<grid, 32 * cv.n_warps, cv.bytes, st>>>(
+        P, cfg, cv, kb_flags, d_recs, d_off, d_modes, uniform_mode, n, stride, d_out, d_res,
+        d_per_task, d_required, d_scratch, scratch_doubles);
+  }
   return cudaGetLastError();
 }
 

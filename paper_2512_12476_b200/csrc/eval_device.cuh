@@ -93,7 +93,15 @@ struct Ws {
   double cc_vol;              // staged volume
   long long* prof;            // diagnostics: this plan's profile slots
   const uint8_t* cls;         // link class matrix [N*N]: shared-memory copy or P.cls
+  // helper-warp team (one plan per CTA, warp 0 leads)
+  Ws* team;                   // the CTA's Ws array (team[0] = lead)
+  int32_t n_warps;
+  volatile int32_t* job;      // [2]: kind, task mask (in team[0])
+  int32_t job_words[2];
 };
+
+constexpr int kMaxTeam = kMaxTeamWarps;
+constexpr int kJobTasks = 1, kJobExit = 2, kJobGeometry = 3;
 
 // diagnostics only (HPG_PLAN_PROFILE): per-plan clock64 phase stamps and
 // per-phase cycle accumulators (sub-phase k < 27 also lands in the plan's
@@ -103,7 +111,7 @@ __device__ unsigned long long g_phase_acc[32];
 #define HPG_PH_BEGIN(k) const long long ph_##k = g_plan_prof ? clock64() : 0
 #define HPG_PH_END(k)                                                         \
   do {                                                                        \
-    if (g_plan_prof && (threadIdx.x & 31) == 0) {                             \
+    if (g_plan_prof && s.prof && (threadIdx.x & 31) == 0) {                   \
       const long long dt_ = clock64() - ph_##k;                               \
       atomicAdd(&g_phase_acc[k], static_cast<unsigned long long>(dt_));       \
       if (k < 27) s.prof[5 + k] += dt_;                                       \
@@ -138,7 +146,7 @@ __device__ __forceinline__ uint8_t* carve_ptr(uint8_t*& p, int bytes) {
   return r;
 }
 
-__device__ inline void carve(Ws& s, uint8_t* base, const Carve& c) {
+__device__ inline uint8_t* carve(Ws& s, uint8_t* base, const Carve& c) {
   uint8_t* p = base;
   const int N = c.n_dev, T = c.n_tasks;
   s.w = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_w));
@@ -172,6 +180,27 @@ __device__ inline void carve(Ws& s, uint8_t* base, const Carve& c) {
   s.sl_save2 = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
   s.split_step = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
   s.cls = c.cls_smem ? carve_ptr(p, N * N) : nullptr;  // else P.cls (stage_link_classes)
+  return p;
+}
+
+// a helper warp's private scratch (team_scratch_bytes); everything else in its
+// Ws aliases the lead's plan state
+__device__ inline uint8_t* carve_team_scratch(Ws& s, uint8_t* p, const Carve& c) {
+  const int N = c.n_dev;
+  s.c_comp = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.c_tp = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.c_pp = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.c_hbm = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.edge = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
+  s.cc = reinterpret_cast<double*>(carve_ptr(p, 8 * kMaxClasses));
+  s.rm = reinterpret_cast<double*>(carve_ptr(p, 8 * 64));
+  s.tour = carve_ptr(p, N);
+  s.peers = carve_ptr(p, N);
+  return p;
+}
+
+__device__ __forceinline__ void bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // Stages the N x N link-class matrix in shared memory (once per CTA): every
@@ -179,11 +208,6 @@ __device__ inline void carve(Ws& s, uint8_t* base, const Carve& c) {
 __device__ inline void stage_link_classes(const DevProblem& P, Ws& s) {
   const int lane = threadIdx.x & 31;
   const int nn = P.n_dev * P.n_dev;
-  if (!s.cls) {
-    if (lane == 0) s.cls = P.cls;
-    __syncwarp();
-    return;
-  }
   uint8_t* dst = const_cast<uint8_t*>(s.cls);
   if ((nn & 7) == 0 && (reinterpret_cast<uintptr_t>(P.cls) & 7) == 0) {
     const uint2* src = reinterpret_cast<const uint2*>(P.cls);
@@ -1218,6 +1242,79 @@ struct E2E {
   bool feasible;
 };
 
+// ---- helper-warp team: the independent per-task task_cost calls of one
+// end_to_end are dealt round-robin over the CTA's warps (named barriers 1 =
+// job posted, 2 = job done). Each warp keeps its own memo bits and scratch;
+// the geometry memo arrays, aggregates and plan state are shared and every
+// task's region is written by one warp only. The lead merges the memo bits.
+
+__device__ __forceinline__ void team_share(const DevProblem& P, const DevCostConfig& cfg, Ws& s,
+                                           int kind, int mask, int w) {
+  int rank = 0;
+  for (int t = 0; t < P.n_tasks; ++t) {
+    if (!((mask >> t) & 1)) continue;
+    if (rank % s.n_warps == w) {
+      if (kind == kJobTasks) {
+        task_cost(P, cfg, s, t, true, s.agg + 7 * t);
+      } else {
+        ensure_geometry(P, s, t);
+      }
+    }
+    ++rank;
+  }
+}
+
+// lead side (warp 0): post a job, do the lead's share, wait, merge memo bits
+__device__ __noinline__ void team_job(const DevProblem& P, const DevCostConfig& cfg, Ws& s,
+                                      int kind, int mask) {
+  const int lane = threadIdx.x & 31;
+  const int threads = 32 * s.n_warps;
+  if (lane == 0) {
+    s.job[0] = kind;
+    s.job[1] = mask;
+  }
+  __syncwarp();
+  bar_sync(1, threads);
+  team_share(P, cfg, s, kind, mask, 0);
+  bar_sync(2, threads);
+  if (lane == 0) {
+    for (int w = 1; w < s.n_warps; ++w) {
+      s.memo_tp_ok |= s.team[w].memo_tp_ok;
+      s.memo_pp_ok |= s.team[w].memo_pp_ok;
+      s.memo_cm_ok |= s.team[w].memo_cm_ok;
+    }
+    if (kind == kJobTasks) s.agg_ok |= mask;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void team_task_costs(const DevProblem& P, const DevCostConfig& cfg,
+                                                Ws& s, int mask) {
+  team_job(P, cfg, s, kJobTasks, mask);
+}
+
+// every task's geometry memo (TP rings, PP pairs, slowest device per cell),
+// spread over the team; every evaluation needs all of it
+__device__ __forceinline__ void team_geometry(const DevProblem& P, const DevCostConfig& cfg,
+                                              Ws& s) {
+  if (s.n_warps <= 1) return;
+  int mask = 0;
+  for (int t = 0; t < P.n_tasks; ++t) {
+    const bool done = ((s.memo_cm_ok >> t) & 1) &&
+                      (s.h.tp[t] <= 1 || ((s.memo_tp_ok >> t) & 1)) &&
+                      (s.h.pp[t] <= 1 || ((s.memo_pp_ok >> t) & 1));
+    if (!done) mask |= 1 << t;
+  }
+  if (__popc(mask) >= 2) team_job(P, cfg, s, kJobGeometry, mask);
+}
+
+__device__ __noinline__ void team_exit(Ws& s) {
+  if (s.n_warps <= 1) return;
+  if ((threadIdx.x & 31) == 0) s.job[0] = kJobExit;
+  __syncwarp();
+  bar_sync(1, 32 * s.n_warps);
+}
+
 // end_to_end_cost (cost_model.cpp:431-487). Per-task aggregates land in s.agg.
 __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig& cfg, Ws& s) {
   const int lane = threadIdx.x & 31;
@@ -1242,6 +1339,12 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
     if (lane == 0) s.resident_ok = 1;
     __syncwarp();
     HPG_PH_END(22);
+  }
+  if (s.n_warps > 1) {
+    int pending = 0;
+    for (int t = 0; t < P.n_tasks; ++t)
+      if (!((s.agg_ok >> t) & 1)) pending |= 1 << t;
+    if (__popc(pending) >= 2) team_task_costs(P, cfg, s, pending);
   }
   double tot[kMaxTasks];
   for (int t = 0; t < P.n_tasks; ++t) {

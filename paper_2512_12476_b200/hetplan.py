@@ -276,7 +276,7 @@ def build_workflow(algorithm: str, mode: str, models: Dict[str, dict], batch: di
         wf.tasks.append(dict(id=i, kind=TASK_KIND[i], h1=m["hidden_size"],
                              h2=m["intermediate_size"], nl=m["num_layers"],
                              emb=bool(m.get("include_embedding", False)),
-                             vocab=m.get("vocab_size", 0), prec=m.get("precision_bytes", 2),
+                             vocab=m.get("vocab_size", 0), prec=2,
                              model_name=name))
     infs = [t["id"] for t in wf.tasks if t["kind"] == 1]
     trs = [t["id"] for t in wf.tasks if t["kind"] == 2]
