@@ -440,12 +440,25 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   // small waves are latency-bound on cold SMs: stage the class matrix in smem
   cv.cls_smem = (n <= 2 * ctx.n_sm && P.N * P.N <= kClsSmemMax) ? 1 : 0;
   // ... and get helper warps for the per-task costs of each plan
-  static const int team_env = [] {
-    const char* v = std::getenv("HPG_TEAM");  // diagnostics: force the team size
-    return v ? std::atoi(v) : -1;
+  static const int team_policy = [] {
+    const char* v = std::getenv("HPG_TEAM_POLICY");  // diagnostics: 0 off, 1 small only
+    return v ? std::atoi(v) : 2;
   }();
-  cv.n_warps = (n <= 2 * ctx.n_sm && P.T >= 2) ? std::min(kMaxTeamWarps, P.T) : 1;
-  if (team_env >= 1) cv.n_warps = std::min(team_env, kMaxTeamWarps);
+  // the largest team with which the whole wave is resident in one round
+  cv.n_warps = 1;
+  if (P.T >= 2 && team_policy >= 1) {
+    for (const int w : {std::min(kMaxTeamWarps, P.T), 2}) {
+      if (w == 2 && team_policy < 2) continue;
+      Carve ct = cv;
+      ct.n_warps = w;
+      int g = 0;
+      cuda_check(eval_grid(ct, n, ctx.n_sm, g), "eval_kernel occupancy");
+      if (g >= n) {
+        cv.n_warps = w;
+        break;
+      }
+    }
+  }
   int grid = 0;
   cuda_check(eval_grid(cv, n, ctx.n_sm, grid), "eval_kernel occupancy");
   const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);

@@ -654,9 +654,10 @@ __device__ __noinline__ void team_helper(const DevProblem& P, const DevCostConfi
 }
 
 // kTeam = 1: one warp per CTA, register-capped for occupancy (big waves, the
-// sweep); kTeam = kMaxTeam: up to four warps per plan (small waves)
+// sweep); kTeam = 2: pairs at the same register cap (medium waves);
+// kTeam = kMaxTeam: up to four warps per plan, uncapped (small waves)
 template <int kTeam>
-__global__ void __launch_bounds__(32 * kTeam, kTeam == 1 ? 16 : 2)
+__global__ void __launch_bounds__(32 * kTeam, kTeam == 1 ? 16 : (kTeam == 2 ? 8 : 2))
 eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
             const uint8_t* __restrict__ recs, const int64_t* __restrict__ off,
             const int32_t* __restrict__ modes, int32_t uniform_mode, int n, int64_t stride,
@@ -862,8 +863,9 @@ cudaError_t grid_for(Carve cv, int n, int n_sm, int& grid) {
 cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid) {
   if (cv.n_warps < 1) cv.n_warps = 1;
   cv.bytes = carve2_bytes(cv);
-  return cv.n_warps == 1 ? grid_for<1>(cv, n, n_sm, grid)
-                         : grid_for<dev::kMaxTeam>(cv, n, n_sm, grid);
+  if (cv.n_warps == 1) return grid_for<1>(cv, n, n_sm, grid);
+  if (cv.n_warps == 2) return grid_for<2>(cv, n, n_sm, grid);
+  return grid_for<dev::kMaxTeam>(cv, n, n_sm, grid);
 }
 
 cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
@@ -878,6 +880,11 @@ cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
   cv.bytes = carve2_bytes(cv);
   if (cv.n_warps == 1) {
     dev::eval_kernel<1><<<grid, 32, cv.bytes, st>>>(P, cfg, cv, kb_flags, d_recs, d_off, d_modes,
+                                                    uniform_mode, n, stride, d_out, d_res,
+                                                    d_per_task, d_required, d_scratch,
+                                                    scratch_doubles);
+  } else if (cv.n_warps == 2) {
+    dev::eval_kernel<2><<<grid, 64, cv.bytes, st>>>(P, cfg, cv, kb_flags, d_recs, d_off, d_modes,
                                                     uniform_mode, n, stride, d_out, d_res,
                                                     d_per_task, d_required, d_scratch,
                                                     scratch_doubles);
