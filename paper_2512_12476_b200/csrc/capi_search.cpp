@@ -199,7 +199,7 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
     DevProblem sweep_prob = C.dprob;
     sweep_prob.ring_cache = nullptr;
     cuda_check(launch_eval(sweep_prob, cfg, cv, 0, C.d_recs.p, nullptr, nullptr, kModeE2E,
-                           static_cast<int>(n), stride, nullptr, C.d_res.p, nullptr, nullptr,
+                           static_cast<int>(n), stride, nullptr, nullptr, C.d_res.p, nullptr, nullptr,
                            C.d_scratch.p, scratch, grid, st),
                "eval_kernel");
     cudaEventRecord(e2, st);

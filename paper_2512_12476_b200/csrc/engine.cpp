@@ -396,11 +396,15 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   Carve cv{};
   cv.n_dev = P.N;
   cv.n_tasks = P.T;
-  int64_t total = 0;
+  int64_t total = 0, ws_total = 0;
+  out.ws_off.resize(n);
   for (int i = 0; i < n; ++i) {
     const Cand& c = *b.cands[i];
     out.off[i] = total;
     total += c.o.bytes;
+    out.ws_off[i] = ws_total;
+    // balanced sections [weights | stage layers], 8-aligned for the doubles
+    ws_total += (c.o.dev_byte - c.o.w_byte + 7) & ~int64_t(7);
     const int T = P.T;
     cv.max_w = std::max(cv.max_w, c.o.w[T]);
     cv.max_sl = std::max(cv.max_sl, c.o.sl[T]);
@@ -408,22 +412,52 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     cv.max_cells = std::max(cv.max_cells, c.o.cell[T]);
     cv.max_dpk = std::max(cv.max_dpk, c.o.dpk[T]);
   }
-  // one input transfer: [offsets i64 | modes i32 (8-aligned) | records]
-  const int64_t in_off = 0, in_modes = 8 * static_cast<int64_t>(n),
-                in_recs = in_modes + ((4 * static_cast<int64_t>(n) + 7) & ~int64_t(7));
+  // one input transfer: [offsets i64 | out offsets i64 | modes i32 (8-aligned) | records]
+  const int64_t nn = static_cast<int64_t>(n);
+  const int64_t in_off = 0, in_ooff = 8 * nn, in_modes = 16 * nn,
+                in_recs = in_modes + ((4 * nn + 7) & ~int64_t(7));
   const int64_t in_bytes = in_recs + total;
   ctx.h_recs.reserve(in_bytes);
   int64_t* h_off = reinterpret_cast<int64_t*>(ctx.h_recs.p + in_off);
+  int64_t* h_ooff = reinterpret_cast<int64_t*>(ctx.h_recs.p + in_ooff);
   int32_t* h_modes = reinterpret_cast<int32_t*>(ctx.h_recs.p + in_modes);
   uint8_t* h_rec = ctx.h_recs.p + in_recs;
-  host_parallel_for(n, n >= 4096, [&](int i) {
-    std::memcpy(h_rec + out.off[i], b.cands[i]->rec.data(), b.cands[i]->o.bytes);
-    h_off[i] = out.off[i];
-    h_modes[i] = b.modes[i];
+  // canonical bytes: tg id + k counts + per task
+  // (3 + pp + slots) + 9 result bytes (+ 8*dp for a weighted generation task)
+  auto canonical = [&](const Cand& c) {
+    int64_t cb = 1 + c.ng + 9;
+    for (int t = 0; t < P.T; ++t) cb += 3 + c.hdr().pp[t] + c.size(t);
+    const int g = P.slot_of_id[1];
+    if (g >= 0) {
+      const double* w = c.w() + c.o.w[g];
+      for (int k = 0; k < c.hdr().dp[g]; ++k)
+        if (w[k] != 1.0) {
+          cb += 8 * c.hdr().dp[g];
+          break;
+        }
+    }
+    return cb;
+  };
+  const int n_chunks = n >= 256 ? 16 : 1;
+  int64_t cb_part[16] = {};
+  host_parallel_for(n_chunks, n_chunks > 1, [&](int ch) {
+    const int i0 = static_cast<int>(static_cast<int64_t>(n) * ch / n_chunks);
+    const int i1 = static_cast<int>(static_cast<int64_t>(n) * (ch + 1) / n_chunks);
+    int64_t cb = 0;
+    for (int i = i0; i < i1; ++i) {
+      const Cand& c = *b.cands[i];
+      std::memcpy(h_rec + out.off[i], c.rec.data(), c.o.bytes);
+      h_off[i] = out.off[i];
+      h_ooff[i] = out.ws_off[i];
+      h_modes[i] = b.modes[i];
+      cb += canonical(c);
+    }
+    cb_part[ch] = cb;
   });
-  // one output transfer: [results 32 B each | balanced records]
-  const int64_t out_res = 0, out_recs = 32 * static_cast<int64_t>(n);
-  const int64_t out_bytes = out_recs + (want_out ? total : 0);
+  for (int ch = 0; ch < n_chunks; ++ch) ctx.canonical_bytes += cb_part[ch];
+  // one output transfer: [results 32 B each | balanced weight / split sections]
+  const int64_t out_res = 0, out_ws = 32 * nn;
+  const int64_t out_bytes = out_ws + (want_out ? ws_total : 0);
   ctx.d_recs.reserve(in_bytes);
   ctx.d_out.reserve(out_bytes);
   if (want_per_task) ctx.d_per_task.reserve(static_cast<size_t>(n) * P.T * 7);
@@ -433,10 +467,11 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, in_bytes, cudaMemcpyHostToDevice, st),
              "H2D wave");
   const int64_t* d_off = reinterpret_cast<const int64_t*>(ctx.d_recs.p + in_off);
+  const int64_t* d_ooff = reinterpret_cast<const int64_t*>(ctx.d_recs.p + in_ooff);
   const int32_t* d_modes = reinterpret_cast<const int32_t*>(ctx.d_recs.p + in_modes);
   const uint8_t* d_rec = ctx.d_recs.p + in_recs;
   EvalResult* d_res = reinterpret_cast<EvalResult*>(ctx.d_out.p + out_res);
-  uint8_t* d_orec = want_out ? ctx.d_out.p + out_recs : nullptr;
+  uint8_t* d_ows = want_out ? ctx.d_out.p + out_ws : nullptr;
   // small waves are latency-bound on cold SMs: stage the class matrix in smem
   cv.cls_smem = (n <= 2 * ctx.n_sm && P.N * P.N <= kClsSmemMax) ? 1 : 0;
   // ... and get helper warps for the per-task costs of each plan
@@ -452,7 +487,11 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
       Carve ct = cv;
       ct.n_warps = w;
       int g = 0;
-      cuda_check(eval_grid(ct, n, ctx.n_sm, g), "eval_kernel occupancy");
+      const cudaError_t e = eval_grid(ct, n, ctx.n_sm, g);  // too much smem: no team
+      if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        continue;
+      }
       if (g >= n) {
         cv.n_warps = w;
         break;
@@ -472,8 +511,8 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     cuda_check(eval_set_plan_profile(d_prof), "profile symbol");
   }
   cuda_check(cudaEventRecord(ctx.ev0, st), "event");
-  cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, d_rec, d_off, d_modes, 0, n, 0, d_orec,
-                         d_res, want_per_task ? ctx.d_per_task.p : nullptr,
+  cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, d_rec, d_off, d_modes, 0, n, 0, d_ows,
+                         d_ooff, d_res, want_per_task ? ctx.d_per_task.p : nullptr,
                          want_required ? ctx.d_required.p : nullptr, ctx.d_scratch.p, scratch,
                          grid, st),
              "eval_kernel launch");
@@ -484,27 +523,10 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   ctx.h2d_bytes += in_bytes;
   ctx.d2h_bytes += out_bytes + (want_per_task ? 8 * static_cast<int64_t>(n) * P.T * 7 : 0) +
                    (want_required ? 8 * static_cast<int64_t>(n) * P.N : 0);
-  for (int i = 0; i < n; ++i) {
-    // canonical bytes: tg id + k counts + per task
-    // (3 + pp + slots) + 9 result bytes (+ 8*dp for a weighted generation task)
-    const Cand& c = *b.cands[i];
-    int64_t cb = 1 + c.ng + 9;
-    for (int t = 0; t < P.T; ++t) cb += 3 + c.hdr().pp[t] + c.size(t);
-    const int g = P.slot_of_id[1];
-    if (g >= 0) {
-      const double* w = c.w() + c.o.w[g];
-      for (int k = 0; k < c.hdr().dp[g]; ++k)
-        if (w[k] != 1.0) {
-          cb += 8 * c.hdr().dp[g];
-          break;
-        }
-    }
-    ctx.canonical_bytes += cb;
-  }
   ctx.h_out.reserve(out_bytes);
   cuda_check(cudaMemcpyAsync(ctx.h_out.p, ctx.d_out.p, out_bytes, cudaMemcpyDeviceToHost, st),
              "D2H wave");
-  out.out_recs = want_out ? ctx.h_out.p + out_recs : nullptr;
+  out.out_ws = want_out ? ctx.h_out.p + out_ws : nullptr;
   if (want_per_task) out.per_task.resize(static_cast<size_t>(n) * P.T * 7);
   if (want_required) out.required.resize(static_cast<size_t>(n) * P.N);
   if (want_per_task)

@@ -152,8 +152,10 @@ void dist_destroy(Dist& d);
 
 struct BatchOut {
   std::vector<EvalResult> res;
-  const uint8_t* out_recs = nullptr;  // balanced records, same offsets as packed input
-  std::vector<int64_t> off;
+  // balanced [weights | stage layers] section of plan i (the record bytes
+  // [o.w_byte, o.dev_byte)) at out_ws + ws_off[i]; devices never change
+  const uint8_t* out_ws = nullptr;
+  std::vector<int64_t> off, ws_off;
   std::vector<double> per_task;          // if requested
   std::vector<double> required;          // if requested
 };

@@ -661,7 +661,8 @@ __global__ void __launch_bounds__(32 * kTeam, kTeam == 1 ? 16 : (kTeam == 2 ? 8 
 eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
             const uint8_t* __restrict__ recs, const int64_t* __restrict__ off,
             const int32_t* __restrict__ modes, int32_t uniform_mode, int n, int64_t stride,
-            uint8_t* __restrict__ out_recs, EvalResult* __restrict__ res,
+            uint8_t* __restrict__ out_ws, const int64_t* __restrict__ out_off,
+            EvalResult* __restrict__ res,
             double* __restrict__ per_task, double* __restrict__ required,
             double* __restrict__ gscratch, int64_t gscratch_doubles) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -790,16 +791,14 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
         if (cur.feasible) r.flags |= kResFeasOut;
       }
     }
-    // ---- write back ----
-    if (out_recs) {
-      uint8_t* orec = out_recs + rec_at;
-      if (lane < 20) reinterpret_cast<int32_t*>(orec)[lane] = reinterpret_cast<const int32_t*>(&s.h)[lane];
-      double* ow = reinterpret_cast<double*>(orec + s.o.w_byte);
-      int32_t* osl = reinterpret_cast<int32_t*>(orec + s.o.sl_byte);
-      uint8_t* odev = orec + s.o.dev_byte;
+    // ---- write back: the record's [weights | stage layers] bytes (devices
+    // and layouts never change) ----
+    if (out_ws && !(s.h.n_tasks & kRecCompact)) {
+      uint8_t* ows = out_ws + out_off[p];
+      double* ow = reinterpret_cast<double*>(ows);
+      int32_t* osl = reinterpret_cast<int32_t*>(ows + (s.o.sl_byte - s.o.w_byte));
       for (int i = lane; i < nw; i += 32) ow[i] = s.w[i];
       for (int i = lane; i < nsl; i += 32) osl[i] = s.sl[i];
-      for (int i = lane; i < nslot; i += 32) odev[i] = s.dev[i];
     }
     if (prof && lane == 0) prof[4] = clock64();
     if (lane == 0) res[p] = r;
@@ -871,7 +870,8 @@ cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid) {
 cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
                         int32_t kb_flags, const uint8_t* d_recs, const int64_t* d_off,
                         const int32_t* d_modes, int32_t uniform_mode, int n, int64_t stride,
-                        uint8_t* d_out, EvalResult* d_res, double* d_per_task,
+                        uint8_t* d_out, const int64_t* d_out_off, EvalResult* d_res,
+                        double* d_per_task,
                         double* d_required, double* d_scratch, int64_t scratch_doubles,
                         int grid, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
@@ -880,17 +880,17 @@ cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
   cv.bytes = carve2_bytes(cv);
   if (cv.n_warps == 1) {
     dev::eval_kernel<1><<<grid, 32, cv.bytes, st>>>(P, cfg, cv, kb_flags, d_recs, d_off, d_modes,
-                                                    uniform_mode, n, stride, d_out, d_res,
+                                                    uniform_mode, n, stride, d_out, d_out_off, d_res,
                                                     d_per_task, d_required, d_scratch,
                                                     scratch_doubles);
   } else if (cv.n_warps == 2) {
     dev::eval_kernel<2><<<grid, 64, cv.bytes, st>>>(P, cfg, cv, kb_flags, d_recs, d_off, d_modes,
-                                                    uniform_mode, n, stride, d_out, d_res,
+                                                    uniform_mode, n, stride, d_out, d_out_off, d_res,
                                                     d_per_task, d_required, d_scratch,
                                                     scratch_doubles);
   } else {
     dev::eval_kernel<dev::kMaxTeam><<<grid, 32 * cv.n_warps, cv.bytes, st>>>(
-        P, cfg, cv, kb_flags, d_recs, d_off, d_modes, uniform_mode, n, stride, d_out, d_res,
+        P, cfg, cv, kb_flags, d_recs, d_off, d_modes, uniform_mode, n, stride, d_out, d_out_off, d_res,
         d_per_task, d_required, d_scratch, scratch_doubles);
   }
   return cudaGetLastError();

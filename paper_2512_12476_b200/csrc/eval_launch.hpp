@@ -24,7 +24,8 @@ cudaError_t eval_grid(Carve cv, int n, int n_sm, int& grid);
 cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
                         int32_t kb_flags, const uint8_t* d_recs, const int64_t* d_off,
                         const int32_t* d_modes, int32_t uniform_mode, int n, int64_t stride,
-                        uint8_t* d_out, EvalResult* d_res, double* d_per_task,
+                        uint8_t* d_out, const int64_t* d_out_off, EvalResult* d_res,
+                        double* d_per_task,
                         double* d_required, double* d_scratch, int64_t scratch_doubles,
                         int grid, cudaStream_t st);
 

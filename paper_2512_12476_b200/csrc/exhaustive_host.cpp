@@ -216,7 +216,7 @@ SearchOut exhaustive_search(Ctx& ctx, const Knobs& K) {
     int grid = 0;
     cuda_check(eval_grid(cv, static_cast<int>(R), ctx.n_sm, grid), "eval occupancy");
     cuda_check(launch_eval(ctx.dprob, cfg, cv, 0, recs.p, nullptr, ctx.d_modes.p, 0,
-                           static_cast<int>(R), stride, nullptr, res.p, nullptr, nullptr,
+                           static_cast<int>(R), stride, nullptr, nullptr, res.p, nullptr, nullptr,
                            ctx.d_scratch.p, scratch, grid, st),
                "eval_kernel");
     cuda_check(launch_exh_reduce(res.p, static_cast<int64_t>(R), part_p + blocks[bi].part_off,
