@@ -478,6 +478,8 @@ struct ArmRun {
   double* clock = nullptr;
   int owner = 0;  // rank that runs it (multi-GPU)
   int64_t n_offspring = 0, n_spec_hit = 0;  // diagnostics
+  double t_make = 0, t_mut = 0, t_swap = 0, t_spec = 0;  // diagnostics (s)
+  int64_t n_make = 0;
 };
 
 // ga_run (search.cpp:437-565) as a coroutine.
@@ -530,10 +532,13 @@ ArmCoro ga_run(ArmRun& run) {
     req.cands.assign(chunk, Cand{});
     snaps.clear();
     const int64_t combo0 = combo;
+    const double tm0 = now_s();
     for (int64_t c = 0; c < chunk; ++c) {
       make_candidate(e, combo++, rng, req.cands[c]);
       snaps.push_back(rng);
     }
+    run.t_make += now_s() - tm0;
+    run.n_make += chunk;
     co_await EvalAwait{&req};
     for (int64_t c = 0; c < chunk; ++c) {
       ++attempts;
@@ -563,19 +568,21 @@ ArmCoro ga_run(ArmRun& run) {
     Rng start, after_all;
     int ntr = 0;
   };
-  auto draw_mut = [&](Rng r, const Cand& parent, MutStage& m) {
-    m.cands.clear();
+  // draws the trials (+ the parent) straight into `out`; m keeps the snapshots
+  auto draw_mut = [&](Rng r, const Cand& parent, MutStage& m, std::vector<Cand>& out) {
     m.snaps.clear();
     m.ntr = 0;
     for (int tries = 0; tries < 8; ++tries) {
-      Cand trial = parent;
-      if (!mutate(e, trial, r)) break;
-      m.cands.push_back(std::move(trial));
+      out.push_back(parent);
+      if (!mutate(e, out.back(), r)) {
+        out.pop_back();
+        break;
+      }
       m.snaps.push_back(r);
       ++m.ntr;
     }
     m.after_all = r;
-    m.cands.push_back(parent);
+    out.push_back(parent);
   };
   // speculative next mutation stage from RNG state r, assuming (child, cost)
   // is inserted as it stands; appended to req after index base
@@ -592,9 +599,8 @@ ArmCoro ga_run(ArmRun& run) {
     Rng rr = r;
     const size_t i = static_cast<size_t>(rr.bounded(n_spec));
     const Cand& parent = !ins || i < pos ? pop[i].plan : (i == pos ? ch : pop[i - 1].plan);
-    draw_mut(rr, parent, spec);
+    draw_mut(rr, parent, spec, req.cands);
     spec.start = r;
-    for (const Cand& c : spec.cands) req.cands.push_back(c);
   };
   auto same_rng = [](const Rng& a, const Rng& b) {
     return a.seed == b.seed && a.s[0] == b.s[0] && a.s[1] == b.s[1] && a.s[2] == b.s[2] &&
@@ -611,8 +617,10 @@ ArmCoro ga_run(ArmRun& run) {
     } else {
       Rng r = rng;
       const size_t i = static_cast<size_t>(r.bounded(pop.size()));
-      draw_mut(r, pop[i].plan, cur);
-      req.cands = cur.cands;
+      req.cands.clear();
+      const double tu0 = now_s();
+      draw_mut(r, pop[i].plan, cur, req.cands);
+      run.t_mut += now_s() - tu0;
       co_await EvalAwait{&req};
       cur.res = req.res;
       cur.cands = std::move(req.cands);
@@ -682,8 +690,9 @@ ArmCoro ga_run(ArmRun& run) {
     // keeps the speculative stage at req[base...] if the walk accepted nothing
     auto take_spec = [&](int base, int w) {
       if (w != 0) return;
-      const int ns = static_cast<int>(spec.cands.size());
+      const int ns = spec.ntr + 1;
       spec.res.assign(req.res.begin() + base, req.res.begin() + base + ns);
+      spec.cands.resize(ns);
       for (int k = 0; k < ns; ++k) spec.cands[k] = std::move(req.cands[base + k]);
       have_spec = true;
     };
@@ -692,12 +701,16 @@ ArmCoro ga_run(ArmRun& run) {
       snaps.clear();
       snaps5.clear();
       const Rng before3 = rng;
+      const double ts0 = now_s();
       const int n3 = draw(3, snaps);
       const Rng before5 = rng;
       const int n5 = draw(5, snaps5);
+      run.t_swap += now_s() - ts0;
       if (n3 + n5 > 0) {
         const int base = static_cast<int>(req.cands.size());
+        const double tp0 = now_s();
         speculate(n5 > 0 ? snaps5.back() : before5, child, cost);
+        run.t_spec += now_s() - tp0;
         co_await EvalAwait{&req};
         rng = before5;  // stream position after the level-3 draws (walk may rewind it)
         const int w3 = walk(0, n3, before3, snaps);
@@ -797,15 +810,24 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
   static const char* spec_log = std::getenv("HPG_SPEC_LOG");  // diagnostics only
   if (spec_log) {
     if (FILE* f = std::fopen(spec_log, "a")) {
-      int64_t off = 0, hit = 0, used = 0;
+      int64_t off = 0, hit = 0, used = 0, nm = 0;
+      double tm = 0, tu = 0, ts = 0, tp = 0;
       for (ArmRun* r : runs) {
         off += r->n_offspring;
         hit += r->n_spec_hit;
         used += r->used;
+        nm += r->n_make;
+        tm += r->t_make;
+        tu += r->t_mut;
+        ts += r->t_swap;
+        tp += r->t_spec;
       }
-      std::fprintf(f, "runs %zu used %lld offspring %lld spec_hits %lld waves_total %lld\n",
+      std::fprintf(f,
+                   "runs %zu used %lld offspring %lld spec_hits %lld waves_total %lld "
+                   "make %lld %.2fms mut %.2fms swap %.2fms spec %.2fms\n",
                    runs.size(), static_cast<long long>(used), static_cast<long long>(off),
-                   static_cast<long long>(hit), static_cast<long long>(waves));
+                   static_cast<long long>(hit), static_cast<long long>(waves),
+                   static_cast<long long>(nm), 1e3 * tm, 1e3 * tu, 1e3 * ts, 1e3 * tp);
       std::fclose(f);
     }
   }
