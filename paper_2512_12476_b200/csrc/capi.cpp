@@ -188,10 +188,10 @@ int hpg_balance(hpg_ctx* ctx, const hpg_plan_table* plans, const hpg_cost_config
     run_batch(C, b, to_dev_cfg(c), which == 3 ? 3 : 0, true, false, false, bo);
     const int T = C.prob.T;
     for (size_t i = 0; i < tps.size(); ++i) {
-      const Cand& in = tps[i].cand;
-      const uint8_t* ws = bo.out_ws + bo.ws_off[i];  // [weights | stage layers]
-      const double* w = reinterpret_cast<const double*>(ws);
-      const int32_t* sl = reinterpret_cast<const int32_t*>(ws + (in.o.sl_byte - in.o.w_byte));
+      Cand& in = tps[i].cand;
+      apply_ws(C.prob, in, bo.out_ws + bo.ws_off[i]);
+      const double* w = in.w();
+      const int32_t* sl = in.sl();
       for (int s = 0; s < T; ++s) {
         if (out_stage_layers) {
           const int64_t so = plans->sl_off[static_cast<int64_t>(i) * T + s];

@@ -1,6 +1,8 @@
 // Problem staging, plan validation/packing and the batched device call.
 #include "engine.hpp"
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -257,8 +259,9 @@ Ctx::~Ctx() {
   if (dist.comm) dist_destroy(dist);
   if (d_blob) cudaFree(d_blob);
   if (d_sweep_tables) cudaFree(d_sweep_tables);
-  if (ev0) cudaEventDestroy(ev0);
-  if (ev1) cudaEventDestroy(ev1);
+  for (cudaEvent_t e : {ev0, ev1, ev2, ev3, ev_done[0], ev_done[1], ev_x[0], ev_x[1], ev_x[2], ev_x[3],
+                        ev_x[4], ev_x[5]})
+    if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -281,7 +284,36 @@ Ctx* create_ctx(const hpg_problem& hp, int device) {
     cuda_check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreate(&ctx->ev0), "event");
     cuda_check(cudaEventCreate(&ctx->ev1), "event");
+    cuda_check(cudaEventCreate(&ctx->ev2), "event");
+    cuda_check(cudaEventCreate(&ctx->ev3), "event");
+    cuda_check(cudaEventCreateWithFlags(&ctx->ev_done[0], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ctx->ev_done[1], cudaEventDisableTiming), "event");
+    for (cudaEvent_t& e : ctx->ev_x) cuda_check(cudaEventCreate(&e), "event");
     stage_problem(*ctx, std::move(P));
+    if (std::getenv("HPG_BW_TEST")) {  // diagnostics: copy bandwidth through the wave buffers
+      for (const size_t mb : {1, 8, 64}) {
+        const size_t n = mb << 20;
+        ctx->h_recs.reserve(n);
+        ctx->d_recs.reserve(n);
+        std::memset(ctx->h_recs.p, 1, n);
+        float ms_h = 0.f, ms_d = 0.f;
+        for (int rep = 0; rep < 3; ++rep) {
+          if (std::getenv("HPG_BW_DIRTY")) std::memset(ctx->h_recs.p, rep, n);  // hot, dirty lines
+          cudaEventRecord(ctx->ev0, ctx->stream);
+          cudaMemcpyAsync(ctx->d_recs.p, ctx->h_recs.p, n, cudaMemcpyHostToDevice, ctx->stream);
+          cudaEventRecord(ctx->ev1, ctx->stream);
+          cudaMemcpyAsync(ctx->h_recs.p, ctx->d_recs.p, n, cudaMemcpyDeviceToHost, ctx->stream);
+          cudaEventRecord(ctx->ev2, ctx->stream);
+          cudaStreamSynchronize(ctx->stream);
+          cudaEventElapsedTime(&ms_h, ctx->ev0, ctx->ev1);
+          cudaEventElapsedTime(&ms_d, ctx->ev1, ctx->ev2);
+        }
+        unsigned int flags = 0;
+        cudaHostGetFlags(&flags, ctx->h_recs.p);
+        std::fprintf(stderr, "hpg bw %zu MB: H2D %.1f GB/s D2H %.1f GB/s (host flags %u)\n", mb,
+                     n / ms_h / 1e6, n / ms_d / 1e6, flags);
+      }
+    }
   } catch (...) {
     delete ctx;
     throw;
@@ -383,28 +415,82 @@ void stage_problem(Ctx& ctxr, Problem&& P) {
   }
 }
 
-void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags, bool want_out,
-               bool want_per_task, bool want_required, BatchOut& out) {
+namespace {
+
+// What balancing can change: the generation task's replica weights
+// (balance_data) and every task's stage split (balance_layers); the other
+// weights stay 1.0 and devices never move. A wave returns [gen weights |
+// stage layers] per plan, 8-aligned.
+inline int64_t ws_bytes_of(const Problem& P, const Cand& c) {
+  const int g = P.slot_of_id[1];
+  const int64_t wg = g >= 0 ? 8 * static_cast<int64_t>(c.hdr().dp[g]) : 0;
+  return (wg + 4 * static_cast<int64_t>(c.o.sl[P.T]) + 7) & ~int64_t(7);
+}
+
+// Copy into pinned staging with non-temporal stores: the H2D DMA then reads
+// DRAM instead of snooping lines left dirty in 16 cores' private caches
+// (measured: 5 GB/s with dirty lines vs 50+ GB/s).
+inline void nt_copy(uint8_t* dst, const uint8_t* src, size_t n) {
+  while (n && (reinterpret_cast<uintptr_t>(dst) & 15)) {
+    *dst++ = *src++;
+    --n;
+  }
+  for (; n >= 16; n -= 16, dst += 16, src += 16)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst),
+                     _mm_loadu_si128(reinterpret_cast<const __m128i*>(src)));
+  while (n--) *dst++ = *src++;
+}
+
+// one wave = one eval_kernel launch; staged (packed + enqueued) and finished
+// (synchronised + unpacked) separately so consecutive chunks of a very large
+// wave overlap host packing with the device work of the previous chunk
+struct WaveBufs {
+  HostBuf<uint8_t>* h_in;
+  DevBuf<uint8_t>* d_in;
+  DevBuf<uint8_t>* d_out;
+  HostBuf<uint8_t>* h_out;
+  cudaEvent_t e0, e1, done, eh, ed, ex;
+};
+
+struct WaveJob {
+  int n = 0;
+  int64_t in_bytes = 0, out_bytes = 0, ws_total = 0;
+  long long* d_prof = nullptr;
+  WaveBufs buf{};
+  std::chrono::steady_clock::time_point t0, t1, t2;
+};
+
+WaveBufs wave_bufs(Ctx& ctx, int set) {
+  if (set == 0)
+    return {&ctx.h_recs, &ctx.d_recs, &ctx.d_out, &ctx.h_out, ctx.ev0, ctx.ev1, ctx.ev_done[0],
+            ctx.ev_x[0], ctx.ev_x[1], ctx.ev_x[4]};
+  return {&ctx.h_recs2, &ctx.d_recs2, &ctx.d_out2, &ctx.h_out2, ctx.ev2, ctx.ev3, ctx.ev_done[1],
+          ctx.ev_x[2], ctx.ev_x[3], ctx.ev_x[5]};
+}
+
+void wave_stage(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags, bool want_out,
+                bool want_per_task, bool want_required, const WaveBufs& buf, BatchOut& out,
+                WaveJob& job) {
   const int n = static_cast<int>(b.cands.size());
+  job = WaveJob{};
+  job.n = n;
+  job.buf = buf;
   out.res.resize(n);
   out.off.resize(n);
+  out.ws_off.resize(n);
   if (n == 0) return;
-  static const char* batch_log = std::getenv("HPG_BATCH_LOG");  // diagnostics only
-  const auto bt0 = std::chrono::steady_clock::now();
-  auto bt1 = bt0, bt2 = bt0, bt3 = bt0;
+  job.t0 = std::chrono::steady_clock::now();
   const Problem& P = ctx.prob;
   Carve cv{};
   cv.n_dev = P.N;
   cv.n_tasks = P.T;
   int64_t total = 0, ws_total = 0;
-  out.ws_off.resize(n);
   for (int i = 0; i < n; ++i) {
     const Cand& c = *b.cands[i];
     out.off[i] = total;
     total += c.o.bytes;
     out.ws_off[i] = ws_total;
-    // balanced sections [weights | stage layers], 8-aligned for the doubles
-    ws_total += (c.o.dev_byte - c.o.w_byte + 7) & ~int64_t(7);
+    ws_total += ws_bytes_of(P, c);
     const int T = P.T;
     cv.max_w = std::max(cv.max_w, c.o.w[T]);
     cv.max_sl = std::max(cv.max_sl, c.o.sl[T]);
@@ -412,16 +498,18 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     cv.max_cells = std::max(cv.max_cells, c.o.cell[T]);
     cv.max_dpk = std::max(cv.max_dpk, c.o.dpk[T]);
   }
+  job.ws_total = ws_total;
   // one input transfer: [offsets i64 | out offsets i64 | modes i32 (8-aligned) | records]
   const int64_t nn = static_cast<int64_t>(n);
   const int64_t in_off = 0, in_ooff = 8 * nn, in_modes = 16 * nn,
                 in_recs = in_modes + ((4 * nn + 7) & ~int64_t(7));
   const int64_t in_bytes = in_recs + total;
-  ctx.h_recs.reserve(in_bytes);
-  int64_t* h_off = reinterpret_cast<int64_t*>(ctx.h_recs.p + in_off);
-  int64_t* h_ooff = reinterpret_cast<int64_t*>(ctx.h_recs.p + in_ooff);
-  int32_t* h_modes = reinterpret_cast<int32_t*>(ctx.h_recs.p + in_modes);
-  uint8_t* h_rec = ctx.h_recs.p + in_recs;
+  job.in_bytes = in_bytes;
+  buf.h_in->reserve(in_bytes);
+  int64_t* h_off = reinterpret_cast<int64_t*>(buf.h_in->p + in_off);
+  int64_t* h_ooff = reinterpret_cast<int64_t*>(buf.h_in->p + in_ooff);
+  int32_t* h_modes = reinterpret_cast<int32_t*>(buf.h_in->p + in_modes);
+  uint8_t* h_rec = buf.h_in->p + in_recs;
   // canonical bytes: tg id + k counts + per task
   // (3 + pp + slots) + 9 result bytes (+ 8*dp for a weighted generation task)
   auto canonical = [&](const Cand& c) {
@@ -446,32 +534,37 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     int64_t cb = 0;
     for (int i = i0; i < i1; ++i) {
       const Cand& c = *b.cands[i];
-      std::memcpy(h_rec + out.off[i], c.rec.data(), c.o.bytes);
+      nt_copy(h_rec + out.off[i], c.rec.data(), c.o.bytes);
       h_off[i] = out.off[i];
       h_ooff[i] = out.ws_off[i];
       h_modes[i] = b.modes[i];
       cb += canonical(c);
     }
+    _mm_sfence();
     cb_part[ch] = cb;
   });
   for (int ch = 0; ch < n_chunks; ++ch) ctx.canonical_bytes += cb_part[ch];
   // one output transfer: [results 32 B each | balanced weight / split sections]
   const int64_t out_res = 0, out_ws = 32 * nn;
   const int64_t out_bytes = out_ws + (want_out ? ws_total : 0);
-  ctx.d_recs.reserve(in_bytes);
-  ctx.d_out.reserve(out_bytes);
+  job.out_bytes = out_bytes;
+  buf.d_in->reserve(in_bytes);
+  buf.d_out->reserve(out_bytes);
   if (want_per_task) ctx.d_per_task.reserve(static_cast<size_t>(n) * P.T * 7);
   if (want_required) ctx.d_required.reserve(static_cast<size_t>(n) * P.N);
   cudaStream_t st = ctx.stream;
-  if (batch_log) bt1 = std::chrono::steady_clock::now();
-  cuda_check(cudaMemcpyAsync(ctx.d_recs.p, ctx.h_recs.p, in_bytes, cudaMemcpyHostToDevice, st),
+  job.t1 = std::chrono::steady_clock::now();
+  static const bool batch_log = std::getenv("HPG_BATCH_LOG") != nullptr;  // diagnostics only
+  if (batch_log) cuda_check(cudaEventRecord(buf.eh, st), "event");
+  cuda_check(cudaMemcpyAsync(buf.d_in->p, buf.h_in->p, in_bytes, cudaMemcpyHostToDevice, st),
              "H2D wave");
-  const int64_t* d_off = reinterpret_cast<const int64_t*>(ctx.d_recs.p + in_off);
-  const int64_t* d_ooff = reinterpret_cast<const int64_t*>(ctx.d_recs.p + in_ooff);
-  const int32_t* d_modes = reinterpret_cast<const int32_t*>(ctx.d_recs.p + in_modes);
-  const uint8_t* d_rec = ctx.d_recs.p + in_recs;
-  EvalResult* d_res = reinterpret_cast<EvalResult*>(ctx.d_out.p + out_res);
-  uint8_t* d_ows = want_out ? ctx.d_out.p + out_ws : nullptr;
+  if (batch_log) cuda_check(cudaEventRecord(buf.ex, st), "event");
+  const int64_t* d_off = reinterpret_cast<const int64_t*>(buf.d_in->p + in_off);
+  const int64_t* d_ooff = reinterpret_cast<const int64_t*>(buf.d_in->p + in_ooff);
+  const int32_t* d_modes = reinterpret_cast<const int32_t*>(buf.d_in->p + in_modes);
+  const uint8_t* d_rec = buf.d_in->p + in_recs;
+  EvalResult* d_res = reinterpret_cast<EvalResult*>(buf.d_out->p + out_res);
+  uint8_t* d_ows = want_out ? buf.d_out->p + out_ws : nullptr;
   // small waves are latency-bound on cold SMs: stage the class matrix in smem
   cv.cls_smem = (n <= 2 * ctx.n_sm && P.N * P.N <= kClsSmemMax) ? 1 : 0;
   // ... and get helper warps for the per-task costs of each plan
@@ -504,29 +597,30 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   // sized once for the largest possible persistent grid (32 CTAs per SM)
   ctx.d_scratch.reserve(static_cast<size_t>(std::max(grid, 32 * ctx.n_sm)) * scratch);
   static const char* plan_prof_log = std::getenv("HPG_PLAN_PROFILE");  // diagnostics only
-  long long* d_prof = nullptr;
   if (plan_prof_log) {
-    cuda_check(cudaMalloc(&d_prof, sizeof(long long) * kPlanProfSlots * n), "profile alloc");
-    cuda_check(cudaMemsetAsync(d_prof, 0, sizeof(long long) * kPlanProfSlots * n, st), "profile clear");
-    cuda_check(eval_set_plan_profile(d_prof), "profile symbol");
+    cuda_check(cudaMalloc(&job.d_prof, sizeof(long long) * kPlanProfSlots * n), "profile alloc");
+    cuda_check(cudaMemsetAsync(job.d_prof, 0, sizeof(long long) * kPlanProfSlots * n, st),
+               "profile clear");
+    cuda_check(eval_set_plan_profile(job.d_prof), "profile symbol");
   }
-  cuda_check(cudaEventRecord(ctx.ev0, st), "event");
+  cuda_check(cudaEventRecord(buf.e0, st), "event");
   cuda_check(launch_eval(ctx.dprob, cfg, cv, kb_flags, d_rec, d_off, d_modes, 0, n, 0, d_ows,
                          d_ooff, d_res, want_per_task ? ctx.d_per_task.p : nullptr,
                          want_required ? ctx.d_required.p : nullptr, ctx.d_scratch.p, scratch,
                          grid, st),
              "eval_kernel launch");
-  cuda_check(cudaEventRecord(ctx.ev1, st), "event");
+  cuda_check(cudaEventRecord(buf.e1, st), "event");
   ++ctx.launches;
   ++ctx.eval_launches;
   ctx.plans_evaluated += n;
   ctx.h2d_bytes += in_bytes;
   ctx.d2h_bytes += out_bytes + (want_per_task ? 8 * static_cast<int64_t>(n) * P.T * 7 : 0) +
                    (want_required ? 8 * static_cast<int64_t>(n) * P.N : 0);
-  ctx.h_out.reserve(out_bytes);
-  cuda_check(cudaMemcpyAsync(ctx.h_out.p, ctx.d_out.p, out_bytes, cudaMemcpyDeviceToHost, st),
+  buf.h_out->reserve(out_bytes);
+  cuda_check(cudaMemcpyAsync(buf.h_out->p, buf.d_out->p, out_bytes, cudaMemcpyDeviceToHost, st),
              "D2H wave");
-  out.out_ws = want_out ? ctx.h_out.p + out_ws : nullptr;
+  out.out_ws = want_out ? buf.h_out->p + out_ws : nullptr;
+  out.ws_bytes = want_out ? ws_total : 0;
   if (want_per_task) out.per_task.resize(static_cast<size_t>(n) * P.T * 7);
   if (want_required) out.required.resize(static_cast<size_t>(n) * P.N);
   if (want_per_task)
@@ -535,11 +629,19 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   if (want_required)
     cuda_check(cudaMemcpyAsync(out.required.data(), ctx.d_required.p, 8 * out.required.size(),
                                cudaMemcpyDeviceToHost, st), "D2H required");
-  if (batch_log) bt2 = std::chrono::steady_clock::now();
-  cuda_check(cudaStreamSynchronize(st), "eval_kernel");
-  if (batch_log) bt3 = std::chrono::steady_clock::now();
+  if (batch_log) cuda_check(cudaEventRecord(buf.ed, st), "event");
+  cuda_check(cudaEventRecord(buf.done, st), "event");
+  job.t2 = std::chrono::steady_clock::now();
+}
+
+void wave_finish(Ctx& ctx, const Batch& b, WaveJob& job, BatchOut& out) {
+  const int n = job.n;
+  if (n == 0) return;
+  const Problem& P = ctx.prob;
+  cuda_check(cudaEventSynchronize(job.buf.done), "eval_kernel");
+  const auto t3 = std::chrono::steady_clock::now();
   float ms = 0.f;
-  cuda_check(cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1), "event time");
+  cuda_check(cudaEventElapsedTime(&ms, job.buf.e0, job.buf.e1), "event time");
   ctx.eval_ms += ms;
   static const char* wave_log = std::getenv("HPG_WAVE_LOG");  // diagnostics only
   if (wave_log) {
@@ -550,20 +652,23 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
       std::fclose(f);
     }
   }
-  if (d_prof) {
+  if (job.d_prof) {
+    static const char* plan_prof_log = std::getenv("HPG_PLAN_PROFILE");
     std::vector<long long> pr(static_cast<size_t>(kPlanProfSlots) * n);
-    cuda_check(cudaMemcpy(pr.data(), d_prof, sizeof(long long) * kPlanProfSlots * n, cudaMemcpyDeviceToHost),
+    cuda_check(cudaMemcpy(pr.data(), job.d_prof, sizeof(long long) * kPlanProfSlots * n,
+                          cudaMemcpyDeviceToHost),
                "profile D2H");
     cuda_check(eval_set_plan_profile(nullptr), "profile symbol");
-    cudaFree(d_prof);
+    cudaFree(job.d_prof);
+    job.d_prof = nullptr;
     static int wave_no = 0;
     if (FILE* f = std::fopen(plan_prof_log, "a")) {
       // wave n ms | per plan: mode stage bal_data bal_layers e2e | dp,pp,tp per task
       for (int i = 0; i < n; ++i) {
         const long long* q = &pr[kPlanProfSlots * static_cast<size_t>(i)];
-        const long long t1 = q[1] ? q[1] : q[0], t2 = q[2] ? q[2] : t1, t3 = q[3] ? q[3] : t2;
+        const long long t1 = q[1] ? q[1] : q[0], t2 = q[2] ? q[2] : t1, t3_ = q[3] ? q[3] : t2;
         std::fprintf(f, "%d %d %.4f %d %lld %lld %lld %lld", wave_no, n, ms, b.modes[i], t1 - q[0],
-                     t2 - t1, t3 - t2, q[4] - t3);
+                     t2 - t1, t3_ - t2, q[4] - t3_);
         const RecHeader& h = b.cands[i]->hdr();
         for (int t = 0; t < P.T; ++t) std::fprintf(f, " %d,%d,%d", h.dp[t], h.pp[t], h.tp[t]);
         std::fprintf(f, " |");
@@ -581,20 +686,87 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
     }
     ++wave_no;
   }
-  std::memcpy(out.res.data(), ctx.h_out.p + out_res, sizeof(EvalResult) * n);
+  std::memcpy(out.res.data(), job.buf.h_out->p, sizeof(EvalResult) * n);
+  static const char* batch_log = std::getenv("HPG_BATCH_LOG");  // diagnostics only
   if (batch_log) {
-    const auto bt4 = std::chrono::steady_clock::now();
-    auto us = [](auto a, auto b) {
-      return std::chrono::duration<double, std::micro>(b - a).count();
+    const auto t4 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b_) {
+      return std::chrono::duration<double, std::micro>(b_ - a).count();
     };
+    float h2d = 0.f, d2h = 0.f, gap = 0.f;
+    cudaEventElapsedTime(&h2d, job.buf.eh, job.buf.ex);
+    cudaEventElapsedTime(&gap, job.buf.ex, job.buf.e0);
+    cudaEventElapsedTime(&d2h, job.buf.e1, job.buf.ed);
     if (FILE* f = std::fopen(batch_log, "a")) {
-      // n in_bytes out_bytes pack_us enqueue_us sync_us post_us kernel_ms
-      std::fprintf(f, "%d %lld %lld %.1f %.1f %.1f %.1f %.4f\n", n,
-                   static_cast<long long>(in_bytes), static_cast<long long>(out_bytes),
-                   us(bt0, bt1), us(bt1, bt2), us(bt2, bt3), us(bt3, bt4), ms);
+      // n in_bytes out_bytes pack_us enqueue_us sync_us post_us kernel_ms h2d_ms d2h_ms
+      std::fprintf(f, "%d %lld %lld %.1f %.1f %.1f %.1f %.4f %.4f %.4f %.4f\n", n,
+                   static_cast<long long>(job.in_bytes), static_cast<long long>(job.out_bytes),
+                   us(job.t0, job.t1), us(job.t1, job.t2), us(job.t2, t3), us(t3, t4), ms, h2d,
+                   d2h, gap);
       std::fclose(f);
     }
   }
+}
+
+}  // namespace
+
+// Very large waves (the first SHA rounds of a 10^5-10^6 budget on 10^4 arms)
+// run as consecutive launches of at most kMaxWavePlans plans, double-buffered:
+// chunk k is packed and enqueued while the device works on chunk k-1, and
+// pinned staging stays bounded instead of growing to gigabytes.
+void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags, bool want_out,
+               bool want_per_task, bool want_required, BatchOut& out) {
+  constexpr int kMaxWavePlans = 32768;
+  const int n = static_cast<int>(b.cands.size());
+  if (n <= kMaxWavePlans || want_per_task || want_required) {
+    WaveJob job;
+    wave_stage(ctx, b, cfg, kb_flags, want_out, want_per_task, want_required, wave_bufs(ctx, 0),
+               out, job);
+    wave_finish(ctx, b, job, out);
+    return;
+  }
+  out.res.clear();
+  out.off.clear();
+  out.ws_off.clear();
+  out.per_task.clear();
+  out.required.clear();
+  out.ws_store.clear();
+  Batch sub[2];
+  BatchOut part[2];
+  WaveJob job[2];
+  auto collect = [&](int set) {
+    wave_finish(ctx, sub[set], job[set], part[set]);
+    const BatchOut& p = part[set];
+    out.res.insert(out.res.end(), p.res.begin(), p.res.end());
+    const int64_t base = static_cast<int64_t>(out.ws_store.size());
+    for (int64_t o : p.ws_off) out.ws_off.push_back(base + o);
+    for (int64_t o : p.off) out.off.push_back(o);
+    if (want_out) out.ws_store.insert(out.ws_store.end(), p.out_ws, p.out_ws + p.ws_bytes);
+  };
+  int k = 0;
+  for (int i0 = 0; i0 < n; i0 += kMaxWavePlans, ++k) {
+    const int i1 = std::min(n, i0 + kMaxWavePlans);
+    const int set = k & 1;
+    sub[set].cands.assign(b.cands.begin() + i0, b.cands.begin() + i1);
+    sub[set].modes.assign(b.modes.begin() + i0, b.modes.begin() + i1);
+    wave_stage(ctx, sub[set], cfg, kb_flags, want_out, false, false, wave_bufs(ctx, set),
+               part[set], job[set]);
+    if (k >= 1) collect(set ^ 1);
+  }
+  collect((k - 1) & 1);
+  out.out_ws = want_out ? out.ws_store.data() : nullptr;
+  out.ws_bytes = static_cast<int64_t>(out.ws_store.size());
+}
+
+void apply_ws(const Problem& P, Cand& c, const uint8_t* ws) {
+  const int g = P.slot_of_id[1];
+  int64_t at = 0;
+  if (g >= 0) {
+    const int64_t wg = 8 * static_cast<int64_t>(c.hdr().dp[g]);
+    std::memcpy(c.w() + c.o.w[g], ws, wg);
+    at = wg;
+  }
+  std::memcpy(c.sl(), ws + at, 4 * static_cast<size_t>(c.o.sl[P.T]));
 }
 
 std::vector<TablePlan> unpack_table(const Problem& P, const hpg_plan_table& t) {

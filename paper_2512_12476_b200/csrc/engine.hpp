@@ -152,10 +152,12 @@ void dist_destroy(Dist& d);
 
 struct BatchOut {
   std::vector<EvalResult> res;
-  // balanced [weights | stage layers] section of plan i (the record bytes
-  // [o.w_byte, o.dev_byte)) at out_ws + ws_off[i]; devices never change
+  // what balancing changed in plan i, at out_ws + ws_off[i]: [generation
+  // task weights | all stage layers] (apply_ws writes it into the record)
   const uint8_t* out_ws = nullptr;
+  int64_t ws_bytes = 0;
   std::vector<int64_t> off, ws_off;
+  std::vector<uint8_t> ws_store;  // chunked waves: the sections of every chunk
   std::vector<double> per_task;          // if requested
   std::vector<double> required;          // if requested
 };
@@ -170,11 +172,11 @@ struct Ctx {
   size_t blob_bytes = 0;
   HostBuf<uint8_t> h_blob;  // pinned staging of the problem tables
   // batch staging
-  HostBuf<uint8_t> h_recs, h_out;
+  HostBuf<uint8_t> h_recs, h_out, h_recs2, h_out2;  // wave staging, two sets
   HostBuf<int64_t> h_off;
   HostBuf<int32_t> h_modes;
   HostBuf<EvalResult> h_res;
-  DevBuf<uint8_t> d_recs, d_out;
+  DevBuf<uint8_t> d_recs, d_out, d_recs2, d_out2;
   DevBuf<int64_t> d_off;
   DevBuf<int32_t> d_modes;
   DevBuf<EvalResult> d_res;
@@ -206,7 +208,10 @@ struct Ctx {
   double eval_ms = 0.0;
   double host_ms = 0.0;   // GA coroutine time (candidate generation, bookkeeping)
   double batch_ms = 0.0;  // run_batch wall time (pack, copies, kernel, sync)
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // kernel timing, buffer set 0
+  cudaEvent_t ev2 = nullptr, ev3 = nullptr;  // kernel timing, buffer set 1
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};  // wave results landed, per set
+  cudaEvent_t ev_x[6] = {};  // diagnostics: copy timing
   ~Ctx();
 };
 
@@ -215,6 +220,9 @@ void stage_problem(Ctx& ctx, Problem&& P);
 void restage(Ctx& ctx, const hpg_problem& p);
 
 // Packs `b`, runs eval_kernel, returns per-plan results (and balanced records).
+// writes a wave's [generation weights | stage layers] section into the record
+void apply_ws(const Problem& P, Cand& c, const uint8_t* ws);
+
 void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
                bool want_out, bool want_per_task, bool want_required, BatchOut& out);
 

@@ -791,13 +791,15 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
         if (cur.feasible) r.flags |= kResFeasOut;
       }
     }
-    // ---- write back: the record's [weights | stage layers] bytes (devices
-    // and layouts never change) ----
+    // ---- write back what balancing can change: [generation task weights |
+    // all stage layers] (engine.cpp ws_bytes_of / apply_ws) ----
     if (out_ws && !(s.h.n_tasks & kRecCompact)) {
       uint8_t* ows = out_ws + out_off[p];
+      const int g = P.gen_slot;
+      const int dpg = g >= 0 ? s.h.dp[g] : 0;
       double* ow = reinterpret_cast<double*>(ows);
-      int32_t* osl = reinterpret_cast<int32_t*>(ows + (s.o.sl_byte - s.o.w_byte));
-      for (int i = lane; i < nw; i += 32) ow[i] = s.w[i];
+      int32_t* osl = reinterpret_cast<int32_t*>(ows + 8 * dpg);
+      for (int i = lane; i < dpg; i += 32) ow[i] = s.w[s.o.w[g] + i];
       for (int i = lane; i < nsl; i += 32) osl[i] = s.sl[i];
     }
     if (prof && lane == 0) prof[4] = clock64();

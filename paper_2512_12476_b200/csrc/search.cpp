@@ -797,8 +797,7 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
         const size_t kk = first[o] + i;
         q->res[i] = bo.res[kk];
         Cand& c = q->cands[i];
-        std::memcpy(c.rec.data() + c.o.w_byte, bo.out_ws + bo.ws_off[kk],
-                    c.o.dev_byte - c.o.w_byte);
+        apply_ws(ctx.prob, c, bo.out_ws + bo.ws_off[kk]);
       }
       r->coro.h.promise().pending = nullptr;
       r->coro.h.resume();
