@@ -259,6 +259,7 @@ Ctx::~Ctx() {
   if (dist.comm) dist_destroy(dist);
   if (d_blob) cudaFree(d_blob);
   if (d_sweep_tables) cudaFree(d_sweep_tables);
+  if (d_gen_tables) cudaFree(d_gen_tables);
   for (cudaEvent_t e : {ev0, ev1, ev2, ev3, ev_done[0], ev_done[1], ev_x[0], ev_x[1], ev_x[2], ev_x[3],
                         ev_x[4], ev_x[5]})
     if (e) cudaEventDestroy(e);
@@ -332,10 +333,14 @@ void restage(Ctx& ctx, const hpg_problem& hp) {
 void stage_problem(Ctx& ctxr, Problem&& P) {
   Ctx* ctx = &ctxr;
   {
-    // sweep tables belong to the previous problem
+    // sweep / generator tables belong to the previous problem
     if (ctx->d_sweep_tables) {
       cudaFree(ctx->d_sweep_tables);
       ctx->d_sweep_tables = nullptr;
+    }
+    if (ctx->d_gen_tables) {
+      cudaFree(ctx->d_gen_tables);
+      ctx->d_gen_tables = nullptr;
     }
     ctx->prob = std::move(P);
     const Problem& Q = ctx->prob;
@@ -499,10 +504,27 @@ void wave_stage(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags
     cv.max_dpk = std::max(cv.max_dpk, c.o.dpk[T]);
   }
   job.ws_total = ws_total;
-  // one input transfer: [offsets i64 | out offsets i64 | modes i32 (8-aligned) | records]
+  // device-generated candidates: compact offsets of their device slots
+  const int n_items = static_cast<int>(b.gen.size());
+  const int64_t n_gen = b.n_gen;
+  out.gen_dev_off.assign(n_gen, 0);
+  int64_t dev_total = 0;
+  for (const GenItem& it : b.gen)
+    for (int c = 0; c < it.count; ++c) {
+      out.gen_dev_off[it.first_out + c] = dev_total;
+      dev_total += b.cands[it.first + c]->o.dev[P.T];
+    }
+  // one input transfer: [offsets i64 | out offsets i64 | modes i32 (8-aligned) |
+  // generator: items | item per candidate i32 | start states | slot offsets i64 |
+  // records]
   const int64_t nn = static_cast<int64_t>(n);
+  auto al8 = [](int64_t x) { return (x + 7) & ~int64_t(7); };
   const int64_t in_off = 0, in_ooff = 8 * nn, in_modes = 16 * nn,
-                in_recs = in_modes + ((4 * nn + 7) & ~int64_t(7));
+                in_items = in_modes + al8(4 * nn),
+                in_citem = in_items + al8(static_cast<int64_t>(sizeof(GenItem)) * n_items),
+                in_starts = in_citem + al8(4 * n_gen),
+                in_goff = in_starts + static_cast<int64_t>(sizeof(Rng)) * n_gen,
+                in_recs = in_goff + 8 * n_gen;
   const int64_t in_bytes = in_recs + total;
   job.in_bytes = in_bytes;
   buf.h_in->reserve(in_bytes);
@@ -510,6 +532,12 @@ void wave_stage(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags
   int64_t* h_ooff = reinterpret_cast<int64_t*>(buf.h_in->p + in_ooff);
   int32_t* h_modes = reinterpret_cast<int32_t*>(buf.h_in->p + in_modes);
   uint8_t* h_rec = buf.h_in->p + in_recs;
+  if (n_items) {
+    std::memcpy(buf.h_in->p + in_items, b.gen.data(), sizeof(GenItem) * n_items);
+    std::memcpy(buf.h_in->p + in_citem, b.gen_item.data(), 4 * n_gen);
+    std::memcpy(buf.h_in->p + in_starts, b.gen_starts.data(), sizeof(Rng) * n_gen);
+    std::memcpy(buf.h_in->p + in_goff, out.gen_dev_off.data(), 8 * n_gen);
+  }
   // canonical bytes: tg id + k counts + per task
   // (3 + pp + slots) + 9 result bytes (+ 8*dp for a weighted generation task)
   auto canonical = [&](const Cand& c) {
@@ -544,9 +572,11 @@ void wave_stage(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags
     cb_part[ch] = cb;
   });
   for (int ch = 0; ch < n_chunks; ++ch) ctx.canonical_bytes += cb_part[ch];
-  // one output transfer: [results 32 B each | balanced weight / split sections]
+  // one output transfer: [results 32 B each | balanced weight / split sections |
+  // generated device slots]
   const int64_t out_res = 0, out_ws = 32 * nn;
-  const int64_t out_bytes = out_ws + (want_out ? ws_total : 0);
+  const int64_t out_gdev = out_ws + (want_out ? ws_total : 0);
+  const int64_t out_bytes = out_gdev + ((dev_total + 7) & ~int64_t(7));
   job.out_bytes = out_bytes;
   buf.d_in->reserve(in_bytes);
   buf.d_out->reserve(out_bytes);
@@ -565,6 +595,16 @@ void wave_stage(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags
   const uint8_t* d_rec = buf.d_in->p + in_recs;
   EvalResult* d_res = reinterpret_cast<EvalResult*>(buf.d_out->p + out_res);
   uint8_t* d_ows = want_out ? buf.d_out->p + out_ws : nullptr;
+  if (n_items) {
+    cuda_check(launch_gen_ga(gen_tables(ctx), reinterpret_cast<const GenItem*>(buf.d_in->p + in_items),
+                             reinterpret_cast<const int32_t*>(buf.d_in->p + in_citem),
+                             reinterpret_cast<const Rng*>(buf.d_in->p + in_starts),
+                             static_cast<int>(n_gen), buf.d_in->p + in_recs, d_off,
+                             reinterpret_cast<const int64_t*>(buf.d_in->p + in_goff),
+                             buf.d_out->p + out_gdev, st),
+               "gen_ga_kernel");
+    ++ctx.launches;
+  }
   // small waves are latency-bound on cold SMs: stage the class matrix in smem
   cv.cls_smem = (n <= 2 * ctx.n_sm && P.N * P.N <= kClsSmemMax) ? 1 : 0;
   // ... and get helper warps for the per-task costs of each plan
@@ -621,6 +661,7 @@ void wave_stage(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags
              "D2H wave");
   out.out_ws = want_out ? buf.h_out->p + out_ws : nullptr;
   out.ws_bytes = want_out ? ws_total : 0;
+  out.gen_devs = n_gen ? buf.h_out->p + out_gdev : nullptr;
   if (want_per_task) out.per_task.resize(static_cast<size_t>(n) * P.T * 7);
   if (want_required) out.required.resize(static_cast<size_t>(n) * P.N);
   if (want_per_task)
@@ -756,6 +797,63 @@ void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
   collect((k - 1) & 1);
   out.out_ws = want_out ? out.ws_store.data() : nullptr;
   out.ws_bytes = static_cast<int64_t>(out.ws_store.size());
+}
+
+const GenTablesDev& gen_tables(Ctx& ctx) {
+  if (ctx.d_gen_tables) return ctx.gen_tb;
+  const Problem& P = ctx.prob;
+  std::vector<int32_t> region_off{0}, node_off{0};
+  std::vector<uint8_t> node_devs;
+  for (const auto& nodes : P.region_nodes) {
+    for (const auto& devs : nodes) {
+      for (int d : devs) node_devs.push_back(static_cast<uint8_t>(d));
+      node_off.push_back(static_cast<int32_t>(node_devs.size()));
+    }
+    region_off.push_back(static_cast<int32_t>(node_off.size() - 1));
+  }
+  std::vector<int16_t> node_rank(P.N);
+  for (int i = 0; i < P.N; ++i) node_rank[i] = static_cast<int16_t>(P.node_rank[i]);
+  std::vector<uint64_t> fm(2 * (kGenFastModMax + 1), 0);
+  for (int d = 1; d <= kGenFastModMax; ++d) {
+    const unsigned __int128 m = ~static_cast<unsigned __int128>(0) / d + 1;
+    fm[2 * d] = static_cast<uint64_t>(m);
+    fm[2 * d + 1] = static_cast<uint64_t>(m >> 64);
+  }
+  auto round16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+  const size_t b_fm = round16(8 * fm.size()), b_ro = round16(4 * region_off.size()),
+               b_no = round16(4 * node_off.size()), b_nr = round16(2 * node_rank.size()),
+               b_nd = round16(node_devs.size() + 1);
+  std::vector<uint8_t> blob(b_fm + b_ro + b_no + b_nr + b_nd, 0);
+  size_t at = 0;
+  std::memcpy(blob.data() + at, fm.data(), 8 * fm.size());
+  const size_t o_ro = (at += b_fm);
+  std::memcpy(blob.data() + at, region_off.data(), 4 * region_off.size());
+  const size_t o_no = (at += b_ro);
+  std::memcpy(blob.data() + at, node_off.data(), 4 * node_off.size());
+  const size_t o_nr = (at += b_no);
+  std::memcpy(blob.data() + at, node_rank.data(), 2 * node_rank.size());
+  const size_t o_nd = (at += b_nr);
+  std::memcpy(blob.data() + at, node_devs.data(), node_devs.size());
+  cuda_check(cudaMalloc(&ctx.d_gen_tables, blob.size()), "cudaMalloc generator tables");
+  cuda_check(cudaMemcpy(ctx.d_gen_tables, blob.data(), blob.size(), cudaMemcpyHostToDevice),
+             "H2D generator tables");
+  const uint8_t* b = static_cast<const uint8_t*>(ctx.d_gen_tables);
+  GenTablesDev& t = ctx.gen_tb;
+  t.n_dev = P.N;
+  t.n_regions = static_cast<int32_t>(P.region_nodes.size());
+  t.n_nodes = P.n_nodes;
+  t.max_nodes_per_region = 0;
+  for (const auto& rn : P.region_nodes)
+    t.max_nodes_per_region = std::max(t.max_nodes_per_region, static_cast<int32_t>(rn.size()));
+  // int16 regions / nodes / 4 x node-rank arrays, then u8 flat + bucket
+  t.smem_per_thread = static_cast<int32_t>(
+      (2 * (t.n_regions + t.max_nodes_per_region + 4 * t.n_nodes) + 2 * P.N + 15) & ~15);
+  t.fastmod = reinterpret_cast<const uint64_t*>(b);
+  t.region_off = reinterpret_cast<const int32_t*>(b + o_ro);
+  t.node_off = reinterpret_cast<const int32_t*>(b + o_no);
+  t.node_rank = reinterpret_cast<const int16_t*>(b + o_nr);
+  t.node_devs = b + o_nd;
+  return t;
 }
 
 void apply_ws(const Problem& P, Cand& c, const uint8_t* ws) {

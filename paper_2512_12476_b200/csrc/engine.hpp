@@ -13,6 +13,7 @@
 
 #include "../../include/hpg.h"
 #include "common.hpp"
+#include "gen_ga.hpp"
 #include "rng.hpp"
 #include "sweep.hpp"
 
@@ -140,6 +141,12 @@ struct HostBuf {  // pinned
 struct Batch {
   std::vector<const Cand*> cands;
   std::vector<int32_t> modes;
+  // candidates whose devices the device generates (gen_ga.cu) before the
+  // evaluation; GenItem.first / first_out index cands / the compact outputs
+  std::vector<GenItem> gen;
+  int n_gen = 0;                   // candidates covered by gen
+  std::vector<int32_t> gen_item;   // [n_gen] item of each generated candidate
+  std::vector<Rng> gen_starts;     // [n_gen] its stream state
 };
 
 // Multi-GPU: NCCL communicator of a context (created once, reused by every
@@ -158,6 +165,10 @@ struct BatchOut {
   int64_t ws_bytes = 0;
   std::vector<int64_t> off, ws_off;
   std::vector<uint8_t> ws_store;  // chunked waves: the sections of every chunk
+  // device-generated candidates (Batch::gen), by compact index j: their
+  // device slots at gen_devs + gen_dev_off[j]
+  const uint8_t* gen_devs = nullptr;
+  std::vector<int64_t> gen_dev_off;
   std::vector<double> per_task;          // if requested
   std::vector<double> required;          // if requested
 };
@@ -194,6 +205,8 @@ struct Ctx {
   // sweep
   void* d_sweep_tables = nullptr;  // owns sweep_tb's arrays
   SweepTablesDev sweep_tb{};
+  void* d_gen_tables = nullptr;  // owns gen_tb's arrays (GA candidates on the device)
+  GenTablesDev gen_tb{};
   DevBuf<double> d_costs;
   DevBuf<uint8_t> d_feas;
   DevBuf<unsigned long long> d_best;
@@ -222,6 +235,8 @@ void restage(Ctx& ctx, const hpg_problem& p);
 // Packs `b`, runs eval_kernel, returns per-plan results (and balanced records).
 // writes a wave's [generation weights | stage layers] section into the record
 void apply_ws(const Problem& P, Cand& c, const uint8_t* ws);
+// problem tables of the device candidate generator (built on first use)
+const GenTablesDev& gen_tables(Ctx& ctx);
 
 void run_batch(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags,
                bool want_out, bool want_per_task, bool want_required, BatchOut& out);

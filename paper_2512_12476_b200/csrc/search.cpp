@@ -290,10 +290,11 @@ struct ArmEnv {
   const Grouping& tg;
   const std::vector<int>& counts;
   ArmLayouts al;
-  std::vector<int> group_of;  // slot -> group
 };
 
-void make_candidate(const ArmEnv& e, int64_t combo, Rng& rng, Cand& c) {
+// make_candidate's layout part (decode_layout_combo, search.cpp:283-316): the
+// record with its layouts, unit weights and uniform splits, devices unset
+void candidate_layouts(const ArmEnv& e, int64_t combo, Cand& c) {
   const Problem& P = e.P;
   int dp[kMaxTasks], pp[kMaxTasks], tp[kMaxTasks];
   for (int s : e.al.task_order) {
@@ -306,6 +307,11 @@ void make_candidate(const ArmEnv& e, int64_t combo, Rng& rng, Cand& c) {
   }
   init_cand(c, P.T, dp, pp, tp, P);
   c.ng = static_cast<int>(e.tg.size());
+}
+
+void make_candidate(const ArmEnv& e, int64_t combo, Rng& rng, Cand& c) {
+  const Problem& P = e.P;
+  candidate_layouts(e, combo, c);
   std::vector<int> flat;
   flat.reserve(P.N);
   medium_assignment(P, e.K.locality_bias, rng, flat);
@@ -417,7 +423,36 @@ bool mutate(const ArmEnv& e, Cand& c, Rng& rng) {
 struct EvalReq {
   std::vector<Cand> cands;
   std::vector<EvalResult> res;
+  // init chunk: `gen_count` new candidates (combinations gen_combo0...) drawn
+  // from gen_rng, generated by the scheduler (host or device); gen_snaps[c] =
+  // the stream state after candidate c
+  bool gen = false;
+  const ArmEnv* env = nullptr;
+  Rng gen_rng;
+  int64_t gen_combo0 = 0;
+  int gen_count = 0;
+  std::vector<Rng> gen_snaps;
+  std::vector<Rng> gen_starts;  // device generation: each candidate's start state
 };
+
+// the generator's view of an arm: groups, counts and the fine-assignment
+// order of make_candidate (task slots group by group)
+GenItem gen_item_of(const ArmEnv& e) {
+  GenItem it{};
+  it.bias = e.K.locality_bias;
+  it.n_groups = static_cast<int32_t>(e.tg.size());
+  int no = 0;
+  for (size_t g = 0; g < e.tg.size(); ++g) {
+    it.counts[g] = e.counts[g];
+    for (int s : e.tg[g]) {
+      it.order_slot[no] = static_cast<int8_t>(s);
+      it.order_group[no] = static_cast<int8_t>(g);
+      ++no;
+    }
+  }
+  it.n_order = no;
+  return it;
+}
 
 struct ArmCoro {
   struct promise_type {
@@ -529,24 +564,28 @@ ArmCoro ga_run(ArmRun& run) {
          attempts < attempt_cap) {
     const int64_t need = init_target - static_cast<int64_t>(pop.size());
     chunk = std::min(attempt_cap - attempts, std::max(chunk * 2, 2 * need + 2));
-    req.cands.assign(chunk, Cand{});
-    snaps.clear();
-    const int64_t combo0 = combo;
-    const double tm0 = now_s();
-    for (int64_t c = 0; c < chunk; ++c) {
-      make_candidate(e, combo++, rng, req.cands[c]);
-      snaps.push_back(rng);
-    }
-    run.t_make += now_s() - tm0;
+    // the scheduler makes the chunk (make_candidate x chunk from this stream
+    // position, on the device when the wave is wide) and returns the stream
+    // state after each candidate
+    req.cands.clear();
+    req.gen = true;
+    req.env = &e;
+    req.gen_rng = rng;
+    req.gen_combo0 = combo;
+    req.gen_count = static_cast<int>(chunk);
     run.n_make += chunk;
     co_await EvalAwait{&req};
+    req.gen = false;
+    const int64_t combo0 = combo;
+    combo += chunk;
+    rng = req.gen_snaps.back();
     for (int64_t c = 0; c < chunk; ++c) {
       ++attempts;
       if (!(req.res[c].flags & kResFeasIn)) continue;
       score(req.cands[c], req.res[c].cost);
       insert_member(req.cands[c], req.res[c].cost);
       if (static_cast<int64_t>(pop.size()) >= init_target) {
-        rng = snaps[c];
+        rng = req.gen_snaps[c];
         combo = combo0 + c + 1;
         break;
       }
@@ -761,14 +800,89 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
   BatchOut bo;
   std::vector<std::pair<ArmRun*, int>> owners;
   std::vector<size_t> first;
+  // init chunks are made on the device (one thread per candidate) when a
+  // wave carries very many of them; below that the host pool is as fast
+  // (measured: a generator launch costs ~0.3 ms, host make_candidate ~4.5 us
+  // per candidate on 16 threads)
+  static const int dev_gen_min = [] {
+    const char* v = std::getenv("HPG_DEVICE_GEN_MIN");  // diagnostics: 0 = always
+    return v ? std::atoi(v) : 256;
+  }();
+  std::vector<EvalReq*> gens;
+  std::vector<int> gen_first_out;
+  std::vector<int> nodes_per_region;
+  for (const auto& rn : ctx.prob.region_nodes) nodes_per_region.push_back(static_cast<int>(rn.size()));
   while (true) {
     b.cands.clear();
     b.modes.clear();
+    b.gen.clear();
+    b.gen_item.clear();
+    b.gen_starts.clear();
+    b.n_gen = 0;
     owners.clear();
+    gens.clear();
+    int64_t wave = 0;
     for (ArmRun* r : runs) {
       if (r->coro.h.done()) continue;
       EvalReq* q = r->coro.h.promise().pending;
       if (!q) continue;
+      if (q->gen) gens.push_back(q);
+      wave += q->gen ? q->gen_count : static_cast<int64_t>(q->cands.size());
+    }
+    const bool device_gen = !gens.empty() && static_cast<int>(gens.size()) >= dev_gen_min &&
+                            wave <= 32768;
+    if (!gens.empty()) {
+      const double tg = now_s();
+      // host: make_candidate x count (stream states recorded); device: the
+      // layouts only, the device assignment follows on the GPU
+      host_parallel_for(static_cast<int>(gens.size()), gens.size() >= 16, [&](int i) {
+        EvalReq* q = gens[i];
+        q->cands.resize(q->gen_count);
+        q->gen_snaps.resize(q->gen_count);
+        if (device_gen) {
+          // layouts here; the stream stepped to every candidate's start (each
+          // draws the same count), the assignments on the device
+          GenItem it = gen_item_of(*q->env);
+          const int64_t draws = gen_draws_per_candidate(ctx.prob.N, nodes_per_region.data(),
+                                                        static_cast<int>(nodes_per_region.size()), it);
+          q->gen_starts.resize(q->gen_count);
+          Rng rng = q->gen_rng;
+          for (int c = 0; c < q->gen_count; ++c) {
+            candidate_layouts(*q->env, q->gen_combo0 + c, q->cands[c]);
+            q->gen_starts[c] = rng;
+            for (int64_t d = 0; d < draws; ++d) rng.next();
+            q->gen_snaps[c] = rng;
+          }
+        } else {
+          Rng rng = q->gen_rng;
+          for (int c = 0; c < q->gen_count; ++c) {
+            make_candidate(*q->env, q->gen_combo0 + c, rng, q->cands[c]);
+            q->gen_snaps[c] = rng;
+          }
+        }
+      });
+      ctx.host_ms += 1e3 * (now_s() - tg);
+    }
+    gen_first_out.clear();
+    for (ArmRun* r : runs) {
+      if (r->coro.h.done()) continue;
+      EvalReq* q = r->coro.h.promise().pending;
+      if (!q) continue;
+      if (q->gen && device_gen) {
+        GenItem it = gen_item_of(*q->env);
+        it.first = static_cast<int32_t>(b.cands.size());
+        it.first_out = b.n_gen;
+        it.count = q->gen_count;
+        gen_first_out.push_back(b.n_gen);
+        for (int c = 0; c < q->gen_count; ++c) {
+          b.gen_item.push_back(static_cast<int32_t>(b.gen.size()));
+          b.gen_starts.push_back(q->gen_starts[c]);
+        }
+        b.gen.push_back(it);
+        b.n_gen += q->gen_count;
+      } else {
+        gen_first_out.push_back(-1);
+      }
       for (size_t i = 0; i < q->cands.size(); ++i) {
         b.cands.push_back(&q->cands[i]);
         b.modes.push_back(kModeEvaluate);
@@ -793,10 +907,13 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
       const int cnt = owners[o].second;
       EvalReq* q = r->coro.h.promise().pending;
       q->res.resize(cnt);
+      const int gj = gen_first_out[o];
       for (int i = 0; i < cnt; ++i) {
         const size_t kk = first[o] + i;
         q->res[i] = bo.res[kk];
         Cand& c = q->cands[i];
+        if (gj >= 0)  // device-generated: its device slots
+          std::memcpy(c.dev(), bo.gen_devs + bo.gen_dev_off[gj + i], c.o.dev[ctx.prob.T]);
         apply_ws(ctx.prob, c, bo.out_ws + bo.ws_off[kk]);
       }
       r->coro.h.promise().pending = nullptr;
@@ -1100,7 +1217,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
                                 (static_cast<uint64_t>(m) << 8) | static_cast<uint64_t>(n);
           r->rng = base_rng.fork(salt);
           TgArm& arm = arms[p.ti];
-          r->env.reset(new ArmEnv{P, K, arm.tg, arm.ggs[gi], build_arm_layouts(P, arm.tg, arm.ggs[gi]), {}});
+          r->env.reset(new ArmEnv{P, K, arm.tg, arm.ggs[gi], build_arm_layouts(P, arm.tg, arm.ggs[gi])});
           batch.push_back(r.get());
           list.push_back(std::move(r));
         };
@@ -1284,7 +1401,7 @@ SearchOut ga_search(Ctx& ctx, const Grouping& tg, const std::vector<int>& counts
   ArmRun r;
   r.slice = slice;
   r.rng = Rng(seed);
-  r.env.reset(new ArmEnv{P, K, tg, counts, build_arm_layouts(P, tg, counts), {}});
+  r.env.reset(new ArmEnv{P, K, tg, counts, build_arm_layouts(P, tg, counts)});
   std::vector<ArmRun*> runs{&r};
   double clock = t0;
   int64_t waves = 0;
