@@ -182,7 +182,7 @@ HPG_HD int carve_bytes(const Carve& c) {
   b += 2 * carve_round(8 * c.max_w) + 2 * carve_round(8 * c.max_cells) + carve_round(8 * c.max_dpk);
   b += 7 * carve_round(8 * N) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
        carve_round(8 * T * 7);
-  b += 2 * carve_round(4 * c.max_sl) + carve_round(4 * c.max_dpk) + 2 * carve_round(4 * N);
+  b += 2 * carve_round(4 * c.max_sl) + carve_round(4 * c.max_dpk) + carve_round(4 * N);
   b += carve_round(c.max_slots) + carve_round(T * N) + 2 * carve_round(N);
   return b;
 }
@@ -203,7 +203,7 @@ HPG_HD int team_scratch_bytes(const Carve& c) {
 
 HPG_HD int carve2_bytes(const Carve& c) {
   return carve_bytes(c) + carve_round(8 * c.max_cells) + 2 * carve_round(8 * c.max_sl) +
-         carve_round(8 * c.n_dev) + carve_round(4 * c.max_sl) + carve_round(4 * c.n_dev) +
+         carve_round(8 * c.n_dev) + carve_round(4 * c.max_sl) +
          (c.cls_smem ? carve_round(c.n_dev * c.n_dev) : 0) +
          (c.n_warps > 1 ? (c.n_warps - 1) * team_scratch_bytes(c) : 0);
 }

@@ -67,14 +67,12 @@ struct Ws {
   double* agg;       // [T*7]
   int32_t* sl_save;  // [sum pp]
   int32_t* split_best;   // [N]
-  int32_t* split_trial;  // [N]
   uint8_t* tour;     // [N]
   uint8_t* peers;    // [N]
   double* mmt;       // [sum pp] model_memory_bytes per (task, stage) at the current split
   double* wmt;       // [sum pp] working_memory_bytes per (task, stage)
   double* wsave;     // [N]
   int32_t* sl_save2;   // [sum pp]
-  int32_t* split_step; // [N]
   double* dtab;      // global scratch: DP ring maxima per (stage, layer count), -1 = unknown
   int32_t* cflag;    // global scratch after dtab: balance_layers column verdicts
   double* ccell;     // global scratch: balance_layers column cell pieces
@@ -168,7 +166,6 @@ __device__ inline uint8_t* carve(Ws& s, uint8_t* base, const Carve& c) {
   s.sl_save = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
   s.dpr_sl = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_dpk));
   s.split_best = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
-  s.split_trial = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
   s.dev = carve_ptr(p, c.max_slots);
   s.dstage = carve_ptr(p, T * N);
   s.tour = carve_ptr(p, N);
@@ -178,7 +175,6 @@ __device__ inline uint8_t* carve(Ws& s, uint8_t* base, const Carve& c) {
   s.wmt = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_sl));
   s.wsave = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
   s.sl_save2 = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
-  s.split_step = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
   s.cls = c.cls_smem ? carve_ptr(p, N * N) : nullptr;  // else P.cls (stage_link_classes)
   return p;
 }
