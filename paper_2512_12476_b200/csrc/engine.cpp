@@ -632,7 +632,13 @@ void wave_stage(Ctx& ctx, const Batch& b, const DevCostConfig& cfg, int kb_flags
     }
   }
   int grid = 0;
-  cuda_check(eval_grid(cv, n, ctx.n_sm, grid), "eval_kernel occupancy");
+  {
+    const cudaError_t e = eval_grid(cv, n, ctx.n_sm, grid);
+    if (e != cudaSuccess)
+      throw InternalError(std::string("eval_kernel occupancy (") + std::to_string(carve2_bytes(cv)) +
+                          " B smem, " + std::to_string(cv.n_warps) + " warps, " +
+                          std::to_string(n) + " plans): " + cudaGetErrorString(e));
+  }
   const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);
   // sized once for the largest possible persistent grid (32 CTAs per SM)
   ctx.d_scratch.reserve(static_cast<size_t>(std::max(grid, 32 * ctx.n_sm)) * scratch);

@@ -831,8 +831,10 @@ namespace {
 template <int kTeam>
 cudaError_t grid_for(Carve cv, int n, int n_sm, int& grid) {
   auto kern = dev::eval_kernel<kTeam>;
+  // opt in to the dynamic size (static + dynamic may not exceed 48 KB without
+  // it, and the kernel's own static shared memory counts)
   static int configured_bytes = 0;
-  if (cv.bytes > 48 * 1024 && cv.bytes > configured_bytes) {
+  if (cv.bytes > configured_bytes) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
     if (e != cudaSuccess) return e;

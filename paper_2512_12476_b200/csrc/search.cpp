@@ -514,6 +514,7 @@ struct ArmRun {
   int owner = 0;  // rank that runs it (multi-GPU)
   int64_t n_offspring = 0, n_spec_hit = 0;  // diagnostics
   double t_make = 0, t_mut = 0, t_swap = 0, t_spec = 0;  // diagnostics (s)
+  int64_t w_init = 0, w_mut = 0, w_swap = 0, w_redraw = 0;  // diagnostics: waves by kind
   int64_t n_make = 0;
 };
 
@@ -574,6 +575,7 @@ ArmCoro ga_run(ArmRun& run) {
     req.gen_combo0 = combo;
     req.gen_count = static_cast<int>(chunk);
     run.n_make += chunk;
+    ++run.w_init;  // diagnostics
     co_await EvalAwait{&req};
     req.gen = false;
     const int64_t combo0 = combo;
@@ -660,6 +662,7 @@ ArmCoro ga_run(ArmRun& run) {
       const double tu0 = now_s();
       draw_mut(r, pop[i].plan, cur, req.cands);
       run.t_mut += now_s() - tu0;
+      ++run.w_mut;  // diagnostics
       co_await EvalAwait{&req};
       cur.res = req.res;
       cur.cands = std::move(req.cands);
@@ -750,6 +753,7 @@ ArmCoro ga_run(ArmRun& run) {
         const double tp0 = now_s();
         speculate(n5 > 0 ? snaps5.back() : before5, child, cost);
         run.t_spec += now_s() - tp0;
+        ++run.w_swap;  // diagnostics
         co_await EvalAwait{&req};
         rng = before5;  // stream position after the level-3 draws (walk may rewind it)
         const int w3 = walk(0, n3, before3, snaps);
@@ -764,6 +768,7 @@ ArmCoro ga_run(ArmRun& run) {
           if (m5 > 0) {
             const int base5 = static_cast<int>(req.cands.size());
             speculate(snaps5.back(), child, cost);
+            ++run.w_redraw;  // diagnostics
             co_await EvalAwait{&req};
             take_spec(base5, walk(0, m5, b5, snaps5));
           }
@@ -926,7 +931,7 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
   static const char* spec_log = std::getenv("HPG_SPEC_LOG");  // diagnostics only
   if (spec_log) {
     if (FILE* f = std::fopen(spec_log, "a")) {
-      int64_t off = 0, hit = 0, used = 0, nm = 0;
+      int64_t off = 0, hit = 0, used = 0, nm = 0, mx = 0, wi = 0, wm = 0, ws = 0, wr = 0;
       double tm = 0, tu = 0, ts = 0, tp = 0;
       for (ArmRun* r : runs) {
         off += r->n_offspring;
@@ -937,13 +942,24 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
         tu += r->t_mut;
         ts += r->t_swap;
         tp += r->t_spec;
+        const int64_t w = r->w_init + r->w_mut + r->w_swap + r->w_redraw;
+        if (w > mx) {
+          mx = w;
+          wi = r->w_init;
+          wm = r->w_mut;
+          ws = r->w_swap;
+          wr = r->w_redraw;
+        }
       }
       std::fprintf(f,
                    "runs %zu used %lld offspring %lld spec_hits %lld waves_total %lld "
-                   "make %lld %.2fms mut %.2fms swap %.2fms spec %.2fms\n",
+                   "make %lld %.2fms mut %.2fms swap %.2fms spec %.2fms | longest run waves %lld "
+                   "(init %lld mut %lld swap %lld redraw %lld)\n",
                    runs.size(), static_cast<long long>(used), static_cast<long long>(off),
                    static_cast<long long>(hit), static_cast<long long>(waves),
-                   static_cast<long long>(nm), 1e3 * tm, 1e3 * tu, 1e3 * ts, 1e3 * tp);
+                   static_cast<long long>(nm), 1e3 * tm, 1e3 * tu, 1e3 * ts, 1e3 * tp,
+                   static_cast<long long>(mx), static_cast<long long>(wi), static_cast<long long>(wm),
+                   static_cast<long long>(ws), static_cast<long long>(wr));
       std::fclose(f);
     }
   }

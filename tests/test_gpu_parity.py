@@ -215,3 +215,18 @@ def test_exhaustive_identical():
             if res.plan["provenance"]["budget"] != r["plan"]["provenance"]["budget"]:
                 bad.append(f"{r['name']}: provenance budget")
     assert not bad, "\n".join(bad[:30])
+
+
+def test_mixed_problem_sizes_in_one_process():
+    """contexts with different shared-memory footprints in one process (the
+    dynamic-smem opt-in must count the kernel's static shared memory: c3 then
+    c4 once failed with an invalid launch configuration)"""
+    import os
+    from paper_2512_12476_b200 import Engine, SearchKnobs, load_topology, load_workflow
+    from golden_util import FIXTURES
+    for cfg in ("c3", "c4", "c1", "c4"):
+        wf = load_workflow(os.path.join(FIXTURES, f"{cfg}.workflow.json"))
+        topo = load_topology(os.path.join(FIXTURES, f"{cfg}.topology.json"))
+        with Engine(wf, topo) as eng:
+            res = eng.nested_sha_search(SearchKnobs(budget=2000, seed=42))
+            assert res.consumed > 0 and res.plan is not None
