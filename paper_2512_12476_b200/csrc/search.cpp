@@ -805,13 +805,14 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
   BatchOut bo;
   std::vector<std::pair<ArmRun*, int>> owners;
   std::vector<size_t> first;
-  // init chunks are made on the device (one thread per candidate) when a
-  // wave carries very many of them; below that the host pool is as fast
-  // (measured: a generator launch costs ~0.3 ms, host make_candidate ~4.5 us
-  // per candidate on 16 threads)
+  // init chunks can be made on the device (one thread per candidate, the
+  // stream stepped to each start on the host). Measured on c3/c4 at B = 1e4
+  // it costs more wave latency (the generator runs ahead of the evaluation,
+  // ~0.5 ms per wave) than it saves host time, so the host pool makes them
+  // unless HPG_DEVICE_GEN_MIN sets a threshold (runs per wave; 0 = always).
   static const int dev_gen_min = [] {
-    const char* v = std::getenv("HPG_DEVICE_GEN_MIN");  // diagnostics: 0 = always
-    return v ? std::atoi(v) : 256;
+    const char* v = std::getenv("HPG_DEVICE_GEN_MIN");
+    return v ? std::atoi(v) : (1 << 30);
   }();
   std::vector<EvalReq*> gens;
   std::vector<int> gen_first_out;

@@ -230,3 +230,19 @@ def test_mixed_problem_sizes_in_one_process():
         with Engine(wf, topo) as eng:
             res = eng.nested_sha_search(SearchKnobs(budget=2000, seed=42))
             assert res.consumed > 0 and res.plan is not None
+
+
+def test_device_generated_init_candidates_identical():
+    """GA init candidates made on the device (HPG_DEVICE_GEN_MIN=0: every
+    init chunk) give the same searches as the reference: c1/c2 goldens and the
+    60 search fuzz cases, in a subprocess (the switch is read once)"""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "search_configs or search_fuzz"],
+                       env=dict(os.environ, HPG_DEVICE_GEN_MIN="0"), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
