@@ -21,11 +21,13 @@ class HostPool {
   }
 
   // Runs fn(i) for i in [0, n); the caller participates. Blocks until done.
+  // Callers from different threads (separate engine contexts) take turns.
   void run(int n, const std::function<void(int)>& fn) {
     if (workers_.empty() || n <= 1) {
       for (int i = 0; i < n; ++i) fn(i);
       return;
     }
+    std::lock_guard<std::mutex> call_lock(call_m_);
     {
       std::lock_guard<std::mutex> lk(m_);
       fn_ = &fn;
@@ -80,7 +82,7 @@ class HostPool {
   }
 
   std::vector<std::thread> workers_;
-  std::mutex m_;
+  std::mutex m_, call_m_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* fn_ = nullptr;
   int n_ = 0;
