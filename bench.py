@@ -281,7 +281,11 @@ def run_engine(args, world, rank, local_rank):
                      "avg_launch_ms": eval_ms / eval_launches,
                      "kernel_share_of_step": eval_ms / total_ms,
                      "note": "latency/issue-bound scalar FP64 gather work; HBM is not the "
-                             "binding resource (SURVEY.md §8 D1)"},
+                             "binding resource (SURVEY.md §8 D1)",
+                     "traffic_note": "ncu --set full replays each launch with flushed caches: "
+                                     "its DRAM bytes are dominated by fetching the kernel's "
+                                     "~0.5 MB of SASS and the problem tables, which stay in "
+                                     "the 126 MB L2 across the waves of a search"},
         "gpu_launches": sum(i["gpu_launches"] for i in infos),
         "waves_per_step": infos[-1]["waves"],
         "plans_scored_on_gpu_per_step": infos[-1]["plans_evaluated_gpu"],
