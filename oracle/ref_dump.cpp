@@ -1150,6 +1150,93 @@ int cmd_cli(const std::string& out_path) {
     record("plan_missing_topology", {"plan", "--workflow", a.workflow_path, "--seed", "1"}, rc,
            o.str(), e.str(), {});
   }
+  // ---- error paths: defective plan / topology / workflow files through
+  // cmd_estimate (resolve_plan, DeviceTopology::make, build_workflow
+  // validation; JSON schema errors) ----
+  const json good_plan = json::parse(file_text(tmp + "/p1.json"));
+  const json good_topo = json::parse(read_file(fx("c1", "topology")));
+  const json good_wf = json::parse(read_file(fx("c1", "workflow")));
+  auto err_case = [&](const std::string& name, const json& plan, const json& topo,
+                      const json& wf) {
+    const std::string pf = name + ".plan.json", tf = name + ".topo.json",
+                      wff = name + ".wf.json";
+    write_file(tmp + "/" + pf, plan.dump(2) + "\n");
+    write_file(tmp + "/" + tf, topo.dump(2) + "\n");
+    write_file(tmp + "/" + wff, wf.dump(2) + "\n");
+    EstimateArgs a;
+    a.plan_path = tmp + "/" + pf;
+    a.workflow_path = tmp + "/" + wff;
+    a.topology_path = tmp + "/" + tf;
+    std::ostringstream o, e;
+    const int rc = cmd_estimate(a, o, e);
+    const std::vector<std::string> argv = {"estimate",   "--plan",     "{tmp}/" + pf,
+                                           "--workflow", "{tmp}/" + wff, "--topology",
+                                           "{tmp}/" + tf};
+    record(name, argv, rc, o.str(), e.str(), {});
+    json& c = cases.back();
+    c["inputs"] = {{pf, plan.dump(2) + "\n"}, {tf, topo.dump(2) + "\n"}, {wff, wf.dump(2) + "\n"}};
+  };
+  auto P = [&](auto f) {
+    json p = good_plan;
+    f(p);
+    return p;
+  };
+  auto T = [&](auto f) {
+    json t = good_topo;
+    f(t);
+    return t;
+  };
+  auto W = [&](auto f) {
+    json w = good_wf;
+    f(w);
+    return w;
+  };
+  const std::string l6 = "6";  // a task id of the c1 PPO workflow
+  err_case("err_plan_empty_groups", P([](json& p) { p["task_groups"] = json::array(); }),
+           good_topo, good_wf);
+  err_case("err_plan_task_twice", P([](json& p) { p["task_groups"][0].push_back(p["task_groups"][0][0]); }),
+           good_topo, good_wf);
+  err_case("err_plan_unknown_task", P([](json& p) { p["task_groups"][0].push_back(9); }),
+           good_topo, good_wf);
+  err_case("err_plan_counts_len", P([](json& p) { p["gpu_counts"].push_back(1); }), good_topo,
+           good_wf);
+  err_case("err_plan_counts_sum", P([](json& p) { p["gpu_counts"][0] = p["gpu_counts"][0].get<int>() + 1; }),
+           good_topo, good_wf);
+  err_case("err_plan_missing_layout", P([&](json& p) { p["layouts"].erase(l6); }), good_topo,
+           good_wf);
+  err_case("err_plan_stage_sum", P([&](json& p) { p["layouts"][l6]["stage_layers"][0] = 1000; }),
+           good_topo, good_wf);
+  err_case("err_plan_weights", P([&](json& p) { p["layouts"][l6]["replica_batch_weights"][0] = 7.0; }),
+           good_topo, good_wf);
+  err_case("err_plan_dp_zero", P([&](json& p) { p["layouts"][l6]["dp"] = 0; }), good_topo,
+           good_wf);
+  err_case("err_plan_unknown_device", P([](json& p) {
+             for (auto& [k, v] : p["assignment"].items()) {
+               v = "nope";
+               break;
+             }
+           }),
+           good_topo, good_wf);
+  err_case("err_plan_schema", P([](json& p) { p.erase("gpu_counts"); }), good_topo, good_wf);
+  err_case("err_topo_no_devices", good_plan, T([](json& t) { t["devices"] = json::array(); }),
+           good_wf);
+  err_case("err_topo_dup_id", good_plan, T([](json& t) { t["devices"][1]["id"] = t["devices"][0]["id"]; }),
+           good_wf);
+  err_case("err_topo_bad_attr", good_plan, T([](json& t) { t["devices"][2]["mem_gb"] = -1.0; }),
+           good_wf);
+  err_case("err_topo_no_region_link", good_plan, T([](json& t) { t["devices"][3]["region"] = "mars"; }),
+           good_wf);
+  err_case("err_topo_bad_defaults", good_plan,
+           T([](json& t) { t["defaults"]["intra_region_bandwidth_gbps"] = 0.0; }), good_wf);
+  err_case("err_topo_schema", good_plan, T([](json& t) { t["devices"][0].erase("node"); }),
+           good_wf);
+  err_case("err_wf_eta", good_plan, good_topo, W([](json& w) { w["eta"] = 1.5; }));
+  err_case("err_wf_batch", good_plan, good_topo, W([](json& w) { w["batch"]["global_batch"] = 0; }));
+  err_case("err_wf_missing_model", good_plan, good_topo, W([](json& w) { w["models"].erase("critic"); }));
+  err_case("err_wf_layers", good_plan, good_topo,
+           W([](json& w) { w["models"]["actor"]["num_layers"] = 0; }));
+  err_case("err_wf_algorithm", good_plan, good_topo, W([](json& w) { w["algorithm"] = "dpo"; }));
+  err_case("err_wf_parse", good_plan, good_topo, json("not an object"));
   write_file(out_path, json{{"cases", cases}}.dump(1) + "\n");
   std::printf("wrote %zu CLI cases to %s\n", cases.size(), out_path.c_str());
   return 0;

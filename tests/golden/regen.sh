@@ -15,9 +15,15 @@ done
 for c in c3 c4; do
   $R evalplans fixtures/$c.workflow.json fixtures/$c.topology.json 42 24 $G/evalplans_$c.json
 done
+# 256 GPUs, 4 types x 8 regions (the engine's device-index limit); topology
+# from the fleet generator: hetplan_b200 scenario --id fleet --gpus
+# 64xA100,64xL40S,64xL4,64xH100 --regions virginia,ohio,paris,frankfurt,tokyo,
+# sydney,saopaulo,mumbai --seed 3 (byte-identical to the committed fixture)
+$R evalplans fixtures/n256.workflow.json fixtures/n256.topology.json 7 16 $G/evalplans_n256.json
 $R fuzz 20251018 250 $G/fuzz_eval.json
 $R search fixtures/c1.workflow.json fixtures/c1.topology.json 1000 42 $G/search_c1_b1000.json $KNOBS
 $R search fixtures/c2.workflow.json fixtures/c2.topology.json 1000 42 $G/search_c2_b1000.json $KNOBS
+$R search fixtures/n256.workflow.json fixtures/n256.topology.json 1000 42 $G/search_n256_b1000.json $KNOBS
 $R searchfuzz 777 60 $G/searchfuzz.json
 $R sweep fixtures/c4.workflow.json fixtures/c4.topology.json 42 0 2000 $G/sweep_c4.json
 $R exhaustive 4242 40 $G/exhaustive.json

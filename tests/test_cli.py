@@ -43,6 +43,9 @@ def _run_cases(cases):
     tmp = _scratch()
     try:
         for c in cases:
+            for fn, text in c.get("inputs", {}).items():  # defective input files
+                with open(os.path.join(tmp, fn), "w") as f:
+                    f.write(text)
             if c["name"] == "estimate_unknown_device":
                 with open(os.path.join(tmp, "p1.json")) as f:
                     t = f.read()
@@ -98,6 +101,8 @@ def test_cli_fleet_reproduces_config4():
 @pytest.mark.gpu
 def test_cli_plan_estimate_compare_identical():
     """plan (json/text, knobs file, budget/seed flags), estimate, compare and
-    their error paths: byte-identical to the reference CLI"""
+    their error paths (defective plans, topologies and workflows: resolve_plan,
+    DeviceTopology::make and build_workflow validation, JSON schema errors):
+    byte-identical to the reference CLI"""
     bad = _run_cases(load("cli/cases.json")["cases"])
     assert not bad, "\n".join(bad[:10])

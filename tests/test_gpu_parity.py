@@ -82,7 +82,7 @@ def test_fuzz_instances_bit_exact():
     assert not bad, "\n".join(bad[:20])
 
 
-@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3", "c4"])
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3", "c4", "n256"])
 def test_config_plans_bit_exact(cfg_name):
     """A.5 generator + testutil::random_plan plans on the survey configs:
     end_to_end_cost, check_memory, balance_data, balance_layers and the
@@ -130,7 +130,8 @@ def check_search(res, gold, ctx=""):
     return bad
 
 
-@pytest.mark.parametrize("name", ["search_c1_b1000.json", "search_c2_b1000.json"])
+@pytest.mark.parametrize("name", ["search_c1_b1000.json", "search_c2_b1000.json",
+                                  "search_n256_b1000.json"])
 def test_search_configs_identical(name):
     from paper_2512_12476_b200 import SearchKnobs
     g = load(name)
