@@ -740,9 +740,15 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
     for (int i = lane; i < nslot; i += 32) s.dev[i] = rdev[i];
     for (int i = lane; i < s.o.dpk[P.n_tasks]; i += 32) s.dpr_sl[i] = -1;
     __syncwarp();
-    for (int t = 0; t < P.n_tasks; ++t) {
-      apportion(P, s, t);
-      mem_tables(P, cfg, s, t);
+    if (s.n_warps > 1 && P.n_tasks > 1 && mode != kModeMemcheck) {
+      // per task, spread over the team: micro-batches, memory tables and
+      // the geometry memo every later phase needs
+      team_job(P, cfg, s, kJobStage, (1 << P.n_tasks) - 1);
+    } else {
+      for (int t = 0; t < P.n_tasks; ++t) {
+        apportion(P, s, t);
+        mem_tables(P, cfg, s, t);
+      }
     }
     build_dstage(P, s);
 

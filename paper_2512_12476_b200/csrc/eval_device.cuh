@@ -99,7 +99,7 @@ struct Ws {
 };
 
 constexpr int kMaxTeam = kMaxTeamWarps;
-constexpr int kJobTasks = 1, kJobExit = 2, kJobGeometry = 3;
+constexpr int kJobTasks = 1, kJobExit = 2, kJobGeometry = 3, kJobStage = 4;
 
 // diagnostics only (HPG_PLAN_PROFILE): per-plan clock64 phase stamps and
 // per-phase cycle accumulators (sub-phase k < 27 also lands in the plan's
@@ -1252,6 +1252,10 @@ __device__ __forceinline__ void team_share(const DevProblem& P, const DevCostCon
     if (rank % s.n_warps == w) {
       if (kind == kJobTasks) {
         task_cost(P, cfg, s, t, true, s.agg + 7 * t);
+      } else if (kind == kJobStage) {
+        apportion(P, s, t);
+        mem_tables(P, cfg, s, t);
+        ensure_geometry(P, s, t);
       } else {
         ensure_geometry(P, s, t);
       }
