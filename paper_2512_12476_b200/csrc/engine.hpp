@@ -195,6 +195,9 @@ struct Ctx {
   DevBuf<double> d_scratch;  // per-CTA global scratch of eval_kernel
   DevBuf<uint8_t> d_ring;    // device-wide ring memo (RingSlot table)
   DevBuf<uint8_t> d_xch_send, d_xch_recv;  // multi-GPU record exchange
+  // device GA (ga_kernel.cuh): runs, record pools, results, queue, control
+  DevBuf<uint8_t> d_ga;
+  HostBuf<uint8_t> h_ga;
   // exhaustive_search block buffers (keys, dedup table, slots, records, ...)
   DevBuf<uint8_t> d_exh_keys, d_exh_recs;
   DevBuf<unsigned long long> d_exh_table, d_exh_slot, d_exh_count;

@@ -653,6 +653,131 @@ __device__ __noinline__ void team_helper(const DevProblem& P, const DevCostConfi
   }
 }
 
+// One plan evaluated by the warp of s (the lead of its team): stage the
+// record, then the requested mode. Record bytes are read with ld.global.cg:
+// the device GA writes records on other SMs within one launch (no stale L1
+// lines). Balanced [generation weights | stage layers] are written to ows
+// (packed, engine.cpp ws_bytes_of) or back into the record (rec_wb).
+__device__ __forceinline__ EvalResult eval_one(const DevProblem& P, const DevCostConfig& cfg,
+                                               Ws& s, int32_t kb_flags,
+                                               const uint8_t* __restrict__ rec, int mode,
+                                               long long* prof, double* per_task,
+                                               double* required, uint8_t* ows, uint8_t* rec_wb) {
+  const int lane = threadIdx.x & 31;
+  if (prof && lane == 0) {
+    s.prof = prof;
+    prof[0] = clock64();
+  }
+  // ---- stage the plan ----
+  if (lane < 20)
+    reinterpret_cast<int32_t*>(&s.h)[lane] = __ldcg(reinterpret_cast<const int32_t*>(rec) + lane);
+  __syncwarp();
+  if (lane == 0) {
+    rec_offsets(s.h, s.o);
+    s.memo_tp_ok = 0;
+    s.memo_pp_ok = 0;
+    s.memo_cm_ok = 0;
+    s.bridge_ok = 0;
+    s.agg_ok = 0;
+    s.resident_ok = 0;
+    s.memv_ok = 0;
+  }
+  __syncwarp();
+  const int nw = s.o.w[P.n_tasks], nsl = s.o.sl[P.n_tasks], nslot = s.o.dev[P.n_tasks];
+  const double* rw = reinterpret_cast<const double*>(rec + s.o.w_byte);
+  const int32_t* rsl = reinterpret_cast<const int32_t*>(rec + s.o.sl_byte);
+  const uint8_t* rdev = rec + s.o.dev_byte;
+  if (s.h.n_tasks & kRecCompact) {
+    for (int i = lane; i < nw; i += 32) s.w[i] = 1.0;
+    for (int t = 0; t < P.n_tasks; ++t) {
+      const int pp = s.h.pp[t];
+      const int64_t nl = P.task[t].nl;
+      for (int j = lane; j < pp; j += 32)
+        s.sl[s.o.sl[t] + j] = static_cast<int32_t>(nl / pp) + (j < nl % pp ? 1 : 0);
+    }
+  } else {
+    for (int i = lane; i < nw; i += 32) s.w[i] = __ldcg(rw + i);
+    for (int i = lane; i < nsl; i += 32) s.sl[i] = __ldcg(rsl + i);
+  }
+  for (int i = lane; i < nslot; i += 32) s.dev[i] = __ldcg(rdev + i);
+  for (int i = lane; i < s.o.dpk[P.n_tasks]; i += 32) s.dpr_sl[i] = -1;
+  __syncwarp();
+  if (s.n_warps > 1 && P.n_tasks > 1 && mode != kModeMemcheck) {
+    // per task, spread over the team: micro-batches, memory tables and
+    // the geometry memo every later phase needs
+    team_job(P, cfg, s, kJobStage, (1 << P.n_tasks) - 1);
+  } else {
+    for (int t = 0; t < P.n_tasks; ++t) {
+      apportion(P, s, t);
+      mem_tables(P, cfg, s, t);
+    }
+  }
+  build_dstage(P, s);
+
+  EvalResult r;
+  r.cost = -1.0;
+  r.reshard_s = 0.0;
+  r.sync_s = 0.0;
+  r.flags = 0;
+  r.pad = 0;
+  const bool feas_in = check_memory(P, cfg, s, required);
+  if (feas_in) r.flags |= kResFeasIn;
+  if (mode == kModeE2E) {
+    const E2E e = end_to_end(P, cfg, s);
+    r.cost = e.e2e;
+    r.reshard_s = e.reshard;
+    r.sync_s = e.sync;
+    if (e.feasible) r.flags |= kResFeasOut;
+    if (per_task) {
+      for (int i = lane; i < 7 * P.n_tasks; i += 32) per_task[i] = s.agg[i];
+    }
+  } else if (mode == kModeEvaluate || mode == kModeChain || mode == kModeBalanceData ||
+             mode == kModeBalanceLayers) {
+    const bool chain = mode == kModeEvaluate || mode == kModeChain;
+    const bool go = mode != kModeEvaluate || feas_in;
+    if (go) {
+      team_geometry(P, cfg, s);
+      bool have_cur = false, ch = false;
+      E2E cur;
+      if ((chain && (kb_flags & 1)) || mode == kModeBalanceData) {
+        if (prof && lane == 0) prof[1] = clock64();
+        have_cur = balance_data_dev(P, cfg, s, cur, ch);
+        if (ch) r.flags |= kResWeights;
+      }
+      if (prof && lane == 0) prof[2] = clock64();
+      if ((chain && (kb_flags & 2)) || mode == kModeBalanceLayers) {
+        balance_layers_dev(P, cfg, s, have_cur, cur, ch);
+        if (ch) r.flags |= kResLayers;
+      }
+      if (prof && lane == 0) prof[3] = clock64();
+      if (!have_cur) cur = end_to_end(P, cfg, s);
+      r.cost = cur.e2e;
+      r.reshard_s = cur.reshard;
+      r.sync_s = cur.sync;
+      if (cur.feasible) r.flags |= kResFeasOut;
+    }
+  }
+  // ---- write back what balancing can change: [generation task weights |
+  // all stage layers] (engine.cpp ws_bytes_of / apply_ws) ----
+  if (!(s.h.n_tasks & kRecCompact)) {
+    const int g = P.gen_slot;
+    const int dpg = g >= 0 ? s.h.dp[g] : 0;
+    if (ows) {
+      double* ow = reinterpret_cast<double*>(ows);
+      int32_t* osl = reinterpret_cast<int32_t*>(ows + 8 * dpg);
+      for (int i = lane; i < dpg; i += 32) ow[i] = s.w[s.o.w[g] + i];
+      for (int i = lane; i < nsl; i += 32) osl[i] = s.sl[i];
+    } else if (rec_wb) {
+      double* ow = reinterpret_cast<double*>(rec_wb + s.o.w_byte) + (g >= 0 ? s.o.w[g] : 0);
+      int32_t* osl = reinterpret_cast<int32_t*>(rec_wb + s.o.sl_byte);
+      for (int i = lane; i < dpg; i += 32) ow[i] = s.w[s.o.w[g] + i];
+      for (int i = lane; i < nsl; i += 32) osl[i] = s.sl[i];
+    }
+  }
+  __syncwarp();
+  return r;
+}
+
 // kTeam = 1: one warp per CTA, register-capped for occupancy (big waves, the
 // sweep); kTeam = 2: pairs at the same register cap (medium waves);
 // kTeam = kMaxTeam: up to four warps per plan, uncapped (small waves)
@@ -696,118 +821,17 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
   Ws& s = team[0];
   for (int p = blockIdx.x; p < n; p += gridDim.x) {
     const int64_t rec_at = off ? off[p] : static_cast<int64_t>(p) * stride;
-    const uint8_t* rec = recs + rec_at;
     const int mode = modes ? modes[p] : uniform_mode;
     if (mode == kModeSkip) {
       if (lane == 0) res[p] = EvalResult{-1.0, 0.0, 0.0, 0, 0};
       continue;
     }
     long long* prof = g_plan_prof ? g_plan_prof + kPlanProfSlots * static_cast<int64_t>(p) : nullptr;
-    if (prof && lane == 0) {
-      s.prof = prof;
-      prof[0] = clock64();
-    }
-    // ---- stage the plan ----
-    if (lane < 20) reinterpret_cast<int32_t*>(&s.h)[lane] = reinterpret_cast<const int32_t*>(rec)[lane];
-    __syncwarp();
-    if (lane == 0) {
-      rec_offsets(s.h, s.o);
-      s.memo_tp_ok = 0;
-      s.memo_pp_ok = 0;
-      s.memo_cm_ok = 0;
-      s.bridge_ok = 0;
-      s.agg_ok = 0;
-      s.resident_ok = 0;
-      s.memv_ok = 0;
-    }
-    __syncwarp();
-    const int nw = s.o.w[P.n_tasks], nsl = s.o.sl[P.n_tasks], nslot = s.o.dev[P.n_tasks];
-    const double* rw = reinterpret_cast<const double*>(rec + s.o.w_byte);
-    const int32_t* rsl = reinterpret_cast<const int32_t*>(rec + s.o.sl_byte);
-    const uint8_t* rdev = rec + s.o.dev_byte;
-    if (s.h.n_tasks & kRecCompact) {
-      for (int i = lane; i < nw; i += 32) s.w[i] = 1.0;
-      for (int t = 0; t < P.n_tasks; ++t) {
-        const int pp = s.h.pp[t];
-        const int64_t nl = P.task[t].nl;
-        for (int j = lane; j < pp; j += 32)
-          s.sl[s.o.sl[t] + j] = static_cast<int32_t>(nl / pp) + (j < nl % pp ? 1 : 0);
-      }
-    } else {
-      for (int i = lane; i < nw; i += 32) s.w[i] = rw[i];
-      for (int i = lane; i < nsl; i += 32) s.sl[i] = rsl[i];
-    }
-    for (int i = lane; i < nslot; i += 32) s.dev[i] = rdev[i];
-    for (int i = lane; i < s.o.dpk[P.n_tasks]; i += 32) s.dpr_sl[i] = -1;
-    __syncwarp();
-    if (s.n_warps > 1 && P.n_tasks > 1 && mode != kModeMemcheck) {
-      // per task, spread over the team: micro-batches, memory tables and
-      // the geometry memo every later phase needs
-      team_job(P, cfg, s, kJobStage, (1 << P.n_tasks) - 1);
-    } else {
-      for (int t = 0; t < P.n_tasks; ++t) {
-        apportion(P, s, t);
-        mem_tables(P, cfg, s, t);
-      }
-    }
-    build_dstage(P, s);
-
-    EvalResult r;
-    r.cost = -1.0;
-    r.reshard_s = 0.0;
-    r.sync_s = 0.0;
-    r.flags = 0;
-    r.pad = 0;
-    const bool feas_in =
-        check_memory(P, cfg, s, required ? required + static_cast<int64_t>(p) * P.n_dev : nullptr);
-    if (feas_in) r.flags |= kResFeasIn;
-    if (mode == kModeE2E) {
-      const E2E e = end_to_end(P, cfg, s);
-      r.cost = e.e2e;
-      r.reshard_s = e.reshard;
-      r.sync_s = e.sync;
-      if (e.feasible) r.flags |= kResFeasOut;
-      if (per_task) {
-        for (int i = lane; i < 7 * P.n_tasks; i += 32)
-          per_task[static_cast<int64_t>(p) * 7 * P.n_tasks + i] = s.agg[i];
-      }
-    } else if (mode == kModeEvaluate || mode == kModeChain || mode == kModeBalanceData ||
-               mode == kModeBalanceLayers) {
-      const bool chain = mode == kModeEvaluate || mode == kModeChain;
-      const bool go = mode != kModeEvaluate || feas_in;
-      if (go) {
-        team_geometry(P, cfg, s);
-        bool have_cur = false, ch = false;
-        E2E cur;
-        if ((chain && (kb_flags & 1)) || mode == kModeBalanceData) {
-          if (prof && lane == 0) prof[1] = clock64();
-          have_cur = balance_data_dev(P, cfg, s, cur, ch);
-          if (ch) r.flags |= kResWeights;
-        }
-        if (prof && lane == 0) prof[2] = clock64();
-        if ((chain && (kb_flags & 2)) || mode == kModeBalanceLayers) {
-          balance_layers_dev(P, cfg, s, have_cur, cur, ch);
-          if (ch) r.flags |= kResLayers;
-        }
-        if (prof && lane == 0) prof[3] = clock64();
-        if (!have_cur) cur = end_to_end(P, cfg, s);
-        r.cost = cur.e2e;
-        r.reshard_s = cur.reshard;
-        r.sync_s = cur.sync;
-        if (cur.feasible) r.flags |= kResFeasOut;
-      }
-    }
-    // ---- write back what balancing can change: [generation task weights |
-    // all stage layers] (engine.cpp ws_bytes_of / apply_ws) ----
-    if (out_ws && !(s.h.n_tasks & kRecCompact)) {
-      uint8_t* ows = out_ws + out_off[p];
-      const int g = P.gen_slot;
-      const int dpg = g >= 0 ? s.h.dp[g] : 0;
-      double* ow = reinterpret_cast<double*>(ows);
-      int32_t* osl = reinterpret_cast<int32_t*>(ows + 8 * dpg);
-      for (int i = lane; i < dpg; i += 32) ow[i] = s.w[s.o.w[g] + i];
-      for (int i = lane; i < nsl; i += 32) osl[i] = s.sl[i];
-    }
+    const EvalResult r =
+        eval_one(P, cfg, s, kb_flags, recs + rec_at, mode, prof,
+                 per_task ? per_task + static_cast<int64_t>(p) * 7 * P.n_tasks : nullptr,
+                 required ? required + static_cast<int64_t>(p) * P.n_dev : nullptr,
+                 out_ws ? out_ws + out_off[p] : nullptr, nullptr);
     if (prof && lane == 0) prof[4] = clock64();
     if (lane == 0) res[p] = r;
     __syncwarp();
@@ -907,3 +931,5 @@ cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
 }
 
 }  // namespace hpg
+
+#include "ga_kernel.cuh"

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "common.hpp"
+#include "ga_dev.hpp"
 
 namespace hpg {
 
@@ -28,6 +29,12 @@ cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
                         double* d_per_task,
                         double* d_required, double* d_scratch, int64_t scratch_doubles,
                         int grid, cudaStream_t st);
+
+// Device-resident GA offspring loop of many runs (ga_kernel.cuh): one
+// persistent launch, grid = SMs x resident one-warp workers
+cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
+                                const GaParams& G, double* gscratch, int64_t gscratch_doubles,
+                                int n_sm, int& grid, cudaStream_t st);
 
 // Segmented best-half selection (search.cpp:590-620) for one SHA level.
 cudaError_t launch_best_half(const double* d_scores, const int32_t* d_seg_off,

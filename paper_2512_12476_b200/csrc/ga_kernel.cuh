@@ -1,0 +1,1173 @@
+// Device-resident GA offspring loop, included by eval.cu so
+// that the workers share eval_one with eval_kernel.
+//
+// ga_run's offspring loop (reference search.cpp:471-563; the host coroutine in
+// search.cpp is the same algorithm with the same speculation) runs as a state
+// machine per run in global memory. A persistent grid of one-warp workers
+// takes tasks from a ticketed ring: "evaluate candidate i of run r" or "step
+// run r". The worker that finishes the last evaluation of a wave continues
+// that run's GA step itself, which draws the next wave's candidates (record
+// copies + device-slot moves with the run's RNG stream, replayed bit for bit),
+// publishes all but one of them and evaluates the last one directly. No host
+// round trip and no lockstep: each run waits only for its own candidates.
+//
+// GA control flow is computed redundantly by all 32 lanes (same loads, same
+// draws); lane 0 writes, and every write other lanes read back is followed
+// by __syncwarp. Everything another SM may have written in this launch is
+// read with ld.global.cg.
+#pragma once
+
+#include "ga_dev.hpp"
+#include "gen_ga.hpp"
+#include "rng_jump.hpp"
+
+#define GA_BOUNDED(r, n) ga_bounded(r, n, c_ga.fastmod)
+
+namespace hpg {
+namespace dev {
+
+// the launch's parameters (constant bank: read by every GA function)
+__constant__ GaParams c_ga;
+
+__device__ __forceinline__ unsigned long long ga_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// next() % n, exactly, through a 128-bit reciprocal (Lemire, Kaser & Kurz
+// 2019; gen_ga.cu bounded_fast, the host's fastmod_u64)
+__device__ __forceinline__ uint64_t ga_bounded(Rng& rng, uint64_t n, const uint64_t* fm) {
+  const uint64_t a = rng.next();
+  if (n > static_cast<uint64_t>(kGenFastModMax)) return a % n;
+  const uint64_t mlo = __ldg(fm + 2 * n), mhi = __ldg(fm + 2 * n + 1);
+  const uint64_t low_lo = mlo * a;
+  const uint64_t low_hi = __umul64hi(mlo, a) + mhi * a;
+  const uint64_t bottom = __umul64hi(low_lo, n);
+  const uint64_t top_lo = low_hi * n;
+  const uint64_t top_hi = __umul64hi(low_hi, n);
+  const uint64_t sum_lo = top_lo + bottom;
+  return top_hi + (sum_lo < top_lo ? 1 : 0);
+}
+
+__device__ __forceinline__ Rng ga_ld_rng(const Rng* p) {
+  Rng r;
+  r.seed = __ldcg(&p->seed);
+  for (int i = 0; i < 4; ++i) r.s[i] = __ldcg(&p->s[i]);
+  return r;
+}
+
+__device__ __forceinline__ void ga_st_rng(Rng* p, const Rng& r) {
+  if ((threadIdx.x & 31) == 0) *p = r;
+}
+
+__device__ __forceinline__ bool ga_same_rng(const Rng& a, const Rng& b) {
+  return a.seed == b.seed && a.s[0] == b.s[0] && a.s[1] == b.s[1] && a.s[2] == b.s[2] &&
+         a.s[3] == b.s[3];
+}
+
+// Per-warp shared-memory scratch of a GA step: the child and a parent record,
+// the trial being built, the finished wave's results and the population, so
+// that drawing a wave costs a handful of L2 round trips, not one per move.
+struct GaSm {
+  uint8_t* gen;  // init generation scratch (aliases the evaluation carve)
+  uint32_t* gw;  // rank set per task group of the current source [kMaxTasks][8]
+  uint8_t* child;
+  uint8_t* par;
+  uint8_t* tmp;
+  EvalResult* res;
+  int32_t* pslot;
+  double* pcost;
+  uint64_t* pseq;
+};
+
+__host__ __device__ inline int ga_smem_bytes(int stride, int max_wave) {
+  return 3 * stride + 32 * max_wave + kGaMaxPop * (4 + 8 + 8) + 32 * kMaxTasks;
+}
+
+struct GaView {
+  GaRun* R;
+  int run;
+  uint8_t* pool;
+  int stride;
+  int ng;
+  int gstart[kMaxTasks + 1];
+  int gslot[kMaxTasks];
+  int counts[kMaxTasks];
+  int opt_off[kMaxTasks + 1];
+  int64_t opt_base;
+  GaSm sm;
+  __device__ uint8_t* slot(int k) const { return pool + static_cast<int64_t>(k) * stride; }
+  __device__ uint8_t* wave_slot(int buf, int i) const {
+    return slot(2 + c_ga.pop_cap + buf * c_ga.max_wave + i);
+  }
+};
+
+// global record -> shared (one round trip: the whole slot)
+__device__ __forceinline__ void ga_ld_rec(uint8_t* dst, const uint8_t* src, int stride) {
+  const int lane = threadIdx.x & 31;
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  for (int i = lane; i < (stride >> 4); i += 32) d[i] = __ldcg(s + i);
+  __syncwarp();
+}
+
+// shared record -> global (the record's own bytes)
+__device__ __forceinline__ void ga_st_rec(uint8_t* dst, const uint8_t* src) {
+  const int lane = threadIdx.x & 31;
+  const int n16 = (*reinterpret_cast<const int32_t*>(src) + 15) >> 4;
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  for (int i = lane; i < n16; i += 32) d[i] = s[i];
+  __syncwarp();
+}
+
+__device__ __forceinline__ void ga_sm_copy(uint8_t* dst, const uint8_t* src) {
+  const int lane = threadIdx.x & 31;
+  const int n16 = (*reinterpret_cast<const int32_t*>(src) + 15) >> 4;
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  for (int i = lane; i < n16; i += 32) d[i] = s[i];
+  __syncwarp();
+}
+
+// global record -> global (improvement / best-member copies)
+__device__ __forceinline__ void ga_rec_copy(uint8_t* dst, const uint8_t* src) {
+  const int lane = threadIdx.x & 31;
+  const int bytes = __ldcg(reinterpret_cast<const int32_t*>(src));
+  const int n16 = (bytes + 15) >> 4;
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  for (int i = lane; i < n16; i += 32) d[i] = __ldcg(s + i);
+  __syncwarp();
+}
+
+// device-slot geometry of a (shared-memory) record
+struct GaGeo {
+  int dev_byte;
+  int off[kMaxTasks + 1];
+};
+
+__device__ __forceinline__ void ga_geo(const uint8_t* rec, int T, GaGeo& g) {
+  const RecHeader& h = *reinterpret_cast<const RecHeader*>(rec);
+  int sw = 0, ssl = 0;
+  g.off[0] = 0;
+  for (int t = 0; t < T; ++t) {
+    sw += h.dp[t];
+    ssl += h.pp[t];
+    g.off[t + 1] = g.off[t] + h.dp[t] * h.pp[t] * h.tp[t];
+  }
+  g.dev_byte = static_cast<int>(sizeof(RecHeader)) + 8 * sw + 4 * ssl;
+}
+
+// group_device_set as a bitmask over id ranks (search.cpp:336-341)
+__device__ __forceinline__ void ga_rank_set(const uint8_t* d, int n,
+                                            uint32_t (&w)[8]) {
+  const int lane = threadIdx.x & 31;
+  uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = lane; i < n; i += 32) {
+    const int r = __ldg(c_ga.id_rank + d[i]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if ((r >> 5) == k) m[k] |= 1u << (r & 31);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = __reduce_or_sync(0xffffffffu, m[k]);
+}
+
+__device__ __forceinline__ int ga_select_rank(const uint32_t (&w)[8],
+                                              uint64_t idx) {
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t pc = static_cast<uint64_t>(__popc(w[k]));
+    if (idx >= pc) {
+      idx -= pc;
+      continue;
+    }
+    uint32_t x = w[k];
+    for (uint64_t i = 0; i < idx; ++i) x &= x - 1;
+    return __ldg(c_ga.by_id_rank + 32 * k + __ffs(x) - 1);
+  }
+  return -1;
+}
+
+// first index i < n with d[i] == v (lane-parallel), or -1
+__device__ __forceinline__ int ga_find(const uint8_t* d, int n, int v) {
+  const int lane = threadIdx.x & 31;
+  for (int b = 0; b < n; b += 32) {
+    const int i = b + lane;
+    const bool hit = i < n && d[i] == v;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) return b + __ffs(m) - 1;
+  }
+  return -1;
+}
+
+// ---- trials drawn lane-parallel ----
+// Every trial of a wave starts from the same source record (the child, or the
+// parent of a mutation stage) and a move consumes a fixed number of draws
+// (level 3: four, level 5: three; a mutation one more for its level), so
+// each lane steps the stream to its trial's start, computes the trial's
+// device-slot patches against the source, and the warp writes the records.
+struct GaSrcInfo {
+  GaGeo geo;
+  int ne;
+  int elig[kMaxTasks];
+};
+
+constexpr int kGaMaxPatch = 2 * kMaxTasks;
+
+// per-source tables: geometry, eligible tasks, rank set of every group
+__device__ void ga_src_info(const GaView& v, const uint8_t* src, GaSrcInfo& si) {
+  ga_geo(src, c_ga.n_tasks, si.geo);
+  si.ne = 0;
+  for (int s = 0; s < c_ga.n_tasks; ++s)
+    if (si.geo.off[s + 1] - si.geo.off[s] >= 2) si.elig[si.ne++] = s;
+  const uint8_t* dv = src + si.geo.dev_byte;
+  for (int g = 0; g < v.ng; ++g) {
+    const int s = v.gslot[v.gstart[g]];
+    uint32_t w[8];
+    ga_rank_set(dv + si.geo.off[s], si.geo.off[s + 1] - si.geo.off[s], w);
+    if ((threadIdx.x & 31) == 0)
+      for (int k = 0; k < 8; ++k) v.sm.gw[g * 8 + k] = w[k];
+  }
+  __syncwarp();
+}
+
+// one move of this lane against the source: patches (absolute device-slot
+// index, new byte); the draws of random_move (search.cpp:360-421)
+__device__ __forceinline__ int ga_lane_move(const GaView& v, const uint8_t* src,
+                                            const GaSrcInfo& si, int level, Rng& rng,
+                                            int (&pp)[kGaMaxPatch], int (&pv)[kGaMaxPatch]) {
+  const uint8_t* dv = src + si.geo.dev_byte;
+  int np = 0;
+  if (level == 3) {
+    const int ng = v.ng;
+    const int g1 = static_cast<int>(GA_BOUNDED(rng, static_cast<uint64_t>(ng)));
+    int g2 = static_cast<int>(GA_BOUNDED(rng, static_cast<uint64_t>(ng - 1)));
+    if (g2 >= g1) ++g2;
+    const int s1 = v.gslot[v.gstart[g1]], s2 = v.gslot[v.gstart[g2]];
+    const int n1 = si.geo.off[s1 + 1] - si.geo.off[s1], n2 = si.geo.off[s2 + 1] - si.geo.off[s2];
+    uint32_t w1[8], w2[8];
+    for (int k = 0; k < 8; ++k) {
+      w1[k] = v.sm.gw[g1 * 8 + k];
+      w2[k] = v.sm.gw[g2 * 8 + k];
+    }
+    const int b = ga_select_rank(w2, GA_BOUNDED(rng, static_cast<uint64_t>(n2)));
+    const int a = ga_select_rank(w1, GA_BOUNDED(rng, static_cast<uint64_t>(n1)));
+    for (int side = 0; side < 2; ++side) {
+      const int g = side ? g2 : g1, from = side ? b : a, to = side ? a : b;
+      for (int k = v.gstart[g]; k < v.gstart[g + 1]; ++k) {
+        const int s = v.gslot[k];
+        const int o = si.geo.off[s], n = si.geo.off[s + 1] - o;
+        for (int i = 0; i < n; ++i)
+          if (dv[o + i] == from) {
+            pp[np] = o + i;
+            pv[np++] = to;
+            break;
+          }
+      }
+    }
+    return np;
+  }
+  const int s = si.elig[GA_BOUNDED(rng, static_cast<uint64_t>(si.ne))];
+  const int o = si.geo.off[s];
+  const uint64_t n = static_cast<uint64_t>(si.geo.off[s + 1] - o);
+  const uint64_t p1 = GA_BOUNDED(rng, n);
+  uint64_t p2 = GA_BOUNDED(rng, n - 1);
+  if (p2 >= p1) ++p2;
+  pp[0] = o + static_cast<int>(p1);
+  pv[0] = dv[o + p2];
+  pp[1] = o + static_cast<int>(p2);
+  pv[1] = dv[o + p1];
+  return 2;
+}
+
+// writes trials [0, n) = the source with lane t's patches, to buffer buf
+// from index at: all record chunks of all trials in one pass, then the patches
+__device__ __forceinline__ void ga_emit_all(const GaView& v, int buf, int at, int n,
+                                            const uint8_t* src, int dev_byte, int np,
+                                            const int (&pp)[kGaMaxPatch],
+                                            const int (&pv)[kGaMaxPatch]) {
+  const int lane = threadIdx.x & 31;
+  const int n16 = (*reinterpret_cast<const int32_t*>(src) + 15) >> 4;
+  const int4* s = reinterpret_cast<const int4*>(src);
+  uint8_t* d0 = v.wave_slot(buf, at);
+  for (int k = lane; k < n * n16; k += 32) {
+    const int t = k / n16, c = k - t * n16;
+    reinterpret_cast<int4*>(d0 + static_cast<int64_t>(t) * v.stride)[c] = s[c];
+  }
+  __syncwarp();
+  if (lane < n) {
+    uint8_t* d = d0 + static_cast<int64_t>(lane) * v.stride + dev_byte;
+    for (int q = 0; q < np; ++q) d[pp[q]] = static_cast<uint8_t>(pv[q]);
+  }
+  __syncwarp();
+}
+
+// draw_mut: up to kGaTrials mutated copies of the (shared) parent, then the
+// parent itself, stored to stage buffer buf from index base
+__device__ void ga_draw_mut(const GaView& v, Rng r, const uint8_t* parent, GaStage* st, int buf,
+                            int base) {
+  const int lane = threadIdx.x & 31;
+  GaSrcInfo si;
+  ga_src_info(v, parent, si);
+  const bool has_l3 = v.ng >= 2, has_l5 = si.ne > 0;
+  int ntr = 0;
+  Rng mine = r;
+  int np = 0, pp[kGaMaxPatch], pv[kGaMaxPatch];
+  if (has_l3 || has_l5) {
+    // stream positions: every trial is one mutate (level draw + move draws)
+    ntr = kGaTrials;
+    Rng q = r;
+    for (int t = 0; t < kGaTrials; ++t) {
+      if (lane == t) mine = q;
+      int level;
+      if (has_l3 && has_l5) {
+        level = GA_BOUNDED(q, 2) == 0 ? 3 : 5;
+      } else {
+        level = has_l3 ? 3 : 5;
+      }
+      for (int k = 0; k < (level == 3 ? 4 : 3); ++k) q.next();
+    }
+    r = q;
+    if (lane < kGaTrials) {
+      int level;
+      if (has_l3 && has_l5) {
+        level = GA_BOUNDED(mine, 2) == 0 ? 3 : 5;
+      } else {
+        level = has_l3 ? 3 : 5;
+      }
+      np = ga_lane_move(v, parent, si, level, mine, pp, pv);
+      st->snaps[lane] = mine;  // the stream after this trial
+    }
+    __syncwarp();
+    ga_emit_all(v, buf, base, ntr, parent, si.geo.dev_byte, np, pp, pv);
+  }
+  ga_st_rng(&st->after_all, r);
+  ga_st_rec(v.wave_slot(buf, base + ntr), parent);
+  if (lane == 0) {
+    st->buf = buf;
+    st->base = base;
+    st->ntr = ntr;
+  }
+  __syncwarp();
+}
+
+
+// ---- init phase: make_candidate on the device (search.cpp:152-234, 283-334) ----
+
+// record layout of combination `combo` (decode_layout_combo): header, unit
+// weights, uniform stage split (init_cand, make_layout plan.cpp:89-100)
+__device__ void ga_lane_layouts(const GaView& v, int64_t combo, uint8_t* rec, RecOffsets& o) {
+    RecHeader h;
+  h.bytes = 0;
+  h.n_tasks = c_ga.n_tasks;
+  for (int t = 0; t < kMaxTasks; ++t) h.dp[t] = h.pp[t] = h.tp[t] = 0;
+  for (int k = 0; k < c_ga.n_tasks; ++k) {
+    const int s = v.gslot[k];
+    const int n_opt = v.opt_off[k + 1] - v.opt_off[k];
+    const short4 l = __ldg(c_ga.opts + v.opt_base + v.opt_off[k] + static_cast<int>(combo % n_opt));
+    combo /= n_opt;
+    h.dp[s] = l.x;
+    h.pp[s] = l.y;
+    h.tp[s] = l.z;
+  }
+  rec_offsets(h, o);
+  h.bytes = o.bytes;
+  int32_t* hw = reinterpret_cast<int32_t*>(rec);
+  const int32_t* hs = reinterpret_cast<const int32_t*>(&h);
+  for (int i = 0; i < 20; ++i) hw[i] = hs[i];
+  double* w = reinterpret_cast<double*>(rec + o.w_byte);
+  for (int i = 0; i < o.w[c_ga.n_tasks]; ++i) w[i] = 1.0;
+  int32_t* sl = reinterpret_cast<int32_t*>(rec + o.sl_byte);
+  for (int t = 0; t < c_ga.n_tasks; ++t) {
+    const int64_t nl = c_ga.task_nl[t];
+    const int pp = h.pp[t];
+    for (int j = 0; j < pp; ++j)
+      sl[o.sl[t] + j] = static_cast<int32_t>(nl / pp) + (j < nl % pp ? 1 : 0);
+  }
+  for (int i = o.dev_byte + o.dev[c_ga.n_tasks]; i < o.bytes; ++i) rec[i] = 0;  // padding
+}
+
+template <typename T>
+__device__ __forceinline__ void ga_shuffle(Rng& rng, T* a, int n, const uint64_t* fm) {
+  for (int i = n; i > 1; --i) {
+    const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
+    const T tmp = a[i - 1];
+    a[i - 1] = a[j];
+    a[j] = tmp;
+  }
+}
+
+// per-lane generation scratch, interleaved across the warp's lanes (element
+// i of a lane's array at [i][lane]): in shared memory (aliasing the idle
+// evaluation carve) or, for large problems, in the worker's global scratch
+struct GaGenScratch {
+  int16_t* s16;  // int16 arrays: regions | nodes | cnt | start | fill | ranks
+  uint8_t* s8;   // uint8 arrays: flat | bucket
+  int lane;
+  __device__ int16_t& a16(int i) const { return s16[i * 32 + lane]; }
+  __device__ uint8_t& a8(int i) const { return s8[i * 32 + lane]; }
+};
+
+// one candidate by this lane: layouts, random_medium_assignment and
+// random_fine_assignment per task of each group (the reference's draws)
+__device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng, uint8_t* rec,
+                             const GaGenScratch& sc) {
+    const uint64_t* fm = c_ga.fastmod;
+  RecOffsets o;
+  ga_lane_layouts(v, combo, rec, o);
+  const int o_nodes = c_ga.n_regions, o_cnt = o_nodes + c_ga.max_nodes_per_region,
+            o_start = o_cnt + c_ga.n_nodes, o_fill = o_start + c_ga.n_nodes, o_ranks = o_fill + c_ga.n_nodes;
+  const int o_bucket = c_ga.n_dev;
+  for (int r = 0; r < c_ga.n_regions; ++r) sc.a16(r) = static_cast<int16_t>(r);
+  for (int i = c_ga.n_regions; i > 1; --i) {
+    const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
+    const int16_t t = sc.a16(i - 1);
+    sc.a16(i - 1) = sc.a16(j);
+    sc.a16(j) = t;
+  }
+  int nf = 0;
+  for (int ri = 0; ri < c_ga.n_regions; ++ri) {
+    const int reg = sc.a16(ri);
+    const int n0 = __ldg(c_ga.region_off + reg), nn = __ldg(c_ga.region_off + reg + 1) - n0;
+    for (int q = 0; q < nn; ++q) sc.a16(o_nodes + q) = static_cast<int16_t>(q);
+    for (int i = nn; i > 1; --i) {
+      const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
+      const int16_t t = sc.a16(o_nodes + i - 1);
+      sc.a16(o_nodes + i - 1) = sc.a16(o_nodes + j);
+      sc.a16(o_nodes + j) = t;
+    }
+    for (int q = 0; q < nn; ++q) {
+      const int node = n0 + sc.a16(o_nodes + q);
+      for (int e = __ldg(c_ga.node_off + node); e < __ldg(c_ga.node_off + node + 1); ++e)
+        sc.a8(nf++) = __ldg(c_ga.node_devs + e);
+    }
+  }
+  for (int i = nf; i > 1; --i) {
+    const bool scramble = (static_cast<double>(rng.next() >> 11) * 0x1.0p-53) < (1.0 - c_ga.bias);
+    const int pick = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
+    if (scramble) {
+      const uint8_t t = sc.a8(i - 1);
+      sc.a8(i - 1) = sc.a8(pick);
+      sc.a8(pick) = t;
+    }
+  }
+  uint8_t* dv = rec + o.dev_byte;
+  int cursor = 0;
+  for (int g = 0; g < v.ng; ++g) {
+    const int n = v.counts[g];
+    for (int k = v.gstart[g]; k < v.gstart[g + 1]; ++k) {
+      const int s = v.gslot[k];
+      for (int r = 0; r < c_ga.n_nodes; ++r) sc.a16(o_cnt + r) = 0;
+      for (int i = 0; i < n; ++i) ++sc.a16(o_cnt + __ldg(c_ga.node_rank + sc.a8(cursor + i)));
+      int nr = 0, acc = 0;
+      for (int r = 0; r < c_ga.n_nodes; ++r) {
+        const int c = sc.a16(o_cnt + r);
+        if (!c) continue;
+        sc.a16(o_ranks + nr++) = static_cast<int16_t>(r);
+        sc.a16(o_start + r) = static_cast<int16_t>(acc);
+        acc += c;
+      }
+      for (int q = 0; q < nr; ++q) {
+        const int rk = sc.a16(o_ranks + q);
+        sc.a16(o_fill + rk) = sc.a16(o_start + rk);
+      }
+      for (int i = 0; i < n; ++i) {
+        const uint8_t d = sc.a8(cursor + i);
+        int16_t& f = sc.a16(o_fill + __ldg(c_ga.node_rank + d));
+        sc.a8(o_bucket + f) = d;
+        ++f;
+      }
+      for (int i = nr; i > 1; --i) {
+        const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
+        const int16_t t = sc.a16(o_ranks + i - 1);
+        sc.a16(o_ranks + i - 1) = sc.a16(o_ranks + j);
+        sc.a16(o_ranks + j) = t;
+      }
+      uint8_t* out = dv + o.dev[s];
+      int pos = 0;
+      for (int q = 0; q < nr; ++q) {
+        const int rk = sc.a16(o_ranks + q);
+        const int b0 = o_bucket + sc.a16(o_start + rk);
+        const int nb = sc.a16(o_cnt + rk);
+        for (int i = nb; i > 1; --i) {
+          const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
+          const uint8_t t = sc.a8(b0 + i - 1);
+          sc.a8(b0 + i - 1) = sc.a8(b0 + j);
+          sc.a8(b0 + j) = t;
+        }
+        for (int i = 0; i < nb; ++i) out[pos++] = sc.a8(b0 + i);
+      }
+    }
+    cursor += n;
+  }
+}
+
+// an init chunk: candidates combo0 + c for c < n from stream state rng, one
+// lane each (lane c steps the stream c * gen_draws values ahead); the stream
+// after candidate c is kept for the chunk's walk
+__device__ void ga_init_chunk(const GaView& v, const Rng& rng, int64_t combo0, int n) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t* jumps = c_ga.jumps + 4 * static_cast<int64_t>(__ldcg(&v.R->jump_off));
+  Rng* snaps = c_ga.init_snaps + static_cast<int64_t>(v.run) * c_ga.init_cap;
+  GaGenScratch sc;
+  uint8_t* base = c_ga.gen_in_smem ? v.sm.gen : c_ga.gen_scratch + static_cast<int64_t>(blockIdx.x) *
+                                                                     c_ga.gen_smem * 32;
+  sc.s16 = reinterpret_cast<int16_t*>(base);
+  sc.s8 = base + 64 * (c_ga.n_regions + c_ga.max_nodes_per_region + 4 * c_ga.n_nodes);
+  sc.lane = lane;
+  Rng r = rng;
+  // lane c starts c candidates (c * gen_draws values) into the chunk, then
+  // moves 31 candidates ahead after each of its candidates
+  if (lane > 0 && lane < n) rng_apply_jump(r, jumps + 4 * (lane - 1));
+  for (int c = lane; c < n; c += 32) {
+    if (c > lane) rng_apply_jump(r, jumps + 4 * 30);
+    ga_lane_make(v, combo0 + c, r, v.wave_slot(0, c), sc);
+    snaps[c] = r;
+  }
+  __threadfence_block();
+  __syncwarp();
+}
+
+// per-run scalar state, identical in every lane during a step
+struct GaHot {
+  Rng rng;
+  int64_t used, streak, seq;
+  double best, best_member_cost;
+  int n_pop, state, have_spec, best_member_flags, impr_flags;
+  int child_buf, child_idx;
+  double child_cost;
+  int n3, n5, m5;
+  Rng before3, before5, b5;
+  int64_t n_offspring, n_waves, n_evals;
+  unsigned long long impr_time;
+  int wave_buf, wave_n;
+  bool child_sm;  // sm.child holds the child record
+  int64_t init_target, attempt_cap, attempts, combo, chunk;
+};
+
+__device__ __forceinline__ void ga_load(const GaRun* R, GaHot& h) {
+  h.rng = ga_ld_rng(&R->rng);
+  h.used = __ldcg(&R->used);
+  h.streak = __ldcg(&R->streak);
+  h.seq = __ldcg(&R->seq);
+  h.best = __ldcg(&R->best);
+  h.best_member_cost = __ldcg(&R->best_member_cost);
+  h.n_pop = __ldcg(&R->n_pop);
+  h.state = __ldcg(&R->state);
+  h.have_spec = __ldcg(&R->have_spec);
+  h.best_member_flags = __ldcg(&R->best_member_flags);
+  h.impr_flags = __ldcg(&R->impr_flags);
+  h.child_buf = __ldcg(&R->child_buf);
+  h.child_idx = __ldcg(&R->child_idx);
+  h.child_cost = __ldcg(&R->child_cost);
+  h.n3 = __ldcg(&R->n3);
+  h.n5 = __ldcg(&R->n5);
+  h.m5 = __ldcg(&R->m5);
+  h.before3 = ga_ld_rng(&R->before3);
+  h.before5 = ga_ld_rng(&R->before5);
+  h.b5 = ga_ld_rng(&R->b5);
+  h.n_offspring = __ldcg(&R->n_offspring);
+  h.n_waves = __ldcg(&R->n_waves);
+  h.n_evals = __ldcg(&R->n_evals);
+  h.impr_time = __ldcg(&R->impr_time);
+  h.wave_buf = __ldcg(&R->wave_buf);
+  h.wave_n = __ldcg(&R->wave_n);
+  h.child_sm = false;
+  h.init_target = __ldcg(&R->init_target);
+  h.attempt_cap = __ldcg(&R->attempt_cap);
+  h.attempts = __ldcg(&R->attempts);
+  h.combo = __ldcg(&R->combo);
+  h.chunk = __ldcg(&R->chunk);
+}
+
+__device__ __forceinline__ void ga_store(GaRun* R, const GaHot& h) {
+  if ((threadIdx.x & 31) == 0) {
+    R->rng = h.rng;
+    R->used = h.used;
+    R->streak = h.streak;
+    R->seq = h.seq;
+    R->best = h.best;
+    R->best_member_cost = h.best_member_cost;
+    R->n_pop = h.n_pop;
+    R->state = h.state;
+    R->have_spec = h.have_spec;
+    R->best_member_flags = h.best_member_flags;
+    R->impr_flags = h.impr_flags;
+    R->child_buf = h.child_buf;
+    R->child_idx = h.child_idx;
+    R->child_cost = h.child_cost;
+    R->n3 = h.n3;
+    R->n5 = h.n5;
+    R->m5 = h.m5;
+    R->before3 = h.before3;
+    R->before5 = h.before5;
+    R->b5 = h.b5;
+    R->n_offspring = h.n_offspring;
+    R->n_waves = h.n_waves;
+    R->n_evals = h.n_evals;
+    R->impr_time = h.impr_time;
+    R->wave_buf = h.wave_buf;
+    R->wave_n = h.wave_n;
+    R->attempts = h.attempts;
+    R->combo = h.combo;
+    R->chunk = h.chunk;
+  }
+  __syncwarp();
+}
+
+// the population to / from shared memory (pop_slot in full: the free slots
+// past n_pop are used by insertions)
+__device__ __forceinline__ void ga_pop_load(const GaView& v, const GaHot& h) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < c_ga.pop_cap; i += 32) {
+    v.sm.pslot[i] = __ldcg(&v.R->pop_slot[i]);
+    if (i < h.n_pop) {
+      v.sm.pcost[i] = __ldcg(&v.R->pop_cost[i]);
+      v.sm.pseq[i] = __ldcg(&v.R->pop_seq[i]);
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void ga_pop_store(const GaView& v, const GaHot& h) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < c_ga.pop_cap; i += 32) {
+    v.R->pop_slot[i] = v.sm.pslot[i];
+    if (i < h.n_pop) {
+      v.R->pop_cost[i] = v.sm.pcost[i];
+      v.R->pop_seq[i] = v.sm.pseq[i];
+    }
+  }
+  __syncwarp();
+}
+
+// the finished wave's results to shared memory
+__device__ __forceinline__ void ga_res_load(const GaView& v, const GaHot& h) {
+  const int lane = threadIdx.x & 31;
+  const double2* s = reinterpret_cast<const double2*>(
+      c_ga.res + static_cast<int64_t>(v.run) * c_ga.res_per_run + h.wave_buf * c_ga.max_wave);
+  double2* d = reinterpret_cast<double2*>(v.sm.res);
+  for (int i = lane; i < 2 * h.wave_n; i += 32) d[i] = __ldcg(s + i);
+  __syncwarp();
+}
+
+// score (search.cpp:454-461): one budget unit; a new run best is an improvement
+__device__ void ga_score(const GaView& v, GaHot& h, const uint8_t* rec_g, double cost) {
+  ++h.used;
+  if (cost < h.best) {
+    h.best = cost;
+    h.impr_time = ga_timer();
+    if ((threadIdx.x & 31) == 0) {
+      const unsigned long long k = atomicAdd(&c_ga.ctl[kGaCtlImpr], 1ull);
+      if (static_cast<int64_t>(k) < c_ga.impr_cap)
+        c_ga.impr[k] = GaImpr{v.run, 0, h.used, cost, h.impr_time};
+    }
+    h.impr_time = __shfl_sync(0xffffffffu, h.impr_time, 0);
+    ga_rec_copy(v.slot(1), rec_g);
+    h.impr_flags |= 1;
+  }
+}
+
+__device__ __forceinline__ void ga_child_to_sm(const GaView& v, GaHot& h) {
+  if (!h.child_sm) {
+    ga_ld_rec(v.sm.child, v.wave_slot(h.child_buf, h.child_idx), v.stride);
+    h.child_sm = true;
+  }
+}
+
+// insert_member (search.cpp:462-470), kept sorted by (cost, insertion seq)
+__device__ void ga_insert(const GaView& v, GaHot& h) {
+  const int lane = threadIdx.x & 31;
+  const int P = c_ga.pop_cap;
+  const double cost = h.child_cost;
+  ga_child_to_sm(v, h);
+  if (cost < h.best_member_cost) {
+    h.best_member_cost = cost;
+    ga_st_rec(v.slot(0), v.sm.child);
+    h.best_member_flags = 3;
+  }
+  const uint64_t seq = static_cast<uint64_t>(h.seq++);
+  int pos = 0;
+  while (pos < h.n_pop && !(cost < v.sm.pcost[pos])) ++pos;
+  const int last = h.n_pop < P ? h.n_pop : P - 1;
+  const int slot = v.sm.pslot[last];
+  for (int i = last; i > pos; --i) {
+    if (lane == 0) {
+      v.sm.pslot[i] = v.sm.pslot[i - 1];
+      v.sm.pcost[i] = v.sm.pcost[i - 1];
+      v.sm.pseq[i] = v.sm.pseq[i - 1];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    v.sm.pslot[pos] = slot;
+    v.sm.pcost[pos] = cost;
+    v.sm.pseq[pos] = seq;
+  }
+  __syncwarp();
+  if (h.n_pop < P) ++h.n_pop;
+  ga_st_rec(v.slot(slot), v.sm.child);
+}
+
+__device__ __forceinline__ void ga_insert_if(const GaView& v, GaHot& h) {
+  if (h.n_pop < c_ga.pop_cap || h.child_cost < v.sm.pcost[h.n_pop - 1]) ga_insert(v, h);
+}
+
+// speculative next mutation stage from state r, assuming the child is
+// inserted as it stands (search.cpp ga_run: same parent draw)
+__device__ void ga_speculate(const GaView& v, GaHot& h, const Rng& r, int buf, int base) {
+  const int P = c_ga.pop_cap;
+  const double cc = h.child_cost;
+  const bool ins = h.n_pop < P || cc < v.sm.pcost[h.n_pop - 1];
+  int pos = h.n_pop, n_spec = h.n_pop;
+  if (ins) {
+    pos = 0;
+    while (pos < h.n_pop && !(v.sm.pcost[pos] > cc)) ++pos;
+    n_spec = h.n_pop + 1 < P ? h.n_pop + 1 : P;
+  }
+  Rng rr = r;
+  const int i = static_cast<int>(GA_BOUNDED(rr, static_cast<uint64_t>(n_spec)));
+  const uint8_t* parent;
+  if (!ins || i < pos || i > pos) {
+    ga_ld_rec(v.sm.par, v.slot(v.sm.pslot[!ins || i < pos ? i : i - 1]), v.stride);
+    parent = v.sm.par;
+  } else {
+    ga_child_to_sm(v, h);
+    parent = v.sm.child;
+  }
+  ga_draw_mut(v, rr, parent, &v.R->spec, buf, base);
+  ga_st_rng(&v.R->spec.start, r);
+  __syncwarp();
+}
+
+// swap trials at one level from the child (search.cpp:534-558 draw loop)
+__device__ int ga_draw(const GaView& v, GaHot& h, int level, int buf, int at, Rng* sn) {
+  const int lane = threadIdx.x & 31;
+  ga_child_to_sm(v, h);
+  GaSrcInfo si;
+  ga_src_info(v, v.sm.child, si);
+  const bool ok = level == 3 ? v.ng >= 2 : si.ne > 0;
+  if (!ok || c_ga.sps <= 0) return 0;  // random_move fails before any draw
+  const int n = c_ga.sps, per = level == 3 ? 4 : 3;
+  int np = 0, pp[kGaMaxPatch], pv[kGaMaxPatch];
+  Rng mine = h.rng;
+  if (lane < n) {
+    for (int k = 0; k < per * lane; ++k) mine.next();
+    np = ga_lane_move(v, v.sm.child, si, level, mine, pp, pv);
+    sn[lane] = mine;
+  }
+  __syncwarp();
+  ga_emit_all(v, buf, at, n, v.sm.child, si.geo.dev_byte, np, pp, pv);
+  // the stream after the last trial
+  h.rng.seed = __shfl_sync(0xffffffffu, mine.seed, n - 1);
+  for (int k = 0; k < 4; ++k) h.rng.s[k] = __shfl_sync(0xffffffffu, mine.s[k], n - 1);
+  return n;
+}
+
+// the sequential trial walk over scored trials [b, b + n) of the finished
+// wave: 1 accepted (new child), 2 budget stop, 0 ran out
+__device__ int ga_walk(const GaView& v, GaHot& h, int b, int n, const Rng& before, const Rng* sn) {
+  const int64_t slice = __ldcg(&v.R->slice);
+  for (int t = 0; t < n; ++t) {
+    if (h.used >= slice) {
+      h.rng = t == 0 ? before : ga_ld_rng(&sn[t - 1]);
+      return 2;
+    }
+    const EvalResult& e = v.sm.res[b + t];
+    if (!(e.flags & kResFeasIn)) continue;
+    const double c2 = e.cost;
+    ga_score(v, h, v.wave_slot(h.wave_buf, b + t), c2);
+    if (c2 < h.child_cost) {
+      h.child_buf = h.wave_buf;
+      h.child_idx = b + t;
+      h.child_cost = c2;
+      h.child_sm = false;
+      h.rng = ga_ld_rng(&sn[t]);
+      return 1;
+    }
+  }
+  if (n > 0) h.rng = ga_ld_rng(&sn[n - 1]);
+  return 0;
+}
+
+// publishes evaluation tasks (run, i) for i in [i0, i1)
+__device__ void ga_publish(int run, int i0, int i1) {
+  const int lane = threadIdx.x & 31;
+  const int n = i1 - i0;
+  if (n <= 0) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&c_ga.ctl[kGaCtlTail], static_cast<unsigned long long>(n));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int k = lane; k < n; k += 32) {
+    const unsigned long long t = base + k;
+    c_ga.q_pay[t & c_ga.q_mask] = make_uint2(static_cast<unsigned>(run), static_cast<unsigned>(i0 + k));
+    __threadfence();
+    atomicExch(&c_ga.q_seq[t & c_ga.q_mask], t + 1);
+  }
+  __syncwarp();
+}
+
+// diagnostics: sub-phase cycles of a GA step (ctl words 100..107)
+#define GA_PH(slot, expr)                                                         \
+  do {                                                                            \
+    const long long ph0_ = c_ga.prof ? clock64() : 0;                               \
+    expr;                                                                         \
+    if (c_ga.prof && (threadIdx.x & 31) == 0)                                        \
+      atomicAdd(&c_ga.ctl[100 + (slot)], static_cast<unsigned long long>(clock64() - ph0_)); \
+  } while (0)
+
+// one GA step of run r: runs the state machine until it needs a wave (returns
+// the index of the wave's candidate this warp evaluates itself) or the run
+// ends (returns -1)
+__device__ int ga_step(int r, const GaSm& sm) {
+  GaRun* R = c_ga.runs + r;
+  GaView v;
+  v.R = R;
+  v.run = r;
+  v.pool = c_ga.pool + __ldcg(&R->pool_off);
+  v.stride = __ldcg(&R->rec_stride);
+  v.ng = __ldcg(&R->ng);
+  for (int k = 0; k <= kMaxTasks; ++k) v.gstart[k] = __ldcg(&R->gstart[k]);
+  for (int k = 0; k < kMaxTasks; ++k) v.gslot[k] = __ldcg(&R->gslot[k]);
+  for (int k = 0; k < kMaxTasks; ++k) v.counts[k] = __ldcg(&R->counts[k]);
+  for (int k = 0; k <= kMaxTasks; ++k) v.opt_off[k] = __ldcg(&R->opt_off[k]);
+  v.opt_base = __ldcg(&R->opt_base);
+  v.sm = sm;
+  const int64_t slice = __ldcg(&R->slice);
+  GaHot h;
+  GA_PH(0, ga_load(R, h); ga_pop_load(v, h);
+        if (h.state != kGaLoop && h.state != kGaInit && h.state != kGaInitDone) ga_res_load(v, h));
+  auto submit = [&](int buf, int n) {
+    h.wave_buf = buf;
+    h.wave_n = n;
+    ++h.n_waves;
+    h.n_evals += n;
+    GA_PH(1, ga_pop_store(v, h); ga_store(R, h); if ((threadIdx.x & 31) == 0) R->pending = n;
+          __threadfence(); __syncwarp(); ga_publish(r, 0, n - 1));
+    return n - 1;
+  };
+  auto finish = [&]() {
+    h.state = kGaDone;
+    ga_pop_store(v, h);
+    ga_store(R, h);
+    __threadfence();
+    if ((threadIdx.x & 31) == 0) {
+      const unsigned long long d = atomicAdd(&c_ga.ctl[kGaCtlDone], 1ull) + 1;
+      if (d == static_cast<unsigned long long>(c_ga.n_runs)) atomicExch(&c_ga.ctl[kGaCtlStop], 1ull);
+    }
+    __syncwarp();
+    return -1;
+  };
+  while (true) {
+    if (h.state == kGaInit) {
+      // init: cycle layout combinations in doubling chunks until init_target
+      // members (search.cpp:437-450 as restated in ga_run)
+      if (!(h.n_pop < h.init_target && h.used < slice && h.attempts < h.attempt_cap)) {
+        if (h.n_pop == 0) return finish();
+        h.state = kGaLoop;
+        continue;
+      }
+      const int64_t need = h.init_target - h.n_pop;
+      const int64_t grow = h.chunk * 2 > 2 * need + 2 ? h.chunk * 2 : 2 * need + 2;
+      h.chunk = h.attempt_cap - h.attempts < grow ? h.attempt_cap - h.attempts : grow;
+      GA_PH(8, ga_init_chunk(v, h.rng, h.combo, static_cast<int>(h.chunk)));
+      if (c_ga.prof && (threadIdx.x & 31) == 0) {
+        atomicAdd(&c_ga.ctl[109], 1ull);
+        atomicAdd(&c_ga.ctl[110], static_cast<unsigned long long>(h.chunk));
+      }
+      h.state = kGaInitDone;
+      return submit(0, static_cast<int>(h.chunk));
+    }
+    if (h.state == kGaInitDone) {
+      const int lane = threadIdx.x & 31;
+      const int n = h.wave_n;
+      const int64_t combo0 = h.combo;
+      h.combo += n;
+      const Rng* snaps = c_ga.init_snaps + static_cast<int64_t>(r) * c_ga.init_cap;
+      h.rng = ga_ld_rng(&snaps[n - 1]);
+      const EvalResult* res = c_ga.res + static_cast<int64_t>(r) * c_ga.res_per_run;
+      bool stop = false;
+      for (int b = 0; b < n && !stop; b += 32) {
+        int fl = 0;
+        double co = 0.0;
+        if (b + lane < n) {
+          fl = __ldcg(&res[b + lane].flags);
+          co = __ldcg(&res[b + lane].cost);
+        }
+        for (int j = 0; j < 32 && b + j < n; ++j) {
+          const int f = __shfl_sync(0xffffffffu, fl, j);
+          const double cj = __shfl_sync(0xffffffffu, co, j);
+          ++h.attempts;
+          if (!(f & kResFeasIn)) continue;
+          const int c = b + j;
+          ga_score(v, h, v.wave_slot(0, c), cj);
+          h.child_buf = 0;
+          h.child_idx = c;
+          h.child_cost = cj;
+          h.child_sm = false;
+          ga_insert(v, h);
+          if (h.n_pop >= h.init_target) {
+            h.rng = ga_ld_rng(&snaps[c]);
+            h.combo = combo0 + c + 1;
+            stop = true;
+            break;
+          }
+        }
+      }
+      h.state = kGaInit;
+      continue;
+    }
+    if (h.state == kGaLoop) {
+      if (!(h.used < slice && h.streak < kGaStreakCap)) return finish();
+      ++h.n_offspring;
+      if (h.have_spec && ga_same_rng(ga_ld_rng(&R->spec.start), h.rng)) {
+        // the speculative stage drawn with the finished wave is this one
+        const int4* s = reinterpret_cast<const int4*>(&R->spec);
+        int4* d = reinterpret_cast<int4*>(&R->cur);
+        const int lane = threadIdx.x & 31;
+        for (int i = lane; i < static_cast<int>(sizeof(GaStage) / 16); i += 32) d[i] = __ldcg(s + i);
+        __syncwarp();
+        h.have_spec = 0;
+        h.state = kGaMut;
+        continue;
+      }
+      h.have_spec = 0;
+      Rng r2 = h.rng;
+      const int i = static_cast<int>(GA_BOUNDED(r2, static_cast<uint64_t>(h.n_pop)));
+      GA_PH(6, ga_ld_rec(sm.par, v.slot(sm.pslot[i]), v.stride);
+            ga_draw_mut(v, r2, sm.par, &R->cur, 0, 0));
+      h.state = kGaMut;
+      return submit(0, __ldcg(&R->cur.ntr) + 1);
+    }
+    if (h.state == kGaMut) {
+      // the stage's results are in sm.res (its wave just finished)
+      const int buf = __ldcg(&R->cur.buf), base = __ldcg(&R->cur.base), ntr = __ldcg(&R->cur.ntr);
+      int chosen = -1;
+      for (int i = 0; i < ntr; ++i)
+        if (sm.res[base + i].flags & kResFeasIn) {
+          chosen = i;
+          break;
+        }
+      if (chosen >= 0) {
+        h.rng = ga_ld_rng(&R->cur.snaps[chosen]);
+        h.child_idx = base + chosen;
+      } else {
+        h.rng = ga_ld_rng(&R->cur.after_all);
+        if (!(sm.res[base + ntr].flags & kResFeasIn)) {
+          ++h.streak;
+          h.state = kGaLoop;
+          continue;
+        }
+        h.child_idx = base + ntr;
+      }
+      h.child_buf = buf;
+      h.child_sm = false;
+      h.child_cost = sm.res[h.child_idx].cost;
+      h.streak = 0;
+      GA_PH(7, ga_score(v, h, v.wave_slot(buf, h.child_idx), h.child_cost));
+      if (h.used < slice) {
+        const int wb = 1 - h.child_buf;
+        h.before3 = h.rng;
+        GA_PH(2, h.n3 = ga_draw(v, h, 3, wb, 0, R->snaps3));
+        h.before5 = h.rng;
+        GA_PH(2, h.n5 = ga_draw(v, h, 5, wb, h.n3, R->snaps5));
+        if (h.n3 + h.n5 > 0) {
+          const int base2 = h.n3 + h.n5;
+          const Rng from = h.n5 > 0 ? ga_ld_rng(&R->snaps5[h.n5 - 1]) : h.before5;
+          GA_PH(3, ga_speculate(v, h, from, wb, base2));
+          h.state = kGaSwap;
+          return submit(wb, base2 + __ldcg(&R->spec.ntr) + 1);
+        }
+        h.rng = h.before5;
+      }
+      GA_PH(5, ga_insert_if(v, h));
+      h.state = kGaLoop;
+      continue;
+    }
+    if (h.state == kGaSwap) {
+      h.rng = h.before5;
+      int w3 = 0;
+      GA_PH(4, w3 = ga_walk(v, h, 0, h.n3, h.before3, R->snaps3));
+      if (w3 == 0 && h.used < slice) {
+        h.rng = h.before5;
+        if (ga_walk(v, h, h.n3, h.n5, h.before5, R->snaps5) == 0) h.have_spec = 1;
+      } else if (w3 == 1 && h.used < slice) {
+        const int wb2 = 1 - h.wave_buf;
+        h.b5 = h.rng;
+        h.m5 = ga_draw(v, h, 5, wb2, 0, R->snaps5);
+        if (h.m5 > 0) {
+          ga_speculate(v, h, ga_ld_rng(&R->snaps5[h.m5 - 1]), wb2, h.m5);
+          h.state = kGaRedraw;
+          return submit(wb2, h.m5 + __ldcg(&R->spec.ntr) + 1);
+        }
+      }
+      ga_insert_if(v, h);
+      h.state = kGaLoop;
+      continue;
+    }
+    if (h.state == kGaRedraw) {
+      if (ga_walk(v, h, 0, h.m5, h.b5, R->snaps5) == 0) h.have_spec = 1;
+      ga_insert_if(v, h);
+      h.state = kGaLoop;
+      continue;
+    }
+    return -1;  // kGaDone: not reached
+  }
+}
+
+// canonical bytes of one plan (engine.cpp wave_stage)
+__device__ __forceinline__ long long ga_canonical(const DevProblem& P, const uint8_t* rec, int ng) {
+  const int32_t* h = reinterpret_cast<const int32_t*>(rec);
+  long long cb = 1 + ng + 9;
+  int sw = 0, wg = 0;
+  for (int t = 0; t < P.n_tasks; ++t) {
+    const int dp = __ldcg(h + 2 + t), pp = __ldcg(h + 2 + kMaxTasks + t),
+              tp = __ldcg(h + 2 + 2 * kMaxTasks + t);
+    cb += 3 + pp + dp * pp * tp;
+    if (t == P.gen_slot) wg = sw;
+    sw += dp;
+  }
+  if (P.gen_slot >= 0) {
+    const int dpg = __ldcg(h + 2 + P.gen_slot);
+    const double* w = reinterpret_cast<const double*>(rec + sizeof(RecHeader)) + wg;
+    bool unit = true;
+    for (int k = 0; k < dpg; ++k)
+      if (__ldcg(w + k) != 1.0) unit = false;
+    if (!unit) cb += 8 * dpg;
+  }
+  return cb;
+}
+
+__global__ void __launch_bounds__(32, 16)
+ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscratch,
+          int64_t gscratch_doubles) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ Ws team[1];
+  const int lane = threadIdx.x & 31;
+  GaSm sm;
+  {
+    // GA scratch after the evaluation carve (launch_ga_offspring sizes it)
+    uint8_t* p = smem + carve2_bytes(cv);
+    const int stride = c_ga.max_stride;
+    sm.child = p;
+    sm.par = p + stride;
+    sm.tmp = p + 2 * stride;
+    sm.res = reinterpret_cast<EvalResult*>(p + 3 * stride);
+    sm.pcost = reinterpret_cast<double*>(p + 3 * stride + 32 * c_ga.max_wave);
+    sm.pseq = reinterpret_cast<uint64_t*>(sm.pcost + kGaMaxPop);
+    sm.pslot = reinterpret_cast<int32_t*>(sm.pseq + kGaMaxPop);
+    sm.gw = reinterpret_cast<uint32_t*>(sm.pslot + kGaMaxPop);
+    sm.gen = smem;
+  }
+  if (lane == 0) {
+    Ws& l = team[0];
+    carve(l, smem, cv);
+    l.dtab = gscratch + static_cast<int64_t>(blockIdx.x) * gscratch_doubles;
+    l.dtab_stride = 0;
+    l.prof = nullptr;
+    l.team = team;
+    l.n_warps = 1;
+    l.job_words[0] = l.job_words[1] = 0;
+    l.job = l.job_words;
+    l.cls = P.cls;
+    if (blockIdx.x == 0) atomicCAS(&c_ga.ctl[kGaCtlT0], 0ull, ga_timer());
+  }
+  __syncwarp();
+  Ws& s = team[0];
+  while (true) {
+    // take a ticket, wait for its task (or for the end of the launch)
+    unsigned long long t = 0;
+    uint2 pay = make_uint2(0, 0);
+    int stop = 0;
+    if (lane == 0) {
+      t = atomicAdd(&c_ga.ctl[kGaCtlHead], 1ull);
+      volatile unsigned long long* seq = c_ga.q_seq + (t & c_ga.q_mask);
+      volatile unsigned long long* stopw = c_ga.ctl + kGaCtlStop;
+      unsigned ns = 32;
+      while (*seq != t + 1) {
+        if (*stopw) {
+          stop = 1;
+          break;
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+      }
+      if (!stop) {
+        __threadfence();
+        pay = __ldcg(c_ga.q_pay + (t & c_ga.q_mask));
+      }
+    }
+    stop = __shfl_sync(0xffffffffu, stop, 0);
+    if (stop) break;
+    int run = static_cast<int>(__shfl_sync(0xffffffffu, pay.x, 0));
+    int idx = static_cast<int>(__shfl_sync(0xffffffffu, pay.y, 0));
+    while (true) {
+      if (idx < 0) {  // GA step
+        const long long c0 = c_ga.prof ? clock64() : 0;
+        idx = ga_step(run, sm);
+        if (c_ga.prof && lane == 0) {
+          atomicAdd(&c_ga.ctl[kGaCtlProf], static_cast<unsigned long long>(clock64() - c0));
+          atomicAdd(&c_ga.ctl[kGaCtlProf + 1], 1ull);
+        }
+        if (idx < 0) break;
+        continue;
+      }
+      const long long c1 = c_ga.prof ? clock64() : 0;
+      GaRun* R = c_ga.runs + run;
+      const int buf = __ldcg(&R->wave_buf);
+      uint8_t* rec = c_ga.pool + __ldcg(&R->pool_off) +
+                     static_cast<int64_t>(2 + c_ga.pop_cap + buf * c_ga.max_wave + idx) *
+                         __ldcg(&R->rec_stride);
+      long long cb = 0;
+      if (lane == 0) cb = ga_canonical(P, rec, __ldcg(&R->ng));
+      const EvalResult e = eval_one(P, cfg, s, c_ga.kb_flags, rec, kModeEvaluate, nullptr, nullptr,
+                                    nullptr, nullptr, rec);
+      int last = 0;
+      if (lane == 0) {
+        c_ga.res[static_cast<int64_t>(run) * c_ga.res_per_run + buf * c_ga.max_wave + idx] = e;
+        atomicAdd(&c_ga.ctl[kGaCtlEvals], 1ull);
+        atomicAdd(&c_ga.ctl[kGaCtlBytes], static_cast<unsigned long long>(cb));
+        __threadfence();
+        last = atomicSub(&R->pending, 1) == 1;
+        if (last) __threadfence();
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (c_ga.prof && lane == 0) {
+        atomicAdd(&c_ga.ctl[kGaCtlProf + 2], static_cast<unsigned long long>(clock64() - c1));
+        atomicAdd(&c_ga.ctl[kGaCtlProf + 3], 1ull);
+      }
+      if (!last) break;
+      idx = -1;  // this warp finished the wave: continue the run
+    }
+  }
+}
+
+}  // namespace dev
+
+cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
+                                const GaParams& G, double* gscratch, int64_t gscratch_doubles,
+                                int n_sm, int& grid, cudaStream_t st) {
+  cv.cls_smem = 0;
+  cv.n_warps = 1;
+  cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave);
+  static int configured = 0;
+  if (cv.bytes > configured) {
+    const cudaError_t e = cudaFuncSetAttribute(
+        dev::ga_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
+    if (e != cudaSuccess) return e;
+    configured = cv.bytes;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::ga_kernel, 32, cv.bytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  grid = n_sm * per_sm;
+  e = cudaMemcpyToSymbolAsync(dev::c_ga, &G, sizeof(GaParams), 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  dev::ga_kernel<<<grid, 32, cv.bytes, st>>>(P, cfg, cv, gscratch, gscratch_doubles);
+  return cudaGetLastError();
+}
+
+}  // namespace hpg

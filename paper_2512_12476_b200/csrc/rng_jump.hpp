@@ -1,0 +1,137 @@
+// xoshiro256 jump-ahead by an arbitrary count (host side): the transition is
+// linear over GF(2); its characteristic polynomial p (degree 256) comes from
+// Berlekamp-Massey on one output bit, and advancing a state by D steps is
+// q(T) applied to it, q = x^D mod p (the construction behind xoshiro's own
+// jump()). Used to give each lane of a device GA init chunk its candidate's
+// start state (ga_kernel.cuh ga_init_chunk).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "rng.hpp"
+
+namespace hpg {
+
+using Poly256 = std::array<uint64_t, 4>;  // coefficients of x^0..x^255
+
+namespace jump_detail {
+
+inline uint64_t bit(const uint64_t* w, int i) { return (w[i >> 6] >> (i & 63)) & 1u; }
+
+// low 256 coefficients of p (p = x^256 + ...)
+inline const Poly256& charpoly() {
+  static const Poly256 p = [] {
+    // 512 terms of one output bit of the state sequence
+    Rng r(0x9E3779B97F4A7C15ull);
+    std::vector<uint8_t> sq(512);
+    for (int i = 0; i < 512; ++i) {
+      sq[i] = static_cast<uint8_t>(r.s[0] & 1u);
+      r.next();
+    }
+    // Berlekamp-Massey over GF(2): connection polynomial C (C[0] = 1)
+    std::vector<uint8_t> C(513, 0), B(513, 0), T;
+    C[0] = B[0] = 1;
+    int L = 0, m = 1;
+    for (int n = 0; n < 512; ++n) {
+      uint8_t d = sq[n];
+      for (int i = 1; i <= L; ++i) d ^= C[i] & sq[n - i];
+      if (!d) {
+        ++m;
+        continue;
+      }
+      T = C;
+      for (int i = 0; i + m <= 512; ++i) C[i + m] ^= B[i];
+      if (2 * L <= n) {
+        L = n + 1 - L;
+        B = T;
+        m = 1;
+      } else {
+        ++m;
+      }
+    }
+    // the characteristic polynomial is the reciprocal of C: p_i = C[L - i]
+    Poly256 out{0, 0, 0, 0};
+    if (L != 256) return out;  // never: xoshiro256's polynomial is primitive
+    for (int i = 0; i < 256; ++i)
+      if (C[256 - i]) out[i >> 6] |= 1ull << (i & 63);
+    return out;
+  }();
+  return p;
+}
+
+// a * b mod p
+inline Poly256 mulmod(const Poly256& a, const Poly256& b) {
+  uint64_t prod[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < 256; ++i) {
+    if (!bit(a.data(), i)) continue;
+    // prod ^= b << i
+    const int w = i >> 6, s = i & 63;
+    for (int k = 0; k < 4; ++k) {
+      prod[k + w] ^= b[k] << s;
+      if (s) prod[k + w + 1] ^= b[k] >> (64 - s);
+    }
+  }
+  const Poly256& p = charpoly();
+  for (int i = 511; i >= 256; --i) {
+    if (!bit(prod, i)) continue;
+    // x^i = x^(i-256) * (p - x^256): clear bit i, xor p << (i - 256)
+    prod[i >> 6] &= ~(1ull << (i & 63));
+    const int sh = i - 256, w = sh >> 6, s = sh & 63;
+    for (int k = 0; k < 4; ++k) {
+      prod[k + w] ^= p[k] << s;
+      if (s) prod[k + w + 1] ^= p[k] >> (64 - s);
+    }
+  }
+  return Poly256{prod[0], prod[1], prod[2], prod[3]};
+}
+
+}  // namespace jump_detail
+
+// x^D mod p
+inline Poly256 jump_poly(uint64_t D) {
+  Poly256 r{1, 0, 0, 0}, base{2, 0, 0, 0};  // 1 and x
+  while (D) {
+    if (D & 1) r = jump_detail::mulmod(r, base);
+    base = jump_detail::mulmod(base, base);
+    D >>= 1;
+  }
+  return r;
+}
+
+// the state advanced by q(T) (q = jump_poly(D) advances D steps)
+HPG_HD void rng_apply_jump(Rng& r, const uint64_t* q) {
+  uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  for (int i = 0; i < 256; ++i) {
+    if ((q[i >> 6] >> (i & 63)) & 1u) {
+      a0 ^= r.s[0];
+      a1 ^= r.s[1];
+      a2 ^= r.s[2];
+      a3 ^= r.s[3];
+    }
+    r.next();
+  }
+  r.s[0] = a0;
+  r.s[1] = a1;
+  r.s[2] = a2;
+  r.s[3] = a3;
+}
+
+// x^(L*D) mod p for L = 1..n (cached per D, process-wide)
+inline const std::vector<Poly256>& jump_table(uint64_t D, int n) {
+  static std::mutex m;
+  static std::map<uint64_t, std::vector<Poly256>> cache;
+  std::lock_guard<std::mutex> lk(m);
+  std::vector<Poly256>& v = cache[D];
+  if (static_cast<int>(v.size()) < n) {
+    const Poly256 q = jump_poly(D);
+    if (v.empty()) v.push_back(q);
+    while (static_cast<int>(v.size()) < n) v.push_back(jump_detail::mulmod(v.back(), q));
+  }
+  return v;
+}
+
+}  // namespace hpg

@@ -17,6 +17,7 @@
 
 #include "eval_launch.hpp"
 #include "host_pool.hpp"
+#include "rng_jump.hpp"
 
 namespace hpg {
 
@@ -497,6 +498,12 @@ struct Improvement {
   double t_wall;
 };
 
+struct Member {
+  Cand plan;
+  double cost;
+  uint64_t seq;
+};
+
 struct ArmRun {
   int64_t ti = 0, gi = 0;
   int64_t slice = 0;
@@ -516,6 +523,11 @@ struct ArmRun {
   double t_make = 0, t_mut = 0, t_swap = 0, t_spec = 0;  // diagnostics (s)
   int64_t w_init = 0, w_mut = 0, w_swap = 0, w_redraw = 0;  // diagnostics: waves by kind
   int64_t n_make = 0;
+  // population (ga_run's locals, kept here so the device can take over)
+  std::vector<Member> pop;
+  uint64_t seq = 0;
+  bool device_ga = false;  // hand the offspring loop to ga_kernel after init
+  bool handoff = false;
 };
 
 // ga_run (search.cpp:437-565) as a coroutine.
@@ -526,13 +538,12 @@ ArmCoro ga_run(ArmRun& run) {
   const int64_t slice = run.slice;
   if (slice <= 0) co_return;
   if (!e.al.feasible) co_return;
-  struct Member {
-    Cand plan;
-    double cost;
-    uint64_t seq;
-  };
-  std::vector<Member> pop;
-  uint64_t seq = 0;
+  if (run.device_ga) {  // the whole run goes to the device (ga_kernel.cuh)
+    run.handoff = true;
+    co_return;
+  }
+  std::vector<Member>& pop = run.pop;
+  uint64_t& seq = run.seq;
   auto score = [&](const Cand& c, double cost) {
     ++run.used;
     if (cost < run.best) {
@@ -783,18 +794,339 @@ ArmCoro ga_run(ArmRun& run) {
   }
 }
 
+// ga_run of every run of a lockstep round on the device, in one persistent
+// launch (ga_kernel.cuh): init chunks, offspring, speculation. The host
+// hands over the arm (layout options, groups, RNG stream, slice) and gets
+// back the run's budget use, best, improvements and best member, exactly as
+// the coroutine would have left them.
+bool device_ga_enabled(const Knobs& K) {
+  static const int env = [] {
+    const char* v = std::getenv("HPG_DEVICE_GA");  // 0 = host GA (lockstep waves)
+    return v ? std::atoi(v) : 1;
+  }();
+  return env != 0 && K.population >= 1 && K.population <= kGaMaxPop &&
+         K.swap_pair_sample >= 0 && K.swap_pair_sample <= kGaMaxSps;
+}
+
+void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, double& clock,
+               int64_t& waves) {
+  const int n = static_cast<int>(runs.size());
+  if (n == 0) return;
+  const double t_prep0 = now_s();
+  const Problem& P = ctx.prob;
+  const DevCostConfig cfg = K.cost_config();
+  const GenTablesDev& gt = gen_tables(ctx);
+  const int kb = (K.balance_data ? 1 : 0) | (K.balance_layers ? 2 : 0);
+  const int pop_cap = K.population, sps = K.swap_pair_sample;
+  const int max_wave = 2 * sps + kGaTrials + 1;
+  std::vector<int> nodes_per_region;
+  for (const auto& rn : P.region_nodes) nodes_per_region.push_back(static_cast<int>(rn.size()));
+  // per run: layout options, record bound, init sizes; shared slot stride
+  Carve cv{};
+  cv.n_dev = P.N;
+  cv.n_tasks = P.T;
+  int stride = 16;
+  int init_cap = 1;
+  int64_t remaining = 0;
+  std::vector<short4> opts;
+  std::vector<Poly256> jumps;
+  std::map<int32_t, int32_t> jump_at;  // gen_draws -> first polynomial
+  std::vector<GaRun> gr(n);
+  for (int i = 0; i < n; ++i) {
+    const ArmRun& r = *runs[i];
+    const ArmEnv& e = *r.env;
+    GaRun& g = gr[i];
+    std::memset(static_cast<void*>(&g), 0, sizeof(g));
+    g.slice = r.slice;
+    g.ng = static_cast<int32_t>(e.tg.size());
+    int k = 0, mw = 0, msl = 0, mslots = 0, mcells = 0, mdpk = 0, mrec = 0;
+    g.opt_base = static_cast<int64_t>(opts.size());
+    for (size_t gi = 0; gi < e.tg.size(); ++gi) {
+      g.gstart[gi] = k;
+      g.counts[gi] = e.counts[gi];
+      for (int s : e.tg[gi]) {
+        g.gslot[k] = s;
+        g.opt_off[k] = static_cast<int32_t>(opts.size() - g.opt_base);
+        int xdp = 0, xpp = 0, xcell = 0, xdpk = 0, xrec = 0;
+        for (const Layout& l : e.al.options[s]) {
+          opts.push_back(make_short4(static_cast<short>(l.dp), static_cast<short>(l.pp),
+                                     static_cast<short>(l.tp), 0));
+          xdp = std::max(xdp, l.dp);
+          xpp = std::max(xpp, l.pp);
+          xcell = std::max(xcell, l.dp * l.pp);
+          xdpk = std::max(xdpk, l.pp * l.tp);
+          xrec = std::max(xrec, 8 * l.dp + 4 * l.pp);
+        }
+        mw += xdp;
+        msl += xpp;
+        mcells += xcell;
+        mdpk += xdpk;
+        mrec += xrec;
+        mslots += e.counts[gi];
+        ++k;
+      }
+    }
+    g.gstart[e.tg.size()] = k;
+    g.opt_off[k] = static_cast<int32_t>(opts.size() - g.opt_base);
+    stride = std::max(stride, (static_cast<int>(sizeof(RecHeader)) + mrec + mslots + 15) & ~15);
+    cv.max_w = std::max(cv.max_w, mw);
+    cv.max_sl = std::max(cv.max_sl, msl);
+    cv.max_slots = std::max(cv.max_slots, mslots);
+    cv.max_cells = std::max(cv.max_cells, mcells);
+    cv.max_dpk = std::max(cv.max_dpk, mdpk);
+    g.gen_draws = static_cast<int32_t>(gen_draws_per_candidate(
+        P.N, nodes_per_region.data(), static_cast<int>(nodes_per_region.size()), gen_item_of(e)));
+    auto ja = jump_at.find(g.gen_draws);
+    if (ja == jump_at.end()) {
+      ja = jump_at.emplace(g.gen_draws, static_cast<int32_t>(jumps.size())).first;
+      const std::vector<Poly256>& tb = jump_table(static_cast<uint64_t>(g.gen_draws), 31);
+      jumps.insert(jumps.end(), tb.begin(), tb.begin() + 31);
+    }
+    g.jump_off = ja->second;
+    const int64_t it = std::max<int64_t>(
+        1, std::min({r.slice, static_cast<int64_t>(K.population), r.slice / 2}));
+    g.init_target = static_cast<int32_t>(it);
+    g.attempt_cap = 64 + 16 * it;
+    init_cap = std::max<int>(init_cap, static_cast<int>(g.attempt_cap));
+    g.rng = r.rng;
+    g.best = kInf;
+    g.best_member_cost = kInf;
+    g.state = kGaInit;
+    for (int m = 0; m < pop_cap; ++m) g.pop_slot[m] = 2 + m;
+    remaining += r.slice;
+  }
+  const int res_per_run = std::max(2 * max_wave, init_cap);
+  const int64_t gen_bytes =
+      (2 * (gt.n_regions + gt.max_nodes_per_region + 4 * gt.n_nodes) + 2 * gt.n_dev + 15) & ~15;
+  const int n_slots = 2 + pop_cap + res_per_run;
+  const int64_t run_bytes = static_cast<int64_t>(n_slots) * stride;
+  for (int i = 0; i < n; ++i) {
+    gr[i].pool_off = run_bytes * i;
+    gr[i].rec_stride = stride;
+  }
+  // work ring: at most one wave per run in flight plus the idle workers' tickets
+  const int max_workers = 16 * ctx.n_sm;
+  const int64_t want_q = 2 * (static_cast<int64_t>(n) * (res_per_run + 1) + 4 * max_workers);
+  uint64_t q_cap = 1024;
+  while (static_cast<int64_t>(q_cap) < want_q) q_cap <<= 1;
+  const int64_t impr_cap = std::max<int64_t>(1, remaining);
+  auto al = [](int64_t x) { return (x + 255) & ~int64_t(255); };
+  const int64_t o_runs = 0, o_pool = al(o_runs + static_cast<int64_t>(sizeof(GaRun)) * n),
+                o_res = al(o_pool + run_bytes * n),
+                o_qpay = al(o_res + static_cast<int64_t>(sizeof(EvalResult)) * n * res_per_run),
+                o_qseq = al(o_qpay + 8 * static_cast<int64_t>(q_cap)),
+                o_ctl = al(o_qseq + 8 * static_cast<int64_t>(q_cap)),
+                o_impr = al(o_ctl + 8 * kGaCtlWords),
+                o_rank = al(o_impr + static_cast<int64_t>(sizeof(GaImpr)) * impr_cap),
+                o_opts = al(o_rank + 8 * 256),
+                o_snaps = al(o_opts + 8 * static_cast<int64_t>(opts.size())),
+                o_gscr = al(o_snaps + static_cast<int64_t>(sizeof(Rng)) * n * init_cap),
+                o_jump = al(o_gscr + static_cast<int64_t>(max_workers) * 32 * gen_bytes),
+                d_total = al(o_jump + 32 * static_cast<int64_t>(jumps.size()));
+  // one generous allocation per context (reallocating inside a search is slow)
+  ctx.d_ga.reserve(std::max<int64_t>(d_total, int64_t{512} << 20));
+  uint8_t* D = ctx.d_ga.p;
+  // host staging: [runs | ctl | ranks | queue seeds | options], results reuse it
+  const int64_t h_runs = 0, h_ctl = al(sizeof(GaRun) * static_cast<int64_t>(n)),
+                h_rank = al(h_ctl + 8 * kGaCtlWords), h_qpay = al(h_rank + 8 * 256),
+                h_qseq = al(h_qpay + 8 * static_cast<int64_t>(n)),
+                h_opts = al(h_qseq + 8 * static_cast<int64_t>(n)),
+                h_jump = al(h_opts + 8 * static_cast<int64_t>(opts.size())),
+                h_best = al(h_jump + 32 * static_cast<int64_t>(jumps.size())),
+                h_imp = al(h_best + 2 * static_cast<int64_t>(stride) * n),
+                h_total = al(h_imp + static_cast<int64_t>(sizeof(GaImpr)) * impr_cap);
+  // staging sized generously once per context: pinned allocations are slow
+  ctx.h_ga.reserve(std::max<int64_t>(h_total, int64_t{32} << 20));
+  uint8_t* H = ctx.h_ga.p;
+  std::memcpy(H + h_runs, gr.data(), sizeof(GaRun) * n);
+  GaRun* hr = reinterpret_cast<GaRun*>(H + h_runs);
+  unsigned long long* hctl = reinterpret_cast<unsigned long long*>(H + h_ctl);
+  std::memset(hctl, 0, 8 * kGaCtlWords);
+  hctl[kGaCtlTail] = static_cast<unsigned long long>(n);
+  int32_t* hrank = reinterpret_cast<int32_t*>(H + h_rank);
+  for (int d = 0; d < 256; ++d) {
+    hrank[d] = d < P.N ? P.id_rank[d] : 0;
+    hrank[256 + d] = d < P.N ? P.by_id_rank[d] : 0;
+  }
+  uint2* hq = reinterpret_cast<uint2*>(H + h_qpay);
+  unsigned long long* hs = reinterpret_cast<unsigned long long*>(H + h_qseq);
+  for (int i = 0; i < n; ++i) {
+    hq[i] = make_uint2(static_cast<unsigned>(i), 0xffffffffu);
+    hs[i] = static_cast<unsigned long long>(i) + 1;
+  }
+  std::memcpy(H + h_opts, opts.data(), 8 * opts.size());
+  std::memcpy(H + h_jump, jumps.data(), 32 * jumps.size());
+  cudaStream_t st = ctx.stream;
+  cuda_check(cudaMemcpyAsync(D + o_runs, H + h_runs, sizeof(GaRun) * n, cudaMemcpyHostToDevice, st), "H2D ga runs");
+  cuda_check(cudaMemcpyAsync(D + o_ctl, H + h_ctl, 8 * kGaCtlWords, cudaMemcpyHostToDevice, st), "H2D ga ctl");
+  cuda_check(cudaMemcpyAsync(D + o_rank, H + h_rank, 8 * 256, cudaMemcpyHostToDevice, st), "H2D ga ranks");
+  cuda_check(cudaMemsetAsync(D + o_qseq, 0, 8 * q_cap, st), "ga queue clear");
+  cuda_check(cudaMemcpyAsync(D + o_qpay, H + h_qpay, 8 * n, cudaMemcpyHostToDevice, st), "H2D ga queue");
+  cuda_check(cudaMemcpyAsync(D + o_qseq, H + h_qseq, 8 * n, cudaMemcpyHostToDevice, st), "H2D ga queue");
+  if (!opts.empty())
+    cuda_check(cudaMemcpyAsync(D + o_opts, H + h_opts, 8 * opts.size(), cudaMemcpyHostToDevice, st),
+               "H2D ga layout options");
+  cuda_check(cudaMemcpyAsync(D + o_jump, H + h_jump, 32 * jumps.size(), cudaMemcpyHostToDevice, st),
+             "H2D ga jump polynomials");
+  GaParams G{};
+  G.runs = reinterpret_cast<GaRun*>(D + o_runs);
+  G.n_runs = n;
+  G.pop_cap = pop_cap;
+  G.sps = sps;
+  G.max_wave = max_wave;
+  G.pool = D + o_pool;
+  G.res = reinterpret_cast<EvalResult*>(D + o_res);
+  G.id_rank = reinterpret_cast<const int32_t*>(D + o_rank);
+  G.by_id_rank = reinterpret_cast<const int32_t*>(D + o_rank) + 256;
+  G.q_pay = reinterpret_cast<uint2*>(D + o_qpay);
+  G.q_seq = reinterpret_cast<unsigned long long*>(D + o_qseq);
+  G.q_mask = q_cap - 1;
+  G.ctl = reinterpret_cast<unsigned long long*>(D + o_ctl);
+  G.impr = reinterpret_cast<GaImpr*>(D + o_impr);
+  G.impr_cap = impr_cap;
+  G.kb_flags = kb;
+  G.n_tasks = P.T;
+  G.max_stride = stride;
+  G.fastmod = gt.fastmod;
+  G.opts = reinterpret_cast<const short4*>(D + o_opts);
+  G.init_snaps = reinterpret_cast<Rng*>(D + o_snaps);
+  G.jumps = reinterpret_cast<const uint64_t*>(D + o_jump);
+  G.gen_scratch = D + o_gscr;
+  G.init_cap = init_cap;
+  G.res_per_run = res_per_run;
+  // interleaved per-lane generation scratch: int16 regions | nodes | 4 x nodes,
+  // uint8 flat | bucket; in shared memory when the evaluation carve holds it
+  G.gen_smem = 2 * (gt.n_regions + gt.max_nodes_per_region + 4 * gt.n_nodes) + 2 * gt.n_dev;
+  {
+    Carve c1 = cv;
+    c1.cls_smem = 0;
+    c1.n_warps = 1;
+    G.gen_in_smem = 32 * G.gen_smem <= carve2_bytes(c1) ? 1 : 0;
+  }
+  G.n_regions = gt.n_regions;
+  G.n_nodes = gt.n_nodes;
+  G.max_nodes_per_region = gt.max_nodes_per_region;
+  G.n_dev = gt.n_dev;
+  G.bias = K.locality_bias;
+  G.region_off = gt.region_off;
+  G.node_off = gt.node_off;
+  G.node_devs = gt.node_devs;
+  G.node_rank = gt.node_rank;
+  for (int t = 0; t < P.T; ++t) G.task_nl[t] = P.tasks[t].nl;
+  static const char* ga_log = std::getenv("HPG_GA_LOG");  // diagnostics only
+  G.prof = ga_log ? 1 : 0;
+  const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);
+  ctx.d_scratch.reserve(static_cast<size_t>(32 * ctx.n_sm) * scratch);
+  const int64_t h2d = static_cast<int64_t>(sizeof(GaRun)) * n + 8 * kGaCtlWords + 8 * 256 +
+                      16 * static_cast<int64_t>(n) + 8 * static_cast<int64_t>(opts.size()) +
+                      32 * static_cast<int64_t>(jumps.size());
+  const double t_launch = now_s();
+  cuda_check(cudaEventRecord(ctx.ev0, st), "event");
+  int grid = 0;
+  cuda_check(launch_ga_offspring(ctx.dprob, cfg, cv, G, ctx.d_scratch.p, scratch, ctx.n_sm, grid, st),
+             "ga_kernel launch");
+  if (grid > max_workers) throw InternalError("ga_kernel grid exceeds its scratch");
+  cuda_check(cudaEventRecord(ctx.ev1, st), "event");
+  ++ctx.launches;
+  ++ctx.eval_launches;
+  // results: run states and control words, the two kept plans per run, then
+  // the improvements
+  cuda_check(cudaMemcpyAsync(H + h_runs, D + o_runs, sizeof(GaRun) * n, cudaMemcpyDeviceToHost, st), "D2H ga runs");
+  cuda_check(cudaMemcpyAsync(H + h_ctl, D + o_ctl, 8 * kGaCtlWords, cudaMemcpyDeviceToHost, st), "D2H ga ctl");
+  cuda_check(cudaMemcpy2DAsync(H + h_best, 2 * stride, D + o_pool, run_bytes, 2 * stride, n,
+                               cudaMemcpyDeviceToHost, st), "D2H ga best plans");
+  cuda_check(cudaStreamSynchronize(st), "ga_kernel");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1);
+  ctx.eval_ms += ms;
+  const int64_t n_impr = static_cast<int64_t>(hctl[kGaCtlImpr]);
+  if (n_impr > impr_cap) throw InternalError("device GA improvement list overflow");
+  if (n_impr > 0)
+    cuda_check(cudaMemcpy(H + h_imp, D + o_impr, sizeof(GaImpr) * n_impr, cudaMemcpyDeviceToHost),
+               "D2H ga improvements");
+  ctx.plans_evaluated += static_cast<int64_t>(hctl[kGaCtlEvals]);
+  ctx.canonical_bytes += static_cast<int64_t>(hctl[kGaCtlBytes]);
+  ctx.h2d_bytes += h2d;
+  ctx.d2h_bytes += static_cast<int64_t>(sizeof(GaRun)) * n + 8 * kGaCtlWords +
+                   2 * static_cast<int64_t>(stride) * n + static_cast<int64_t>(sizeof(GaImpr)) * n_impr;
+  const unsigned long long t0_dev = hctl[kGaCtlT0];
+  auto cand_at = [&](const uint8_t* rec, int ng) {
+    Cand c;
+    const int32_t bytes = *reinterpret_cast<const int32_t*>(rec);
+    c.rec.assign(rec, rec + bytes);
+    rec_offsets(c.hdr(), c.o);
+    c.ng = ng;
+    return c;
+  };
+  std::vector<GaImpr> imp(reinterpret_cast<GaImpr*>(H + h_imp),
+                          reinterpret_cast<GaImpr*>(H + h_imp) + n_impr);
+  std::stable_sort(imp.begin(), imp.end(), [](const GaImpr& a, const GaImpr& b) {
+    return a.run != b.run ? a.run < b.run : a.local_idx < b.local_idx;
+  });
+  for (int i = 0; i < n; ++i) {
+    const GaRun& g = hr[i];
+    ArmRun& r = *runs[i];
+    const int ng = static_cast<int>(r.env->tg.size());
+    r.used = g.used;
+    r.best = g.best;
+    r.n_offspring += g.n_offspring;
+    r.w_mut += g.n_waves;
+    if (g.best_member_flags & 2) {
+      r.best_member = cand_at(H + h_best + 2 * static_cast<int64_t>(stride) * i, ng);
+      r.best_member_cost = g.best_member_cost;
+      r.has_best_member = true;
+    }
+  }
+  for (size_t k = 0; k < imp.size(); ++k) {
+    const GaImpr& x = imp[k];
+    ArmRun& r = *runs[x.run];
+    const double t = t_launch + 1e-9 * static_cast<double>(x.t - t0_dev);
+    r.impr.push_back(Improvement{x.local_idx, x.cost, Cand{}, t});
+    const bool last = k + 1 == imp.size() || imp[k + 1].run != x.run;
+    if (last && (hr[x.run].impr_flags & 1))
+      r.impr.back().plan = cand_at(H + h_best + 2 * static_cast<int64_t>(stride) * x.run + stride,
+                                   static_cast<int>(r.env->tg.size()));
+  }
+  int64_t mx = 0;
+  for (int i = 0; i < n; ++i) mx = std::max<int64_t>(mx, hr[i].n_waves);
+  waves += mx;
+  clock = now_s();
+  if (ga_log) {
+    if (FILE* f = std::fopen(ga_log, "a")) {
+      // runs grid stride evals impr max_waves prep_ms kernel_ms total_ms |
+      // step_kcycles_avg steps eval_kcycles_avg evals
+      const unsigned long long* pf = hctl + kGaCtlProf;
+      std::fprintf(f, "%d %d %d %llu %lld %lld %.3f %.3f %.3f | %.1f %llu %.1f %llu\n", n, grid,
+                   stride, hctl[kGaCtlEvals], static_cast<long long>(n_impr),
+                   static_cast<long long>(mx), 1e3 * (t_launch - t_prep0), ms,
+                   1e3 * (clock - t_prep0), pf[1] ? 1e-3 * pf[0] / pf[1] : 0.0, pf[1],
+                   pf[3] ? 1e-3 * pf[2] / pf[3] : 0.0, pf[3]);
+      // sub-phases (kcycles per step): load store draw spec walk3 insert mut/init score
+      std::fprintf(f, "   ");
+      for (int q = 0; q < 8; ++q)
+        std::fprintf(f, " %.1f", pf[1] ? 1e-3 * hctl[100 + q] / pf[1] : 0.0);
+      // init chunks: kcycles per chunk, chunks, candidates
+      std::fprintf(f, " | init %.1f %llu %llu\n", hctl[109] ? 1e-3 * hctl[108] / hctl[109] : 0.0,
+                   hctl[109], hctl[110]);
+      std::fclose(f);
+    }
+  }
+}
+
 // Runs all arm coroutines to completion, batching their requests per wave.
 void run_lockstep(Ctx& ctx, const Knobs& K, std::vector<ArmRun*>& runs, double& clock,
                   int64_t& waves) {
   const DevCostConfig cfg = K.cost_config();
   const int kb = (K.balance_data ? 1 : 0) | (K.balance_layers ? 2 : 0);
   double th = now_s();
+  const bool dev_ga = device_ga_enabled(K);
   // arms are independent: their GA steps (candidate generation, population
   // bookkeeping) run on a host thread pool; only the GPU wave is shared
   const int nr = static_cast<int>(runs.size());
 host_parallel_for(nr, nr >= 16, [&](int i) {
     ArmRun* r = runs[i];
     r->clock = &clock;
+    r->device_ga = dev_ga;
     r->coro = ga_run(*r);
     r->coro.h.resume();
   });
@@ -928,6 +1260,14 @@ host_parallel_for(nr, nr >= 16, [&](int i) {
     for (auto& [r, cnt] : owners)
       if (r->coro.h.promise().exc) std::rethrow_exception(r->coro.h.promise().exc);
     ctx.host_ms += 1e3 * (now_s() - clock);
+  }
+  std::vector<ArmRun*> handed;
+  for (ArmRun* r : runs)
+    if (r->handoff) handed.push_back(r);
+  if (!handed.empty()) {
+    const double tb = now_s();
+    device_ga(ctx, K, handed, clock, waves);
+    ctx.batch_ms += 1e3 * (now_s() - tb);
   }
   static const char* spec_log = std::getenv("HPG_SPEC_LOG");  // diagnostics only
   if (spec_log) {

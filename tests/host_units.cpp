@@ -3,11 +3,13 @@
 //   * fastmod_u64 == the hardware remainder for random and edge-case inputs
 //   * Rng streams equal the reference's documented xoshiro256** / splitmix64
 //     (first draws of Rng(42) recorded from the compiled reference)
+//   * jump-ahead polynomials (rng_jump.hpp) == stepping the stream D times
 #include <cinttypes>
 #include <cstdio>
 #include <cstdlib>
 
 #include "../paper_2512_12476_b200/csrc/rng.hpp"
+#include "../paper_2512_12476_b200/csrc/rng_jump.hpp"
 
 int main(int argc, char** argv) {
   using namespace hpg;
@@ -42,5 +44,24 @@ int main(int argc, char** argv) {
   const uint64_t y = f.bounded(100);
   const double z = f.uniform();
   std::printf("fork7 %" PRIu64 " bounded100 %" PRIu64 " uniform %.17g\n", x, y, z);
-  return bad == 0 ? 0 : 1;
+  // jump-ahead: x^D mod p applied to a state == D draws; table x^(L*D)
+  uint64_t jbad = 0;
+  Rng jr(777);
+  for (int trial = 0; trial < 64; ++trial) {
+    const uint64_t D = trial < 4 ? static_cast<uint64_t>(trial) : jr.next() % 3000;
+    Rng a0(jr.next()), b0 = a0;
+    for (uint64_t k = 0; k < D; ++k) a0.next();
+    const Poly256 q = jump_poly(D);
+    rng_apply_jump(b0, q.data());
+    for (int w = 0; w < 4; ++w) jbad += a0.s[w] != b0.s[w];
+    const std::vector<Poly256>& tb = jump_table(D, 31);
+    for (int L : {1, 7, 31}) {
+      Rng c0(jr.next()), d0 = c0;
+      for (uint64_t k = 0; k < D * L; ++k) c0.next();
+      rng_apply_jump(d0, tb[L - 1].data());
+      for (int w = 0; w < 4; ++w) jbad += c0.s[w] != d0.s[w];
+    }
+  }
+  std::printf("jump mismatches %" PRIu64 "\n", jbad);
+  return bad == 0 && jbad == 0 ? 0 : 1;
 }

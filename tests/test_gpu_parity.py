@@ -233,10 +233,15 @@ def test_mixed_problem_sizes_in_one_process():
             assert res.consumed > 0 and res.plan is not None
 
 
-def test_device_generated_init_candidates_identical():
-    """GA init candidates made on the device (HPG_DEVICE_GEN_MIN=0: every
-    init chunk) give the same searches as the reference: c1/c2 goldens and the
-    60 search fuzz cases, in a subprocess (the switch is read once)"""
+@pytest.mark.parametrize("env", [{"HPG_DEVICE_GA": "0"},
+                                 {"HPG_DEVICE_GA": "0", "HPG_DEVICE_GEN_MIN": "0"}],
+                         ids=["host_ga", "host_ga_device_init"])
+def test_host_ga_paths_identical(env):
+    """The default search runs ga_run on the device (ga_kernel.cuh). The host
+    coroutine GA in lockstep waves (HPG_DEVICE_GA=0), with init candidates
+    made by the host pool or on the device (HPG_DEVICE_GEN_MIN=0), gives the
+    same searches: c1/c2 goldens and the 60 search fuzz cases, in a
+    subprocess (the switches are read once)"""
     import os
     import subprocess
     import sys
@@ -244,6 +249,5 @@ def test_device_generated_init_candidates_identical():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
                         os.path.join(here, "test_gpu_parity.py"), "-k",
                         "search_configs or search_fuzz"],
-                       env=dict(os.environ, HPG_DEVICE_GEN_MIN="0"), capture_output=True,
-                       text=True, timeout=900)
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

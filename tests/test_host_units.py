@@ -1,5 +1,6 @@
 """CPU tests of host-side building blocks (no GPU): the exact fast remainder
-used by the candidate generator and the Rng stream pinned to the reference."""
+used by the candidate generator, the Rng stream pinned to the reference and
+its jump-ahead."""
 import json
 import os
 import subprocess
@@ -21,6 +22,13 @@ def test_fastmod_exact(host_units):
     out = subprocess.run([host_units, "42"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout
     assert "mismatches 0" in out.stdout
+
+
+def test_rng_jump_ahead_exact(host_units):
+    """x^D mod p (Berlekamp-Massey characteristic polynomial) applied to a
+    state equals D draws: the device GA's init chunks start every lane there"""
+    out = subprocess.run([host_units, "42"], capture_output=True, text=True)
+    assert "jump mismatches 0" in out.stdout, out.stdout
 
 
 def test_rng_stream_matches_reference(host_units):
