@@ -254,7 +254,9 @@ def run_engine(args, world, rank, local_rank):
     total_ms = sum(step_ms)
     value = consumed / (total_ms / 1000.0)
     e2e_value = consumed / (sum(e2e_ms) / 1000.0)
-    # roofline of the dominant kernel (eval_kernel): canonical bytes / event time
+    # roofline of the dominant kernel: ga_kernel (the device GA of a SHA round,
+    # whose warps evaluate every candidate; eval_kernel for the final
+    # breakdown): canonical bytes of the plans evaluated / CUDA-event time
     eval_ms = sum(i["eval_kernel_ms"] for i in infos)
     eval_launches = sum(i["eval_launches"] for i in infos)
     cbytes = sum(i["canonical_bytes"] for i in infos)
@@ -273,19 +275,19 @@ def run_engine(args, world, rank, local_rank):
                 "h2d_bytes_per_step": int(statistics.median(h2d)),
                 "d2h_bytes_per_step": int(statistics.median(d2h)),
                 "ms_per_step": sum(e2e_ms) / args.steps},
-        "roofline": {"bound": "hbm", "kernel": "eval_kernel", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "ga_kernel", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                     "traffic": ncu_traffic("eval_kernel"),
+                     "traffic": ncu_traffic("ga_kernel"),
                      "algorithmic_bytes_per_launch": cbytes / eval_launches,
                      "avg_launch_ms": eval_ms / eval_launches,
                      "kernel_share_of_step": eval_ms / total_ms,
                      "note": "latency/issue-bound scalar FP64 gather work; HBM is not the "
                              "binding resource (SURVEY.md §8 D1)",
-                     "traffic_note": "ncu --set full replays each launch with flushed caches: "
-                                     "its DRAM bytes are dominated by fetching the kernel's "
-                                     "~0.5 MB of SASS and the problem tables, which stay in "
-                                     "the 126 MB L2 across the waves of a search"},
+                     "traffic_note": "ncu --set full replays a launch with flushed caches: "
+                                     "its DRAM bytes are the kernel's SASS, the problem "
+                                     "tables and the round's record pools, which stay in "
+                                     "the 126 MB L2 while the round runs"},
         "gpu_launches": sum(i["gpu_launches"] for i in infos),
         "waves_per_step": infos[-1]["waves"],
         "plans_scored_on_gpu_per_step": infos[-1]["plans_evaluated_gpu"],

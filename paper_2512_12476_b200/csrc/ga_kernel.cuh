@@ -215,6 +215,7 @@ struct GaSrcInfo {
 };
 
 constexpr int kGaMaxPatch = 2 * kMaxTasks;
+constexpr int kGaPendBias = 1 << 20;  // pending while a wave is still being drawn
 
 // per-source tables: geometry, eligible tasks, rank set of every group
 __device__ void ga_src_info(const GaView& v, const uint8_t* src, GaSrcInfo& si) {
@@ -797,6 +798,8 @@ __device__ void ga_publish(int run, int i0, int i1) {
   const int lane = threadIdx.x & 31;
   const int n = i1 - i0;
   if (n <= 0) return;
+  __threadfence();  // every lane's record stores before any task is visible
+  __syncwarp();
   unsigned long long base = 0;
   if (lane == 0) base = atomicAdd(&c_ga.ctl[kGaCtlTail], static_cast<unsigned long long>(n));
   base = __shfl_sync(0xffffffffu, base, 0);
@@ -818,9 +821,9 @@ __device__ void ga_publish(int run, int i0, int i1) {
       atomicAdd(&c_ga.ctl[100 + (slot)], static_cast<unsigned long long>(clock64() - ph0_)); \
   } while (0)
 
-// one GA step of run r: runs the state machine until it needs a wave (returns
-// the index of the wave's candidate this warp evaluates itself) or the run
-// ends (returns -1)
+// one GA step of run r: runs the state machine until it has published a wave
+// that is still being evaluated or the run ends (returns 0); 1 asks the
+// worker to step the run again (not used: a finished wave continues here)
 __device__ int ga_step(int r, const GaSm& sm) {
   GaRun* R = c_ga.runs + r;
   GaView v;
@@ -839,14 +842,37 @@ __device__ int ga_step(int r, const GaSm& sm) {
   GaHot h;
   GA_PH(0, ga_load(R, h); ga_pop_load(v, h);
         if (h.state != kGaLoop && h.state != kGaInit && h.state != kGaInitDone) ga_res_load(v, h));
-  auto submit = [&](int buf, int n) {
+  // A wave's candidates are published as they are drawn, so evaluation
+  // overlaps the rest of the step: pending starts biased and drops to the
+  // true count when the step closes the wave.
+  auto wave_begin = [&](int buf) {
     h.wave_buf = buf;
+    if ((threadIdx.x & 31) == 0) {
+      R->wave_buf = buf;
+      R->pending = kGaPendBias;
+    }
+    __threadfence();
+    __syncwarp();
+  };
+  auto wave_cancel = [&]() {
+    if ((threadIdx.x & 31) == 0) R->pending = 0;
+    __syncwarp();
+  };
+  // closes the wave of n candidates; 1 when they have all been evaluated
+  // already (this warp continues the run), else 0
+  auto wave_end = [&](int n) {
     h.wave_n = n;
     ++h.n_waves;
     h.n_evals += n;
-    GA_PH(1, ga_pop_store(v, h); ga_store(R, h); if ((threadIdx.x & 31) == 0) R->pending = n;
-          __threadfence(); __syncwarp(); ga_publish(r, 0, n - 1));
-    return n - 1;
+    int done = 0;
+    GA_PH(1, ga_pop_store(v, h); ga_store(R, h); __threadfence();
+          if ((threadIdx.x & 31) == 0) done = atomicAdd(&R->pending, n - kGaPendBias) == kGaPendBias - n;
+          done = __shfl_sync(0xffffffffu, done, 0));
+    if (done) {
+      __threadfence();
+      if (h.state != kGaInitDone) ga_res_load(v, h);
+    }
+    return done;
   };
   auto finish = [&]() {
     h.state = kGaDone;
@@ -858,7 +884,7 @@ __device__ int ga_step(int r, const GaSm& sm) {
       if (d == static_cast<unsigned long long>(c_ga.n_runs)) atomicExch(&c_ga.ctl[kGaCtlStop], 1ull);
     }
     __syncwarp();
-    return -1;
+    return 0;
   };
   while (true) {
     if (h.state == kGaInit) {
@@ -872,13 +898,16 @@ __device__ int ga_step(int r, const GaSm& sm) {
       const int64_t need = h.init_target - h.n_pop;
       const int64_t grow = h.chunk * 2 > 2 * need + 2 ? h.chunk * 2 : 2 * need + 2;
       h.chunk = h.attempt_cap - h.attempts < grow ? h.attempt_cap - h.attempts : grow;
+      wave_begin(0);
       GA_PH(8, ga_init_chunk(v, h.rng, h.combo, static_cast<int>(h.chunk)));
       if (c_ga.prof && (threadIdx.x & 31) == 0) {
         atomicAdd(&c_ga.ctl[109], 1ull);
         atomicAdd(&c_ga.ctl[110], static_cast<unsigned long long>(h.chunk));
       }
       h.state = kGaInitDone;
-      return submit(0, static_cast<int>(h.chunk));
+      ga_publish(r, 0, static_cast<int>(h.chunk));
+      if (wave_end(static_cast<int>(h.chunk))) continue;
+      return 0;
     }
     if (h.state == kGaInitDone) {
       const int lane = threadIdx.x & 31;
@@ -936,10 +965,14 @@ __device__ int ga_step(int r, const GaSm& sm) {
       h.have_spec = 0;
       Rng r2 = h.rng;
       const int i = static_cast<int>(GA_BOUNDED(r2, static_cast<uint64_t>(h.n_pop)));
+      wave_begin(0);
       GA_PH(6, ga_ld_rec(sm.par, v.slot(sm.pslot[i]), v.stride);
             ga_draw_mut(v, r2, sm.par, &R->cur, 0, 0));
       h.state = kGaMut;
-      return submit(0, __ldcg(&R->cur.ntr) + 1);
+      const int nm = __ldcg(&R->cur.ntr) + 1;
+      ga_publish(r, 0, nm);
+      if (wave_end(nm)) continue;
+      return 0;
     }
     if (h.state == kGaMut) {
       // the stage's results are in sm.res (its wave just finished)
@@ -969,17 +1002,24 @@ __device__ int ga_step(int r, const GaSm& sm) {
       GA_PH(7, ga_score(v, h, v.wave_slot(buf, h.child_idx), h.child_cost));
       if (h.used < slice) {
         const int wb = 1 - h.child_buf;
+        wave_begin(wb);
         h.before3 = h.rng;
         GA_PH(2, h.n3 = ga_draw(v, h, 3, wb, 0, R->snaps3));
+        ga_publish(r, 0, h.n3);
         h.before5 = h.rng;
         GA_PH(2, h.n5 = ga_draw(v, h, 5, wb, h.n3, R->snaps5));
+        ga_publish(r, h.n3, h.n3 + h.n5);
         if (h.n3 + h.n5 > 0) {
           const int base2 = h.n3 + h.n5;
           const Rng from = h.n5 > 0 ? ga_ld_rng(&R->snaps5[h.n5 - 1]) : h.before5;
           GA_PH(3, ga_speculate(v, h, from, wb, base2));
           h.state = kGaSwap;
-          return submit(wb, base2 + __ldcg(&R->spec.ntr) + 1);
+          const int nw = base2 + __ldcg(&R->spec.ntr) + 1;
+          ga_publish(r, base2, nw);
+          if (wave_end(nw)) continue;
+          return 0;
         }
+        wave_cancel();
         h.rng = h.before5;
       }
       GA_PH(5, ga_insert_if(v, h));
@@ -996,12 +1036,18 @@ __device__ int ga_step(int r, const GaSm& sm) {
       } else if (w3 == 1 && h.used < slice) {
         const int wb2 = 1 - h.wave_buf;
         h.b5 = h.rng;
+        wave_begin(wb2);
         h.m5 = ga_draw(v, h, 5, wb2, 0, R->snaps5);
+        ga_publish(r, 0, h.m5);
         if (h.m5 > 0) {
           ga_speculate(v, h, ga_ld_rng(&R->snaps5[h.m5 - 1]), wb2, h.m5);
           h.state = kGaRedraw;
-          return submit(wb2, h.m5 + __ldcg(&R->spec.ntr) + 1);
+          const int nw = h.m5 + __ldcg(&R->spec.ntr) + 1;
+          ga_publish(r, h.m5, nw);
+          if (wave_end(nw)) continue;
+          return 0;
         }
+        wave_cancel();
       }
       ga_insert_if(v, h);
       h.state = kGaLoop;
@@ -1013,7 +1059,7 @@ __device__ int ga_step(int r, const GaSm& sm) {
       h.state = kGaLoop;
       continue;
     }
-    return -1;  // kGaDone: not reached
+    return 0;  // kGaDone: not reached
   }
 }
 
@@ -1104,14 +1150,14 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
     int run = static_cast<int>(__shfl_sync(0xffffffffu, pay.x, 0));
     int idx = static_cast<int>(__shfl_sync(0xffffffffu, pay.y, 0));
     while (true) {
-      if (idx < 0) {  // GA step
+      if (idx < 0) {  // GA step (again while its waves finish before it closes them)
         const long long c0 = c_ga.prof ? clock64() : 0;
-        idx = ga_step(run, sm);
+        const int again = ga_step(run, sm);
         if (c_ga.prof && lane == 0) {
           atomicAdd(&c_ga.ctl[kGaCtlProf], static_cast<unsigned long long>(clock64() - c0));
           atomicAdd(&c_ga.ctl[kGaCtlProf + 1], 1ull);
         }
-        if (idx < 0) break;
+        if (!again) break;
         continue;
       }
       const long long c1 = c_ga.prof ? clock64() : 0;
