@@ -807,6 +807,51 @@ int cmd_search(const std::string& wfp, const std::string& tpp, std::int64_t budg
   return j["replay_consistent"].get<bool>() ? 0 : 1;
 }
 
+
+// ga_search (search.hpp:127-135) on its own: for a few arms of a fixture
+// (task grouping from enumerate_task_groupings, GPU grouping from
+// enumerate_gpu_groupings) and slices/seeds, the best member's plan and
+// cost, the evaluations used and its breakdown.
+int cmd_ga(const std::string& wfp, const std::string& tpp, const std::string& out,
+           const std::string& knobs_path) {
+  const WorkflowGraph wf = parse_workflow_json(read_file(wfp));
+  const DeviceTopology topo = parse_topology_json(read_file(tpp));
+  SearchKnobs k = knobs_from(knobs_path);
+  const auto tgs = enumerate_task_groupings(wf);
+  json recs = json::array();
+  Rng pick(2024);
+  for (int c = 0; c < 12; ++c) {
+    const TaskGrouping& tg = tgs[pick.bounded(tgs.size())];
+    const auto ggs = enumerate_gpu_groupings(topo.size(), static_cast<int>(tg.groups.size()), 1);
+    if (ggs.empty()) continue;
+    const GpuGrouping& gg = ggs[pick.bounded(ggs.size())];
+    const std::int64_t slice = 1 + static_cast<std::int64_t>(pick.bounded(c < 6 ? 40 : 400));
+    const std::uint64_t seed = pick.next();
+    const GaResult r = ga_search(tg, gg, wf, topo, slice, Rng(seed), k);
+    json j;
+    j["groups"] = tg.groups;
+    j["counts"] = gg.counts;
+    j["slice"] = slice;
+    j["seed"] = std::to_string(seed);
+    j["evals"] = r.evals;
+    j["cost"] = hx(r.cost);
+    j["has_plan"] = r.plan.has_value();
+    if (r.plan) {
+      j["plan"] = plan_json(*r.plan, topo);
+      j["breakdown"] = breakdown_json(r.breakdown);
+    }
+    recs.push_back(j);
+  }
+  json o;
+  o["knobs"] = knobs_json(k);
+  o["workflow"] = workflow_json(wf);
+  o["topology"] = topology_json(topo);
+  o["records"] = recs;
+  write_file(out, o.dump() + "\n");
+  std::printf("ga %zu records -> %s\n", recs.size(), out.c_str());
+  return 0;
+}
+
 int cmd_searchfuzz(std::uint64_t seed, int n, const std::string& out) {
   Rng rng(seed);
   json recs = json::array();
@@ -1382,6 +1427,7 @@ int main(int argc, char** argv) {
     if (cmd == "search")
       return cmd_search(arg(2), arg(3), std::stoll(arg(4)), std::stoull(arg(5)), arg(6),
                         argc > 7 ? argv[7] : "");
+    if (cmd == "ga") return cmd_ga(arg(2), arg(3), arg(4), argc > 5 ? arg(5) : "");
     if (cmd == "searchfuzz") return cmd_searchfuzz(std::stoull(arg(2)), std::stoi(arg(3)), arg(4));
     if (cmd == "exhaustive") return cmd_exhaustive(std::stoull(arg(2)), std::stoi(arg(3)), arg(4));
     if (cmd == "cli") return cmd_cli(arg(2));

@@ -73,6 +73,7 @@ struct alignas(16) GaRun {
   double child_cost;
   int32_t n3, n5, m5, pad0;
   Rng before3, before5, b5;
+  Rng spec_from;  // stream position of the swap wave's speculative stage
   int64_t n_offspring, n_waves, n_evals, pad1;
   unsigned long long impr_time;  // globaltimer at the latest improvement
   int32_t pop_slot[kGaMaxPop];

@@ -215,7 +215,9 @@ struct GaSrcInfo {
 };
 
 constexpr int kGaMaxPatch = 2 * kMaxTasks;
-constexpr int kGaPendBias = 1 << 20;  // pending while a wave is still being drawn
+constexpr int kGaPendBias = 1 << 20;  // pending per share of a wave still being drawn
+// ring task kinds (payload index): >= 0 evaluate candidate i; step; draws
+constexpr int kGaTaskStep = -1, kGaTaskDraw3 = -15, kGaTaskDraw5 = -14, kGaTaskSpec = -13;
 
 // per-source tables: geometry, eligible tasks, rank set of every group
 __device__ void ga_src_info(const GaView& v, const uint8_t* src, GaSrcInfo& si) {
@@ -812,6 +814,54 @@ __device__ void ga_publish(int run, int i0, int i1) {
   __syncwarp();
 }
 
+
+// One draw of a swap wave (kGaTaskDraw3 / kGaTaskDraw5 / kGaTaskSpec) from
+// the positions the step stored: draws, publishes its candidates and closes
+// its share. 1 when the whole wave has been evaluated already (the caller
+// continues the run).
+__device__ int ga_draw_task(int r, int kind, const GaSm& sm) {
+  GaRun* R = c_ga.runs + r;
+  GaView v;
+  v.R = R;
+  v.run = r;
+  v.pool = c_ga.pool + __ldcg(&R->pool_off);
+  v.stride = __ldcg(&R->rec_stride);
+  v.ng = __ldcg(&R->ng);
+  for (int k = 0; k <= kMaxTasks; ++k) v.gstart[k] = __ldcg(&R->gstart[k]);
+  for (int k = 0; k < kMaxTasks; ++k) v.gslot[k] = __ldcg(&R->gslot[k]);
+  v.sm = sm;
+  GaHot h;
+  ga_load(R, h);
+  const int wb = h.wave_buf;
+  int i0 = 0, i1 = 0;
+  if (kind == kGaTaskDraw3) {
+    h.rng = h.before3;
+    ga_draw(v, h, 3, wb, 0, R->snaps3);
+    i0 = 0;
+    i1 = h.n3;
+  } else if (kind == kGaTaskDraw5) {
+    h.rng = h.before5;
+    ga_draw(v, h, 5, wb, h.n3, R->snaps5);
+    i0 = h.n3;
+    i1 = h.n3 + h.n5;
+  } else {
+    ga_pop_load(v, h);
+    const int base2 = h.n3 + h.n5;
+    ga_speculate(v, h, ga_ld_rng(&R->spec_from), wb, base2);
+    i0 = base2;
+    i1 = base2 + __ldcg(&R->spec.ntr) + 1;
+    if ((threadIdx.x & 31) == 0) R->wave_n = i1;
+  }
+  ga_publish(r, i0, i1);
+  __threadfence();
+  int done = 0;
+  if ((threadIdx.x & 31) == 0)
+    done = atomicAdd(&R->pending, (i1 - i0) - kGaPendBias) == kGaPendBias - (i1 - i0);
+  done = __shfl_sync(0xffffffffu, done, 0);
+  if (done) __threadfence();
+  return done;
+}
+
 // diagnostics: sub-phase cycles of a GA step (ctl words 100..107)
 #define GA_PH(slot, expr)                                                         \
   do {                                                                            \
@@ -956,8 +1006,8 @@ __device__ int ga_step(int r, const GaSm& sm) {
         const int4* s = reinterpret_cast<const int4*>(&R->spec);
         int4* d = reinterpret_cast<int4*>(&R->cur);
         const int lane = threadIdx.x & 31;
-        for (int i = lane; i < static_cast<int>(sizeof(GaStage) / 16); i += 32) d[i] = __ldcg(s + i);
-        __syncwarp();
+        GA_PH(3, for (int i = lane; i < static_cast<int>(sizeof(GaStage) / 16); i += 32) d[i] = __ldcg(s + i);
+              __syncwarp());
         h.have_spec = 0;
         h.state = kGaMut;
         continue;
@@ -1001,26 +1051,71 @@ __device__ int ga_step(int r, const GaSm& sm) {
       h.streak = 0;
       GA_PH(7, ga_score(v, h, v.wave_slot(buf, h.child_idx), h.child_cost));
       if (h.used < slice) {
+        // the swap wave: L3 trials, L5 trials and the speculative stage.
+        // Their stream positions are fixed in advance (a level-3 move draws
+        // four values, a level-5 move three), so other workers draw two of
+        // the three at the same time (ga_draw_task) while this one draws the
+        // first; each publishes its candidates and closes its share of the wave
         const int wb = 1 - h.child_buf;
-        wave_begin(wb);
+        ga_child_to_sm(v, h);
+        GaGeo geo;
+        ga_geo(sm.child, c_ga.n_tasks, geo);
+        int ne = 0;
+        for (int s = 0; s < c_ga.n_tasks; ++s) ne += geo.off[s + 1] - geo.off[s] >= 2;
+        const int sps = c_ga.sps;
+        h.n3 = v.ng >= 2 && sps > 0 ? sps : 0;
+        h.n5 = ne > 0 && sps > 0 ? sps : 0;
         h.before3 = h.rng;
-        GA_PH(2, h.n3 = ga_draw(v, h, 3, wb, 0, R->snaps3));
-        ga_publish(r, 0, h.n3);
-        h.before5 = h.rng;
-        GA_PH(2, h.n5 = ga_draw(v, h, 5, wb, h.n3, R->snaps5));
-        ga_publish(r, h.n3, h.n3 + h.n5);
         if (h.n3 + h.n5 > 0) {
-          const int base2 = h.n3 + h.n5;
-          const Rng from = h.n5 > 0 ? ga_ld_rng(&R->snaps5[h.n5 - 1]) : h.before5;
-          GA_PH(3, ga_speculate(v, h, from, wb, base2));
+          Rng q = h.rng;
+          for (int k2 = 0; k2 < 4 * h.n3; ++k2) q.next();
+          h.before5 = q;
+          for (int k2 = 0; k2 < 3 * h.n5; ++k2) q.next();
+          h.rng = q;
+          const int first = h.n3 > 0 ? kGaTaskDraw3 : kGaTaskDraw5;
+          const int shares = (h.n3 > 0) + (h.n5 > 0) + 1;
+          h.wave_buf = wb;
+          ++h.n_waves;
           h.state = kGaSwap;
-          const int nw = base2 + __ldcg(&R->spec.ntr) + 1;
-          ga_publish(r, base2, nw);
-          if (wave_end(nw)) continue;
+          ga_pop_store(v, h);
+          ga_store(R, h);
+          if ((threadIdx.x & 31) == 0) {
+            R->wave_buf = wb;
+            R->spec_from = q;
+            R->pending = shares * kGaPendBias;
+          }
+          __threadfence();
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) {
+            // the other draws go to the ring
+            const int n_t = shares - 1;
+            const unsigned long long base = atomicAdd(&c_ga.ctl[kGaCtlTail],
+                                                      static_cast<unsigned long long>(n_t));
+            // first = L3 when there are L3 trials, else L5; the rest: L5
+            // (when both levels draw) and the speculative stage
+            int kinds[2], nk = 0;
+            if (first == kGaTaskDraw3 && h.n5 > 0) kinds[nk++] = kGaTaskDraw5;
+            kinds[nk++] = kGaTaskSpec;
+            for (int k3 = 0; k3 < nk; ++k3) {
+              const unsigned long long t = base + k3;
+              c_ga.q_pay[t & c_ga.q_mask] =
+                  make_uint2(static_cast<unsigned>(r), static_cast<unsigned>(kinds[k3]));
+              __threadfence();
+              atomicExch(&c_ga.q_seq[t & c_ga.q_mask], t + 1);
+            }
+          }
+          __syncwarp();
+          int dn = 0;
+          GA_PH(2, dn = ga_draw_task(r, first, sm));
+          if (dn) {
+            ga_load(R, h);
+            ga_pop_load(v, h);
+            ga_res_load(v, h);
+            continue;
+          }
           return 0;
         }
-        wave_cancel();
-        h.rng = h.before5;
+        h.before5 = h.rng;
       }
       GA_PH(5, ga_insert_if(v, h));
       h.state = kGaLoop;
@@ -1032,7 +1127,9 @@ __device__ int ga_step(int r, const GaSm& sm) {
       GA_PH(4, w3 = ga_walk(v, h, 0, h.n3, h.before3, R->snaps3));
       if (w3 == 0 && h.used < slice) {
         h.rng = h.before5;
-        if (ga_walk(v, h, h.n3, h.n5, h.before5, R->snaps5) == 0) h.have_spec = 1;
+        int w5 = 0;
+        GA_PH(4, w5 = ga_walk(v, h, h.n3, h.n5, h.before5, R->snaps5));
+        if (w5 == 0) h.have_spec = 1;
       } else if (w3 == 1 && h.used < slice) {
         const int wb2 = 1 - h.wave_buf;
         h.b5 = h.rng;
@@ -1049,7 +1146,7 @@ __device__ int ga_step(int r, const GaSm& sm) {
         }
         wave_cancel();
       }
-      ga_insert_if(v, h);
+      GA_PH(5, ga_insert_if(v, h));
       h.state = kGaLoop;
       continue;
     }
@@ -1117,11 +1214,14 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
     l.n_warps = 1;
     l.job_words[0] = l.job_words[1] = 0;
     l.job = l.job_words;
-    l.cls = P.cls;
+    if (!cv.cls_smem) l.cls = P.cls;  // else carved last (the init scratch stays below it)
     if (blockIdx.x == 0) atomicCAS(&c_ga.ctl[kGaCtlT0], 0ull, ga_timer());
   }
   __syncwarp();
   Ws& s = team[0];
+  // persistent workers: the link-class matrix is staged once
+  if (cv.cls_smem) stage_link_classes(P, s);
+  __syncwarp();
   while (true) {
     // take a ticket, wait for its task (or for the end of the launch)
     unsigned long long t = 0;
@@ -1150,6 +1250,11 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
     int run = static_cast<int>(__shfl_sync(0xffffffffu, pay.x, 0));
     int idx = static_cast<int>(__shfl_sync(0xffffffffu, pay.y, 0));
     while (true) {
+      if (idx <= kGaTaskSpec) {  // one draw of a swap wave
+        if (!ga_draw_task(run, idx, sm)) break;
+        idx = kGaTaskStep;
+        continue;
+      }
       if (idx < 0) {  // GA step (again while its waves finish before it closes them)
         const long long c0 = c_ga.prof ? clock64() : 0;
         const int again = ga_step(run, sm);
@@ -1195,7 +1300,9 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
 cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
                                 const GaParams& G, double* gscratch, int64_t gscratch_doubles,
                                 int n_sm, int& grid, cudaStream_t st) {
-  cv.cls_smem = 0;
+  // small problems: each persistent worker keeps the N x N link-class matrix
+  // in shared memory (after everything else in its carve)
+  cv.cls_smem = P.n_dev * P.n_dev <= 4096 ? 1 : 0;
   cv.n_warps = 1;
   cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave);
   static int configured = 0;

@@ -25,6 +25,9 @@ $R search fixtures/c1.workflow.json fixtures/c1.topology.json 1000 42 $G/search_
 $R search fixtures/c2.workflow.json fixtures/c2.topology.json 1000 42 $G/search_c2_b1000.json $KNOBS
 $R search fixtures/n256.workflow.json fixtures/n256.topology.json 1000 42 $G/search_n256_b1000.json $KNOBS
 $R searchfuzz 777 60 $G/searchfuzz.json
+for c in c1 c2 c3; do
+  $R ga fixtures/$c.workflow.json fixtures/$c.topology.json $G/ga_$c.json $KNOBS
+done
 $R sweep fixtures/c4.workflow.json fixtures/c4.topology.json 42 0 2000 $G/sweep_c4.json
 $R exhaustive 4242 40 $G/exhaustive.json
 python3 - <<'PY'

@@ -156,6 +156,34 @@ def test_search_fuzz_identical():
     assert not bad, "\n".join(bad[:30])
 
 
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3"])
+def test_ga_search_identical(cfg_name):
+    """ga_search on its own (search.hpp:127-135): twelve arms per config with
+    slices 1-400 and random seeds, feasible and infeasible; evaluations used,
+    best member plan (bit-exact weights, splits, assignment), its cost and
+    breakdown."""
+    from paper_2512_12476_b200 import SearchKnobs
+    g = load(f"ga_{cfg_name}.json")
+    knobs = SearchKnobs.from_json(g["knobs"])
+    bad = []
+    with _engine(g["workflow"], g["topology"]) as eng:
+        for i, r in enumerate(g["records"]):
+            res = eng.ga_search(r["groups"], r["counts"], r["slice"], int(r["seed"]), knobs)
+            ctx = f"{cfg_name} arm {i}"
+            if res.consumed != r["evals"]:
+                bad.append(f"{ctx} evals {res.consumed} != {r['evals']}")
+            if bool(res.plan) != bool(r["has_plan"]):
+                bad.append(f"{ctx} has_plan {bool(res.plan)} != {r['has_plan']}")
+                continue
+            if not res.plan:
+                continue
+            bad += _check_plan_eq(res.plan, r["plan"], ctx)
+            if not same(res.arms[0][2], hx(r["cost"])):
+                bad.append(f"{ctx} cost {res.arms[0][2]} != {hx(r['cost'])}")
+            bad += check_breakdown(res.breakdown, r["breakdown"], ctx)
+    assert not bad, "\n".join(bad[:20])
+
+
 def test_sweep_c4_bit_exact():
     """config-5 generator on the GPU reproduces the reference's costs bit for
     bit (plans regenerated on the CPU by ref_dump from the same counters)."""
@@ -240,14 +268,14 @@ def test_host_ga_paths_identical(env):
     """The default search runs ga_run on the device (ga_kernel.cuh). The host
     coroutine GA in lockstep waves (HPG_DEVICE_GA=0), with init candidates
     made by the host pool or on the device (HPG_DEVICE_GEN_MIN=0), gives the
-    same searches: c1/c2 goldens and the 60 search fuzz cases, in a
-    subprocess (the switches are read once)"""
+    same searches: c1/c2/n256 goldens, the 60 search fuzz cases and the
+    ga_search arms, in a subprocess (the switches are read once)"""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
                         os.path.join(here, "test_gpu_parity.py"), "-k",
-                        "search_configs or search_fuzz"],
+                        "search_configs or search_fuzz or ga_search"],
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
