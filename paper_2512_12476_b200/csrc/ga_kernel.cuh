@@ -35,19 +35,27 @@ __device__ __forceinline__ unsigned long long ga_timer() {
   return t;
 }
 
-// next() % n, exactly, through a 128-bit reciprocal (Lemire, Kaser & Kurz
-// 2019; gen_ga.cu bounded_fast, the host's fastmod_u64)
+// next() % n, exactly: for n <= kGaModMax, (hi * 2^32 + lo) % n =
+// ((hi % n) * (2^32 % n) + lo % n) % n, each 32-bit remainder by Lemire's
+// direct method (M = floor((2^64 - 1) / n) + 1; x % n = mulhi(M * x, n),
+// exact for every 32-bit x) from a constant-bank table: no divide, no L2
+// round trip (the workers' L1 is mostly shared memory)
+constexpr int kGaModMax = 1024;
+__constant__ uint64_t c_mod_m[kGaModMax + 1];   // M per divisor
+__constant__ uint32_t c_mod_p32[kGaModMax + 1];  // 2^32 mod n
+
+__device__ __forceinline__ uint32_t ga_mod32(uint32_t x, uint32_t n, uint64_t m) {
+  return static_cast<uint32_t>(__umul64hi(m * x, n));
+}
+
 __device__ __forceinline__ uint64_t ga_bounded(Rng& rng, uint64_t n, const uint64_t* fm) {
+  (void)fm;
   const uint64_t a = rng.next();
-  if (n > static_cast<uint64_t>(kGenFastModMax)) return a % n;
-  const uint64_t mlo = __ldg(fm + 2 * n), mhi = __ldg(fm + 2 * n + 1);
-  const uint64_t low_lo = mlo * a;
-  const uint64_t low_hi = __umul64hi(mlo, a) + mhi * a;
-  const uint64_t bottom = __umul64hi(low_lo, n);
-  const uint64_t top_lo = low_hi * n;
-  const uint64_t top_hi = __umul64hi(low_hi, n);
-  const uint64_t sum_lo = top_lo + bottom;
-  return top_hi + (sum_lo < top_lo ? 1 : 0);
+  if (n > static_cast<uint64_t>(kGaModMax)) return a % n;
+  const uint32_t d = static_cast<uint32_t>(n);
+  const uint64_t m = c_mod_m[d];
+  const uint32_t hi = static_cast<uint32_t>(a >> 32), lo = static_cast<uint32_t>(a);
+  return ga_mod32(ga_mod32(hi, d, m) * c_mod_p32[d] + ga_mod32(lo, d, m), d, m);
 }
 
 __device__ __forceinline__ Rng ga_ld_rng(const Rng* p) {
@@ -70,6 +78,13 @@ __device__ __forceinline__ bool ga_same_rng(const Rng& a, const Rng& b) {
 // the trial being built, the finished wave's results and the population, so
 // that drawing a wave costs a handful of L2 round trips, not one per move.
 struct GaSm {
+  // problem tables staged once per worker (dependent lookups in the draws)
+  const uint8_t* id_rank;     // [N] device -> id rank
+  const uint8_t* by_id_rank;  // [N] id rank -> device
+  const uint8_t* node_rank;   // [N] device -> node rank
+  const uint8_t* node_devs;   // [N] devices in region / node order
+  const int16_t* region_off;  // [regions + 1]
+  const int16_t* node_off;    // [nodes + 1]
   uint8_t* gen;  // init generation scratch (aliases the evaluation carve)
   uint32_t* gw;  // rank set per task group of the current source [kMaxTasks][8]
   uint8_t* child;
@@ -81,8 +96,14 @@ struct GaSm {
   uint64_t* pseq;
 };
 
-__host__ __device__ inline int ga_smem_bytes(int stride, int max_wave) {
-  return 3 * stride + 32 * max_wave + kGaMaxPop * (4 + 8 + 8) + 32 * kMaxTasks;
+__host__ __device__ inline int ga_tables_bytes(int n_dev, int n_regions, int n_nodes) {
+  return (4 * n_dev + 2 * (n_regions + 1) + 2 * (n_nodes + 1) + 15) & ~15;
+}
+
+__host__ __device__ inline int ga_smem_bytes(int stride, int max_wave, int n_dev, int n_regions,
+                                             int n_nodes) {
+  return 3 * stride + 32 * max_wave + kGaMaxPop * (4 + 8 + 8) + 32 * kMaxTasks +
+         ga_tables_bytes(n_dev, n_regions, n_nodes);
 }
 
 struct GaView {
@@ -161,12 +182,12 @@ __device__ __forceinline__ void ga_geo(const uint8_t* rec, int T, GaGeo& g) {
 }
 
 // group_device_set as a bitmask over id ranks (search.cpp:336-341)
-__device__ __forceinline__ void ga_rank_set(const uint8_t* d, int n,
+__device__ __forceinline__ void ga_rank_set(const uint8_t* id_rank, const uint8_t* d, int n,
                                             uint32_t (&w)[8]) {
   const int lane = threadIdx.x & 31;
   uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = lane; i < n; i += 32) {
-    const int r = __ldg(c_ga.id_rank + d[i]);
+    const int r = id_rank[d[i]];
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       if ((r >> 5) == k) m[k] |= 1u << (r & 31);
@@ -175,7 +196,7 @@ __device__ __forceinline__ void ga_rank_set(const uint8_t* d, int n,
   for (int k = 0; k < 8; ++k) w[k] = __reduce_or_sync(0xffffffffu, m[k]);
 }
 
-__device__ __forceinline__ int ga_select_rank(const uint32_t (&w)[8],
+__device__ __forceinline__ int ga_select_rank(const uint8_t* by_id_rank, const uint32_t (&w)[8],
                                               uint64_t idx) {
   for (int k = 0; k < 8; ++k) {
     const uint64_t pc = static_cast<uint64_t>(__popc(w[k]));
@@ -185,7 +206,7 @@ __device__ __forceinline__ int ga_select_rank(const uint32_t (&w)[8],
     }
     uint32_t x = w[k];
     for (uint64_t i = 0; i < idx; ++i) x &= x - 1;
-    return __ldg(c_ga.by_id_rank + 32 * k + __ffs(x) - 1);
+    return by_id_rank[32 * k + __ffs(x) - 1];
   }
   return -1;
 }
@@ -229,7 +250,7 @@ __device__ void ga_src_info(const GaView& v, const uint8_t* src, GaSrcInfo& si) 
   for (int g = 0; g < v.ng; ++g) {
     const int s = v.gslot[v.gstart[g]];
     uint32_t w[8];
-    ga_rank_set(dv + si.geo.off[s], si.geo.off[s + 1] - si.geo.off[s], w);
+    ga_rank_set(v.sm.id_rank, dv + si.geo.off[s], si.geo.off[s + 1] - si.geo.off[s], w);
     if ((threadIdx.x & 31) == 0)
       for (int k = 0; k < 8; ++k) v.sm.gw[g * 8 + k] = w[k];
   }
@@ -255,8 +276,8 @@ __device__ __forceinline__ int ga_lane_move(const GaView& v, const uint8_t* src,
       w1[k] = v.sm.gw[g1 * 8 + k];
       w2[k] = v.sm.gw[g2 * 8 + k];
     }
-    const int b = ga_select_rank(w2, GA_BOUNDED(rng, static_cast<uint64_t>(n2)));
-    const int a = ga_select_rank(w1, GA_BOUNDED(rng, static_cast<uint64_t>(n1)));
+    const int b = ga_select_rank(v.sm.by_id_rank, w2, GA_BOUNDED(rng, static_cast<uint64_t>(n2)));
+    const int a = ga_select_rank(v.sm.by_id_rank, w1, GA_BOUNDED(rng, static_cast<uint64_t>(n1)));
     for (int side = 0; side < 2; ++side) {
       const int g = side ? g2 : g1, from = side ? b : a, to = side ? a : b;
       for (int k = v.gstart[g]; k < v.gstart[g + 1]; ++k) {
@@ -415,95 +436,123 @@ struct GaGenScratch {
 
 // one candidate by this lane: layouts, random_medium_assignment and
 // random_fine_assignment per task of each group (the reference's draws)
-__device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng, uint8_t* rec,
+__device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng_io, uint8_t* rec,
                              const GaGenScratch& sc) {
-    const uint64_t* fm = c_ga.fastmod;
+  // everything the loops touch in registers / restrict pointers: the byte
+  // stores below would otherwise force reloads of the stream state and of
+  // every pointer (char stores alias everything)
+  Rng rng = rng_io;
+  const int lane = sc.lane;
+  int16_t* __restrict__ s16 = sc.s16;
+  uint8_t* __restrict__ s8 = sc.s8;
+  const uint8_t* __restrict__ node_rank = v.sm.node_rank;
+  const uint8_t* __restrict__ node_devs = v.sm.node_devs;
+  const int16_t* __restrict__ region_off = v.sm.region_off;
+  const int16_t* __restrict__ node_off = v.sm.node_off;
+  const int n_regions = c_ga.n_regions, n_nodes = c_ga.n_nodes;
+  const double keep = 1.0 - c_ga.bias;
+#define A16(i) s16[(i) * 32 + lane]
+#define A8(i) s8[(i) * 32 + lane]
   RecOffsets o;
+  const long long p0 = c_ga.prof ? clock64() : 0;
   ga_lane_layouts(v, combo, rec, o);
-  const int o_nodes = c_ga.n_regions, o_cnt = o_nodes + c_ga.max_nodes_per_region,
-            o_start = o_cnt + c_ga.n_nodes, o_fill = o_start + c_ga.n_nodes, o_ranks = o_fill + c_ga.n_nodes;
+  const long long p1 = c_ga.prof ? clock64() : 0;
+  const int o_nodes = n_regions, o_cnt = o_nodes + c_ga.max_nodes_per_region,
+            o_start = o_cnt + n_nodes, o_fill = o_start + n_nodes, o_ranks = o_fill + n_nodes;
   const int o_bucket = c_ga.n_dev;
-  for (int r = 0; r < c_ga.n_regions; ++r) sc.a16(r) = static_cast<int16_t>(r);
-  for (int i = c_ga.n_regions; i > 1; --i) {
-    const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
-    const int16_t t = sc.a16(i - 1);
-    sc.a16(i - 1) = sc.a16(j);
-    sc.a16(j) = t;
+  for (int r = 0; r < n_regions; ++r) A16(r) = static_cast<int16_t>(r);
+  for (int i = n_regions; i > 1; --i) {
+    const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+    const int16_t t = A16(i - 1);
+    A16(i - 1) = A16(j);
+    A16(j) = t;
   }
   int nf = 0;
-  for (int ri = 0; ri < c_ga.n_regions; ++ri) {
-    const int reg = sc.a16(ri);
-    const int n0 = __ldg(c_ga.region_off + reg), nn = __ldg(c_ga.region_off + reg + 1) - n0;
-    for (int q = 0; q < nn; ++q) sc.a16(o_nodes + q) = static_cast<int16_t>(q);
+  for (int ri = 0; ri < n_regions; ++ri) {
+    const int reg = A16(ri);
+    const int n0 = region_off[reg], nn = region_off[reg + 1] - n0;
+    for (int q = 0; q < nn; ++q) A16(o_nodes + q) = static_cast<int16_t>(q);
     for (int i = nn; i > 1; --i) {
-      const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
-      const int16_t t = sc.a16(o_nodes + i - 1);
-      sc.a16(o_nodes + i - 1) = sc.a16(o_nodes + j);
-      sc.a16(o_nodes + j) = t;
+      const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+      const int16_t t = A16(o_nodes + i - 1);
+      A16(o_nodes + i - 1) = A16(o_nodes + j);
+      A16(o_nodes + j) = t;
     }
     for (int q = 0; q < nn; ++q) {
-      const int node = n0 + sc.a16(o_nodes + q);
-      for (int e = __ldg(c_ga.node_off + node); e < __ldg(c_ga.node_off + node + 1); ++e)
-        sc.a8(nf++) = __ldg(c_ga.node_devs + e);
+      const int node = n0 + A16(o_nodes + q);
+      for (int e = node_off[node]; e < node_off[node + 1]; ++e) A8(nf++) = node_devs[e];
     }
   }
   for (int i = nf; i > 1; --i) {
-    const bool scramble = (static_cast<double>(rng.next() >> 11) * 0x1.0p-53) < (1.0 - c_ga.bias);
-    const int pick = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
+    const bool scramble = (static_cast<double>(rng.next() >> 11) * 0x1.0p-53) < keep;
+    const int pick = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
     if (scramble) {
-      const uint8_t t = sc.a8(i - 1);
-      sc.a8(i - 1) = sc.a8(pick);
-      sc.a8(pick) = t;
+      const uint8_t t = A8(i - 1);
+      A8(i - 1) = A8(pick);
+      A8(pick) = t;
     }
   }
-  uint8_t* dv = rec + o.dev_byte;
+  uint8_t* __restrict__ dv = rec + o.dev_byte;
+  int dev_off[kMaxTasks + 1];
+  for (int t = 0; t <= kMaxTasks; ++t) dev_off[t] = o.dev[t];
+  const long long p2 = c_ga.prof ? clock64() : 0;
   int cursor = 0;
   for (int g = 0; g < v.ng; ++g) {
     const int n = v.counts[g];
     for (int k = v.gstart[g]; k < v.gstart[g + 1]; ++k) {
       const int s = v.gslot[k];
-      for (int r = 0; r < c_ga.n_nodes; ++r) sc.a16(o_cnt + r) = 0;
-      for (int i = 0; i < n; ++i) ++sc.a16(o_cnt + __ldg(c_ga.node_rank + sc.a8(cursor + i)));
+      for (int r = 0; r < n_nodes; ++r) A16(o_cnt + r) = 0;
+      for (int i = 0; i < n; ++i) ++A16(o_cnt + node_rank[A8(cursor + i)]);
       int nr = 0, acc = 0;
-      for (int r = 0; r < c_ga.n_nodes; ++r) {
-        const int c = sc.a16(o_cnt + r);
+      for (int r = 0; r < n_nodes; ++r) {
+        const int c = A16(o_cnt + r);
         if (!c) continue;
-        sc.a16(o_ranks + nr++) = static_cast<int16_t>(r);
-        sc.a16(o_start + r) = static_cast<int16_t>(acc);
+        A16(o_ranks + nr++) = static_cast<int16_t>(r);
+        A16(o_start + r) = static_cast<int16_t>(acc);
         acc += c;
       }
       for (int q = 0; q < nr; ++q) {
-        const int rk = sc.a16(o_ranks + q);
-        sc.a16(o_fill + rk) = sc.a16(o_start + rk);
+        const int rk = A16(o_ranks + q);
+        A16(o_fill + rk) = A16(o_start + rk);
       }
       for (int i = 0; i < n; ++i) {
-        const uint8_t d = sc.a8(cursor + i);
-        int16_t& f = sc.a16(o_fill + __ldg(c_ga.node_rank + d));
-        sc.a8(o_bucket + f) = d;
-        ++f;
+        const uint8_t d = A8(cursor + i);
+        const int fi = o_fill + node_rank[d];
+        const int f = A16(fi);
+        A8(o_bucket + f) = d;
+        A16(fi) = static_cast<int16_t>(f + 1);
       }
       for (int i = nr; i > 1; --i) {
-        const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
-        const int16_t t = sc.a16(o_ranks + i - 1);
-        sc.a16(o_ranks + i - 1) = sc.a16(o_ranks + j);
-        sc.a16(o_ranks + j) = t;
+        const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+        const int16_t t = A16(o_ranks + i - 1);
+        A16(o_ranks + i - 1) = A16(o_ranks + j);
+        A16(o_ranks + j) = t;
       }
-      uint8_t* out = dv + o.dev[s];
+      uint8_t* __restrict__ out = dv + dev_off[s];
       int pos = 0;
       for (int q = 0; q < nr; ++q) {
-        const int rk = sc.a16(o_ranks + q);
-        const int b0 = o_bucket + sc.a16(o_start + rk);
-        const int nb = sc.a16(o_cnt + rk);
+        const int rk = A16(o_ranks + q);
+        const int b0 = o_bucket + A16(o_start + rk);
+        const int nb = A16(o_cnt + rk);
         for (int i = nb; i > 1; --i) {
-          const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
-          const uint8_t t = sc.a8(b0 + i - 1);
-          sc.a8(b0 + i - 1) = sc.a8(b0 + j);
-          sc.a8(b0 + j) = t;
+          const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+          const uint8_t t = A8(b0 + i - 1);
+          A8(b0 + i - 1) = A8(b0 + j);
+          A8(b0 + j) = t;
         }
-        for (int i = 0; i < nb; ++i) out[pos++] = sc.a8(b0 + i);
+        for (int i = 0; i < nb; ++i) out[pos++] = A8(b0 + i);
       }
     }
     cursor += n;
+  }
+#undef A16
+#undef A8
+  rng_io = rng;
+  if (c_ga.prof && lane == 1) {  // diagnostics: layouts, medium, fine
+    atomicAdd(&c_ga.ctl[99], static_cast<unsigned long long>(p1 - p0));
+    atomicAdd(&c_ga.ctl[125], static_cast<unsigned long long>(p2 - p1));
+    atomicAdd(&c_ga.ctl[126], static_cast<unsigned long long>(clock64() - p2));
+    atomicAdd(&c_ga.ctl[127], 1ull);
   }
 }
 
@@ -523,11 +572,21 @@ __device__ void ga_init_chunk(const GaView& v, const Rng& rng, int64_t combo0, i
   Rng r = rng;
   // lane c starts c candidates (c * gen_draws values) into the chunk, then
   // moves 31 candidates ahead after each of its candidates
+  const long long t0 = c_ga.prof ? clock64() : 0;
   if (lane > 0 && lane < n) rng_apply_jump(r, jumps + 4 * (lane - 1));
+  const long long t1 = c_ga.prof ? clock64() : 0;
+  long long tj = 0;
   for (int c = lane; c < n; c += 32) {
+    const long long a = c_ga.prof ? clock64() : 0;
     if (c > lane) rng_apply_jump(r, jumps + 4 * 30);
+    if (c_ga.prof) tj += clock64() - a;
     ga_lane_make(v, combo0 + c, r, v.wave_slot(0, c), sc);
     snaps[c] = r;
+  }
+  if (c_ga.prof && lane == 1 && n > 1) {  // diagnostics: first jump, later jumps, total
+    atomicAdd(&c_ga.ctl[111], static_cast<unsigned long long>(t1 - t0));
+    atomicAdd(&c_ga.ctl[97], static_cast<unsigned long long>(tj));
+    atomicAdd(&c_ga.ctl[98], static_cast<unsigned long long>(clock64() - t0));
   }
   __threadfence_block();
   __syncwarp();
@@ -1203,6 +1262,30 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
     sm.pslot = reinterpret_cast<int32_t*>(sm.pseq + kGaMaxPop);
     sm.gw = reinterpret_cast<uint32_t*>(sm.pslot + kGaMaxPop);
     sm.gen = smem;
+    uint8_t* tb = reinterpret_cast<uint8_t*>(sm.gw + 8 * kMaxTasks);
+    const int N = c_ga.n_dev;
+    uint8_t* id_rank = tb;
+    uint8_t* by_id_rank = tb + N;
+    uint8_t* node_rank = tb + 2 * N;
+    uint8_t* node_devs = tb + 3 * N;
+    int16_t* region_off = reinterpret_cast<int16_t*>(tb + 4 * N);
+    int16_t* node_off = region_off + c_ga.n_regions + 1;
+    const int lane0 = threadIdx.x & 31;
+    for (int i = lane0; i < N; i += 32) {
+      id_rank[i] = static_cast<uint8_t>(c_ga.id_rank[i]);
+      by_id_rank[i] = static_cast<uint8_t>(c_ga.by_id_rank[i]);
+      node_rank[i] = static_cast<uint8_t>(c_ga.node_rank[i]);
+      node_devs[i] = c_ga.node_devs[i];
+    }
+    for (int i = lane0; i <= c_ga.n_regions; i += 32) region_off[i] = static_cast<int16_t>(c_ga.region_off[i]);
+    for (int i = lane0; i <= c_ga.n_nodes; i += 32) node_off[i] = static_cast<int16_t>(c_ga.node_off[i]);
+    sm.id_rank = id_rank;
+    sm.by_id_rank = by_id_rank;
+    sm.node_rank = node_rank;
+    sm.node_devs = node_devs;
+    sm.region_off = region_off;
+    sm.node_off = node_off;
+    __syncwarp();
   }
   if (lane == 0) {
     Ws& l = team[0];
@@ -1304,7 +1387,8 @@ cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, C
   // in shared memory (after everything else in its carve)
   cv.cls_smem = P.n_dev * P.n_dev <= 4096 ? 1 : 0;
   cv.n_warps = 1;
-  cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave);
+  cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave, G.n_dev, G.n_regions,
+                                                    G.n_nodes);
   static int configured = 0;
   if (cv.bytes > configured) {
     const cudaError_t e = cudaFuncSetAttribute(
@@ -1317,6 +1401,22 @@ cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, C
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   grid = n_sm * per_sm;
+  static bool mod_tables = false;
+  if (!mod_tables) {
+    static uint64_t mm[dev::kGaModMax + 1];
+    static uint32_t p32[dev::kGaModMax + 1];
+    mm[0] = 0;
+    p32[0] = 0;
+    for (int d = 1; d <= dev::kGaModMax; ++d) {
+      mm[d] = ~uint64_t(0) / static_cast<uint64_t>(d) + 1;
+      p32[d] = static_cast<uint32_t>((uint64_t(1) << 32) % static_cast<uint64_t>(d));
+    }
+    e = cudaMemcpyToSymbol(dev::c_mod_m, mm, sizeof(mm));
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyToSymbol(dev::c_mod_p32, p32, sizeof(p32));
+    if (e != cudaSuccess) return e;
+    mod_tables = true;
+  }
   e = cudaMemcpyToSymbolAsync(dev::c_ga, &G, sizeof(GaParams), 0, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   dev::ga_kernel<<<grid, 32, cv.bytes, st>>>(P, cfg, cv, gscratch, gscratch_doubles);

@@ -1106,8 +1106,15 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
       for (int q = 0; q < 8; ++q)
         std::fprintf(f, " %.1f", pf[1] ? 1e-3 * hctl[100 + q] / pf[1] : 0.0);
       // init chunks: kcycles per chunk, chunks, candidates
-      std::fprintf(f, " | init %.1f %llu %llu\n", hctl[109] ? 1e-3 * hctl[108] / hctl[109] : 0.0,
-                   hctl[109], hctl[110]);
+      std::fprintf(f, " | init %.1f %llu %llu | lane1 jump0 %.1f jumps %.1f total %.1f\n",
+                   hctl[109] ? 1e-3 * hctl[108] / hctl[109] : 0.0, hctl[109], hctl[110],
+                   hctl[109] ? 1e-3 * hctl[111] / hctl[109] : 0.0,
+                   hctl[109] ? 1e-3 * hctl[97] / hctl[109] : 0.0,
+                   hctl[109] ? 1e-3 * hctl[98] / hctl[109] : 0.0);
+      std::fprintf(f, "    make: layouts %.1f medium %.1f fine %.1f kcycles (n %llu) gen_in_smem %d\n",
+                   hctl[127] ? 1e-3 * hctl[99] / hctl[127] : 0.0,
+                   hctl[127] ? 1e-3 * hctl[125] / hctl[127] : 0.0,
+                   hctl[127] ? 1e-3 * hctl[126] / hctl[127] : 0.0, hctl[127], G.gen_in_smem);
       std::fclose(f);
     }
   }
