@@ -41,6 +41,7 @@ enum GaState : int32_t {
   kGaDone = 4,
   kGaInit = 5,      // draw the next init chunk
   kGaInitDone = 6,  // take the chunk's results
+  kGaSwap3 = 7,     // throughput mode: the L3-only swap wave finished
 };
 
 struct alignas(16) GaRun {
@@ -138,6 +139,7 @@ struct GaParams {
   const int16_t* node_rank;
   int64_t task_nl[kMaxTasks];
   int32_t max_stride;  // record slot stride (multiple of 16)
+  int32_t split_runs;  // more live runs than this: swap waves without L5 / speculation up front
   int32_t prof;        // diagnostics: cycle counters in ctl[kGaCtlProf..]
 };
 

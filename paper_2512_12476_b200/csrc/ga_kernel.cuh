@@ -1125,6 +1125,39 @@ __device__ int ga_step(int r, const GaSm& sm) {
         h.n3 = v.ng >= 2 && sps > 0 ? sps : 0;
         h.n5 = ne > 0 && sps > 0 ? sps : 0;
         h.before3 = h.rng;
+        // throughput mode (many live runs: the GPU is busy with evaluations):
+        // the L3 trials alone first; L5 and the speculative stage follow only
+        // if no L3 trial is accepted (as a redraw wave from the same stream
+        // position), which spends fewer evaluations per offspring
+        const bool split = h.n3 > 0 && static_cast<long long>(c_ga.n_runs) -
+                                               static_cast<long long>(__ldcg(&c_ga.ctl[kGaCtlDone])) >
+                                           c_ga.split_runs;
+        if (split) {
+          Rng q = h.rng;
+          for (int k2 = 0; k2 < 4 * h.n3; ++k2) q.next();
+          h.before5 = q;
+          h.wave_buf = wb;
+          ++h.n_waves;
+          h.state = kGaSwap3;
+          ga_pop_store(v, h);
+          ga_store(R, h);
+          if ((threadIdx.x & 31) == 0) {
+            R->wave_buf = wb;
+            R->wave_n = h.n3;
+            R->pending = kGaPendBias;
+          }
+          __threadfence();
+          __syncwarp();
+          int dn = 0;
+          GA_PH(2, dn = ga_draw_task(r, kGaTaskDraw3, sm));
+          if (dn) {
+            ga_load(R, h);
+            ga_pop_load(v, h);
+            ga_res_load(v, h);
+            continue;
+          }
+          return 0;
+        }
         if (h.n3 + h.n5 > 0) {
           Rng q = h.rng;
           for (int k2 = 0; k2 < 4 * h.n3; ++k2) q.next();
@@ -1190,7 +1223,34 @@ __device__ int ga_step(int r, const GaSm& sm) {
         GA_PH(4, w5 = ga_walk(v, h, h.n3, h.n5, h.before5, R->snaps5));
         if (w5 == 0) h.have_spec = 1;
       } else if (w3 == 1 && h.used < slice) {
-        const int wb2 = 1 - h.wave_buf;
+        const int wb2 = 1 - h.child_buf;
+        h.b5 = h.rng;
+        wave_begin(wb2);
+        h.m5 = ga_draw(v, h, 5, wb2, 0, R->snaps5);
+        ga_publish(r, 0, h.m5);
+        if (h.m5 > 0) {
+          ga_speculate(v, h, ga_ld_rng(&R->snaps5[h.m5 - 1]), wb2, h.m5);
+          h.state = kGaRedraw;
+          const int nw = h.m5 + __ldcg(&R->spec.ntr) + 1;
+          ga_publish(r, h.m5, nw);
+          if (wave_end(nw)) continue;
+          return 0;
+        }
+        wave_cancel();
+      }
+      GA_PH(5, ga_insert_if(v, h));
+      h.state = kGaLoop;
+      continue;
+    }
+    if (h.state == kGaSwap3) {
+      // the L3-only wave: then the L5 trials (+ speculation) from the child,
+      // whichever it is now, at the stream position the walk leaves: the
+      // L3 walk's acceptance point, or the end of the L3 draws
+      h.rng = h.before5;
+      int w3 = 0;
+      GA_PH(4, w3 = ga_walk(v, h, 0, h.n3, h.before3, R->snaps3));
+      if ((w3 == 0 || w3 == 1) && h.used < slice) {
+        const int wb2 = 1 - h.child_buf;
         h.b5 = h.rng;
         wave_begin(wb2);
         h.m5 = ga_draw(v, h, 5, wb2, 0, R->snaps5);
@@ -1417,7 +1477,9 @@ cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, C
     if (e != cudaSuccess) return e;
     mod_tables = true;
   }
-  e = cudaMemcpyToSymbolAsync(dev::c_ga, &G, sizeof(GaParams), 0, cudaMemcpyHostToDevice, st);
+  GaParams g2 = G;
+  if (g2.split_runs < 0) g2.split_runs = grid / 16;  // ~one swap wave per run fills the workers
+  e = cudaMemcpyToSymbolAsync(dev::c_ga, &g2, sizeof(GaParams), 0, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   dev::ga_kernel<<<grid, 32, cv.bytes, st>>>(P, cfg, cv, gscratch, gscratch_doubles);
   return cudaGetLastError();

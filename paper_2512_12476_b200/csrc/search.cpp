@@ -987,6 +987,11 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   G.kb_flags = kb;
   G.n_tasks = P.T;
   G.max_stride = stride;
+  static const int split_env = [] {
+    const char* e = std::getenv("HPG_GA_SPLIT_RUNS");  // diagnostics: live-run threshold
+    return e ? std::atoi(e) : -1;
+  }();
+  G.split_runs = split_env;  // -1: grid / 16 (launch_ga_offspring)
   G.fastmod = gt.fastmod;
   G.opts = reinterpret_cast<const short4*>(D + o_opts);
   G.init_snaps = reinterpret_cast<Rng*>(D + o_snaps);
