@@ -122,7 +122,6 @@ struct GaParams {
   GaImpr* impr;
   int64_t impr_cap;
   int32_t kb_flags, n_tasks;
-  const uint64_t* fastmod;  // bounded() reciprocals (gen_ga.hpp GenTablesDev::fastmod)
   // init phase: candidate generation (make_candidate on the device)
   const short4* opts;        // layout options (dp, pp, tp, -)
   Rng* init_snaps;           // [run][init_cap] stream after each init candidate

@@ -21,7 +21,7 @@
 #include "gen_ga.hpp"
 #include "rng_jump.hpp"
 
-#define GA_BOUNDED(r, n) ga_bounded(r, n, c_ga.fastmod)
+#define GA_BOUNDED(r, n) ga_bounded(r, n)
 
 namespace hpg {
 namespace dev {
@@ -48,8 +48,7 @@ __device__ __forceinline__ uint32_t ga_mod32(uint32_t x, uint32_t n, uint64_t m)
   return static_cast<uint32_t>(__umul64hi(m * x, n));
 }
 
-__device__ __forceinline__ uint64_t ga_bounded(Rng& rng, uint64_t n, const uint64_t* fm) {
-  (void)fm;
+__device__ __forceinline__ uint64_t ga_bounded(Rng& rng, uint64_t n) {
   const uint64_t a = rng.next();
   if (n > static_cast<uint64_t>(kGaModMax)) return a % n;
   const uint32_t d = static_cast<uint32_t>(n);
@@ -413,16 +412,6 @@ __device__ void ga_lane_layouts(const GaView& v, int64_t combo, uint8_t* rec, Re
   for (int i = o.dev_byte + o.dev[c_ga.n_tasks]; i < o.bytes; ++i) rec[i] = 0;  // padding
 }
 
-template <typename T>
-__device__ __forceinline__ void ga_shuffle(Rng& rng, T* a, int n, const uint64_t* fm) {
-  for (int i = n; i > 1; --i) {
-    const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), fm));
-    const T tmp = a[i - 1];
-    a[i - 1] = a[j];
-    a[j] = tmp;
-  }
-}
-
 // per-lane generation scratch, interleaved across the warp's lanes (element
 // i of a lane's array at [i][lane]): in shared memory (aliasing the idle
 // evaluation carve) or, for large problems, in the worker's global scratch
@@ -462,7 +451,7 @@ __device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng_io, uint8_
   const int o_bucket = c_ga.n_dev;
   for (int r = 0; r < n_regions; ++r) A16(r) = static_cast<int16_t>(r);
   for (int i = n_regions; i > 1; --i) {
-    const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+    const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i)));
     const int16_t t = A16(i - 1);
     A16(i - 1) = A16(j);
     A16(j) = t;
@@ -473,7 +462,7 @@ __device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng_io, uint8_
     const int n0 = region_off[reg], nn = region_off[reg + 1] - n0;
     for (int q = 0; q < nn; ++q) A16(o_nodes + q) = static_cast<int16_t>(q);
     for (int i = nn; i > 1; --i) {
-      const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+      const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i)));
       const int16_t t = A16(o_nodes + i - 1);
       A16(o_nodes + i - 1) = A16(o_nodes + j);
       A16(o_nodes + j) = t;
@@ -485,7 +474,7 @@ __device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng_io, uint8_
   }
   for (int i = nf; i > 1; --i) {
     const bool scramble = (static_cast<double>(rng.next() >> 11) * 0x1.0p-53) < keep;
-    const int pick = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+    const int pick = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i)));
     if (scramble) {
       const uint8_t t = A8(i - 1);
       A8(i - 1) = A8(pick);
@@ -523,7 +512,7 @@ __device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng_io, uint8_
         A16(fi) = static_cast<int16_t>(f + 1);
       }
       for (int i = nr; i > 1; --i) {
-        const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+        const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i)));
         const int16_t t = A16(o_ranks + i - 1);
         A16(o_ranks + i - 1) = A16(o_ranks + j);
         A16(o_ranks + j) = t;
@@ -535,7 +524,7 @@ __device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng_io, uint8_
         const int b0 = o_bucket + A16(o_start + rk);
         const int nb = A16(o_cnt + rk);
         for (int i = nb; i > 1; --i) {
-          const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i), nullptr));
+          const int j = static_cast<int>(ga_bounded(rng, static_cast<uint64_t>(i)));
           const uint8_t t = A8(b0 + i - 1);
           A8(b0 + i - 1) = A8(b0 + j);
           A8(b0 + j) = t;

@@ -992,7 +992,6 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
     return e ? std::atoi(e) : -1;
   }();
   G.split_runs = split_env;  // -1: grid / 16 (launch_ga_offspring)
-  G.fastmod = gt.fastmod;
   G.opts = reinterpret_cast<const short4*>(D + o_opts);
   G.init_snaps = reinterpret_cast<Rng*>(D + o_snaps);
   G.jumps = reinterpret_cast<const uint64_t*>(D + o_jump);
