@@ -1291,14 +1291,19 @@ __device__ __forceinline__ long long ga_canonical(const DevProblem& P, const uin
   return cb;
 }
 
-__global__ void __launch_bounds__(32, 16)
+// kTeam = 1: one-warp workers (busy rounds); kTeam = 2: each worker has a
+// helper warp for the per-task parts of an evaluation (eval_kernel's teams),
+// for rounds with few live runs where an evaluation's latency is the chain
+template <int kTeam>
+__global__ void __launch_bounds__(32 * kTeam, 16 / kTeam)
 ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscratch,
           int64_t gscratch_doubles) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ Ws team[1];
+  __shared__ Ws team[kTeam];
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   GaSm sm;
-  {
+  if (warp == 0) {
     // GA scratch after the evaluation carve (launch_ga_offspring sizes it)
     uint8_t* p = smem + carve2_bytes(cv);
     const int stride = c_ga.max_stride;
@@ -1336,24 +1341,32 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
     sm.node_off = node_off;
     __syncwarp();
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     Ws& l = team[0];
-    carve(l, smem, cv);
+    uint8_t* p = carve(l, smem, cv);
     l.dtab = gscratch + static_cast<int64_t>(blockIdx.x) * gscratch_doubles;
     l.dtab_stride = 0;
     l.prof = nullptr;
     l.team = team;
-    l.n_warps = 1;
+    l.n_warps = kTeam;
     l.job_words[0] = l.job_words[1] = 0;
     l.job = l.job_words;
     if (!cv.cls_smem) l.cls = P.cls;  // else carved last (the init scratch stays below it)
+    for (int w = 1; w < kTeam; ++w) {
+      team[w] = l;
+      p = carve_team_scratch(team[w], p, cv);
+    }
     if (blockIdx.x == 0) atomicCAS(&c_ga.ctl[kGaCtlT0], 0ull, ga_timer());
   }
-  __syncwarp();
+  __syncthreads();
   Ws& s = team[0];
   // persistent workers: the link-class matrix is staged once
-  if (cv.cls_smem) stage_link_classes(P, s);
-  __syncwarp();
+  if (warp == 0 && cv.cls_smem) stage_link_classes(P, s);
+  __syncthreads();
+  if (warp > 0) {  // helper: per-task jobs of warp 0's evaluations
+    team_helper(P, cfg, team, warp);
+    return;
+  }
   while (true) {
     // take a ticket, wait for its task (or for the end of the launch)
     unsigned long long t = 0;
@@ -1425,28 +1438,29 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
       idx = -1;  // this warp finished the wave: continue the run
     }
   }
+  team_exit(s);
 }
 
 }  // namespace dev
 
-cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
-                                const GaParams& G, double* gscratch, int64_t gscratch_doubles,
-                                int n_sm, int& grid, cudaStream_t st) {
-  // small problems: each persistent worker keeps the N x N link-class matrix
-  // in shared memory (after everything else in its carve)
-  cv.cls_smem = P.n_dev * P.n_dev <= 4096 ? 1 : 0;
-  cv.n_warps = 1;
+namespace {
+template <int kTeam>
+cudaError_t ga_launch_team(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
+                           const GaParams& G, double* gscratch, int64_t gscratch_doubles,
+                           int n_sm, int& grid, cudaStream_t st) {
+  auto kern = dev::ga_kernel<kTeam>;
+  cv.n_warps = kTeam;
   cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave, G.n_dev, G.n_regions,
                                                     G.n_nodes);
   static int configured = 0;
+  cudaError_t e;
   if (cv.bytes > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(
-        dev::ga_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
     if (e != cudaSuccess) return e;
     configured = cv.bytes;
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::ga_kernel, 32, cv.bytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kTeam, cv.bytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   grid = n_sm * per_sm;
@@ -1470,8 +1484,32 @@ cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, C
   if (g2.split_runs < 0) g2.split_runs = grid / 16;  // ~one swap wave per run fills the workers
   e = cudaMemcpyToSymbolAsync(dev::c_ga, &g2, sizeof(GaParams), 0, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
-  dev::ga_kernel<<<grid, 32, cv.bytes, st>>>(P, cfg, cv, gscratch, gscratch_doubles);
+  kern<<<grid, 32 * kTeam, cv.bytes, st>>>(P, cfg, cv, gscratch, gscratch_doubles);
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
+                                const GaParams& G, double* gscratch, int64_t gscratch_doubles,
+                                int n_sm, int& grid, cudaStream_t st) {
+  // small problems: each persistent worker keeps the N x N link-class matrix
+  // in shared memory (after everything else in its carve)
+  cv.cls_smem = P.n_dev * P.n_dev <= 4096 ? 1 : 0;
+  // few live runs (one wave of every run fits on half the SMs' worker slots):
+  // workers with a helper warp, which shortens each evaluation
+  static const int team_env = [] {
+    const char* v = std::getenv("HPG_GA_TEAM");  // diagnostics: 1 or 2 forces the team size
+    return v ? std::atoi(v) : 0;
+  }();
+  const bool pair = team_env == 2 ||
+                    (team_env == 0 && P.n_tasks >= 2 &&
+                     static_cast<int64_t>(G.n_runs) * G.max_wave <= 4 * static_cast<int64_t>(n_sm));
+  if (pair) {
+    const cudaError_t e = ga_launch_team<2>(P, cfg, cv, G, gscratch, gscratch_doubles, n_sm, grid, st);
+    if (e != cudaErrorInvalidConfiguration) return e;
+    (void)cudaGetLastError();
+  }
+  return ga_launch_team<1>(P, cfg, cv, G, gscratch, gscratch_doubles, n_sm, grid, st);
 }
 
 }  // namespace hpg
