@@ -1293,9 +1293,10 @@ __device__ __forceinline__ long long ga_canonical(const DevProblem& P, const uin
 
 // kTeam = 1: one-warp workers (busy rounds); kTeam = 2: each worker has a
 // helper warp for the per-task parts of an evaluation (eval_kernel's teams),
-// for rounds with few live runs where an evaluation's latency is the chain
+// for rounds with few live runs where an evaluation's latency is the chain;
+// kTeam = 4: three helpers, registers uncapped (the last, narrowest rounds)
 template <int kTeam>
-__global__ void __launch_bounds__(32 * kTeam, 16 / kTeam)
+__global__ void __launch_bounds__(32 * kTeam, kTeam == 4 ? 2 : 16 / kTeam)
 ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscratch,
           int64_t gscratch_doubles) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1495,16 +1496,24 @@ cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, C
   // small problems: each persistent worker keeps the N x N link-class matrix
   // in shared memory (after everything else in its carve)
   cv.cls_smem = P.n_dev * P.n_dev <= 4096 ? 1 : 0;
-  // few live runs (one wave of every run fits on half the SMs' worker slots):
-  // workers with a helper warp, which shortens each evaluation
+  // few live runs (at most one per SM): workers with helper warps, which
+  // shorten each evaluation (measured per SHA round on c1-c4: teams of four
+  // win whenever runs <= SMs and lose throughput in the wide early rounds)
   static const int team_env = [] {
-    const char* v = std::getenv("HPG_GA_TEAM");  // diagnostics: 1 or 2 forces the team size
+    const char* v = std::getenv("HPG_GA_TEAM");  // diagnostics: 1, 2 or 4 forces the team size
     return v ? std::atoi(v) : 0;
   }();
-  const bool pair = team_env == 2 ||
-                    (team_env == 0 && P.n_tasks >= 2 &&
-                     static_cast<int64_t>(G.n_runs) * G.max_wave <= 4 * static_cast<int64_t>(n_sm));
-  if (pair) {
+  int team = 1;
+  if (team_env == 1 || team_env == 2 || team_env == 4)
+    team = team_env;
+  else if (P.n_tasks >= 2 && G.n_runs <= n_sm)
+    team = P.n_tasks >= 3 ? 4 : 2;
+  if (team == 4) {
+    const cudaError_t e = ga_launch_team<4>(P, cfg, cv, G, gscratch, gscratch_doubles, n_sm, grid, st);
+    if (e != cudaErrorInvalidConfiguration) return e;
+    (void)cudaGetLastError();
+  }
+  if (team >= 2) {
     const cudaError_t e = ga_launch_team<2>(P, cfg, cv, G, gscratch, gscratch_doubles, n_sm, grid, st);
     if (e != cudaErrorInvalidConfiguration) return e;
     (void)cudaGetLastError();
