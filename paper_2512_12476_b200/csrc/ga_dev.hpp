@@ -24,6 +24,7 @@ constexpr int kGaTrials = 8;      // mutation tries per offspring (search.cpp:49
 constexpr int kGaMaxPop = 64;     // population knob limit of the device path
 constexpr int kGaMaxSps = 16;     // swap_pair_sample limit of the device path
 constexpr int kGaStreakCap = 64;  // infeasible-offspring streak (search.cpp:481)
+constexpr int kGaJumps = 127;     // jump polynomials per gen_draws: lane offsets of a 4-warp team
 
 // a mutation stage: ntr mutated trials + the unmutated parent at
 // stage buffer `buf`, indices [base, base + ntr]

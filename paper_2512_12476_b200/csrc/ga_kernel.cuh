@@ -93,6 +93,8 @@ struct GaSm {
   int32_t* pslot;
   double* pcost;
   uint64_t* pseq;
+  struct GaInitJob* ijob;  // team job slot for init chunks (teams only)
+  int n_warps;             // warps per worker
 };
 
 __host__ __device__ inline int ga_tables_bytes(int n_dev, int n_regions, int n_nodes) {
@@ -121,6 +123,15 @@ struct GaView {
   __device__ uint8_t* wave_slot(int buf, int i) const {
     return slot(2 + c_ga.pop_cap + buf * c_ga.max_wave + i);
   }
+};
+
+// an init chunk posted to the team's helper warps (kJobGaInit)
+constexpr int kJobGaInit = 16;
+struct GaInitJob {
+  GaView v;
+  Rng rng;
+  int64_t combo0;
+  int n, kind;
 };
 
 // global record -> shared (one round trip: the whole slot)
@@ -545,37 +556,70 @@ __device__ void ga_lane_make(const GaView& v, int64_t combo, Rng& rng_io, uint8_
   }
 }
 
-// an init chunk: candidates combo0 + c for c < n from stream state rng, one
-// lane each (lane c steps the stream c * gen_draws values ahead); the stream
-// after candidate c is kept for the chunk's walk
-__device__ void ga_init_chunk(const GaView& v, const Rng& rng, int64_t combo0, int n) {
+// an init chunk's candidates on team lane tl of L (tl = 32 * warp + lane):
+// candidates combo0 + c for c = tl, tl + L, ... < n from stream state rng
+// (lane tl steps the stream tl * gen_draws values ahead, then L - 1
+// candidates ahead after each of its candidates); the stream after candidate
+// c is kept for the chunk's walk. base: this warp's generation scratch.
+__device__ void ga_init_part(const GaView& v, const Rng& rng, int64_t combo0, int n, int tl, int L,
+                             uint8_t* base) {
   const int lane = threadIdx.x & 31;
   const uint64_t* jumps = c_ga.jumps + 4 * static_cast<int64_t>(__ldcg(&v.R->jump_off));
   Rng* snaps = c_ga.init_snaps + static_cast<int64_t>(v.run) * c_ga.init_cap;
   GaGenScratch sc;
-  uint8_t* base = c_ga.gen_in_smem ? v.sm.gen : c_ga.gen_scratch + static_cast<int64_t>(blockIdx.x) *
-                                                                     c_ga.gen_smem * 32;
   sc.s16 = reinterpret_cast<int16_t*>(base);
   sc.s8 = base + 64 * (c_ga.n_regions + c_ga.max_nodes_per_region + 4 * c_ga.n_nodes);
   sc.lane = lane;
   Rng r = rng;
-  // lane c starts c candidates (c * gen_draws values) into the chunk, then
-  // moves 31 candidates ahead after each of its candidates
   const long long t0 = c_ga.prof ? clock64() : 0;
-  if (lane > 0 && lane < n) rng_apply_jump(r, jumps + 4 * (lane - 1));
+  if (tl > 0 && tl < n) rng_apply_jump(r, jumps + 4 * (tl - 1));
   const long long t1 = c_ga.prof ? clock64() : 0;
   long long tj = 0;
-  for (int c = lane; c < n; c += 32) {
+  for (int c = tl; c < n; c += L) {
     const long long a = c_ga.prof ? clock64() : 0;
-    if (c > lane) rng_apply_jump(r, jumps + 4 * 30);
+    if (c > tl) rng_apply_jump(r, jumps + 4 * (L - 2));
     if (c_ga.prof) tj += clock64() - a;
     ga_lane_make(v, combo0 + c, r, v.wave_slot(0, c), sc);
     snaps[c] = r;
   }
-  if (c_ga.prof && lane == 1 && n > 1) {  // diagnostics: first jump, later jumps, total
+  if (c_ga.prof && tl == 1 && n > 1) {  // diagnostics: first jump, later jumps, total
     atomicAdd(&c_ga.ctl[111], static_cast<unsigned long long>(t1 - t0));
     atomicAdd(&c_ga.ctl[97], static_cast<unsigned long long>(tj));
     atomicAdd(&c_ga.ctl[98], static_cast<unsigned long long>(clock64() - t0));
+  }
+}
+
+// a helper warp's generation scratch (global; warp 0 keeps its own slot)
+__device__ __forceinline__ uint8_t* ga_helper_gen(int w, int n_warps) {
+  const int64_t slot = gridDim.x + static_cast<int64_t>(blockIdx.x) * (n_warps - 1) + (w - 1);
+  return c_ga.gen_scratch + slot * c_ga.gen_smem * 32;
+}
+
+// an init chunk (warp 0 of a worker): one candidate per lane, over the whole
+// team when the chunk is wider than a warp (the helpers wait on the team's
+// job barrier between evaluations)
+__device__ void ga_init_chunk(const GaView& v, const Rng& rng, int64_t combo0, int n) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* base = c_ga.gen_in_smem ? v.sm.gen : c_ga.gen_scratch + static_cast<int64_t>(blockIdx.x) *
+                                                                     c_ga.gen_smem * 32;
+  const int nw = v.sm.n_warps;
+  if (nw > 1 && n > 32) {
+    GaInitJob* j = v.sm.ijob;
+    if (lane == 0) {
+      j->v = v;
+      j->rng = rng;
+      j->combo0 = combo0;
+      j->n = n;
+      j->kind = kJobGaInit;
+    }
+    __syncwarp();
+    bar_sync(1, 32 * nw);
+    ga_init_part(v, rng, combo0, n, lane, 32 * nw, base);
+    __threadfence();
+    bar_sync(2, 32 * nw);
+    if (lane == 0) j->kind = 0;
+  } else {
+    ga_init_part(v, rng, combo0, n, lane, 32, base);
   }
   __threadfence_block();
   __syncwarp();
@@ -1291,6 +1335,44 @@ __device__ __forceinline__ long long ga_canonical(const DevProblem& P, const uin
   return cb;
 }
 
+// helper warps of a GA worker: init-chunk candidates (kJobGaInit) and the
+// per-task parts of the lead's evaluations (team_helper's jobs)
+__device__ __noinline__ void ga_team_helper(const DevProblem& P, const DevCostConfig& cfg, Ws* team,
+                                            int w, const GaInitJob* ij) {
+  const int lane = threadIdx.x & 31;
+  Ws& s = team[w];
+  const Ws& s0 = team[0];
+  const int threads = 32 * s.n_warps;
+  uint8_t* gen = ga_helper_gen(w, s.n_warps);
+  while (true) {
+    bar_sync(1, threads);
+    if (ij->kind == kJobGaInit) {
+      ga_init_part(ij->v, ij->rng, ij->combo0, ij->n, 32 * w + lane, threads, gen);
+      __threadfence();
+      bar_sync(2, threads);
+      continue;
+    }
+    const int kind = s0.job[0], mask = s0.job[1];
+    if (kind == kJobExit) return;
+    {  // the lead's current plan view
+      const int32_t* hs = reinterpret_cast<const int32_t*>(&s0.h);
+      int32_t* hd = reinterpret_cast<int32_t*>(&s.h);
+      for (int i = lane; i < static_cast<int>(sizeof(RecHeader) / 4); i += 32) hd[i] = hs[i];
+      const int32_t* os = reinterpret_cast<const int32_t*>(&s0.o);
+      int32_t* od = reinterpret_cast<int32_t*>(&s.o);
+      for (int i = lane; i < static_cast<int>(sizeof(RecOffsets) / 4); i += 32) od[i] = os[i];
+      if (lane == 0) {
+        s.memo_tp_ok = s0.memo_tp_ok;
+        s.memo_pp_ok = s0.memo_pp_ok;
+        s.memo_cm_ok = s0.memo_cm_ok;
+      }
+      __syncwarp();
+    }
+    team_share(P, cfg, s, kind, mask, w);
+    bar_sync(2, threads);
+  }
+}
+
 // kTeam = 1: one-warp workers (busy rounds); kTeam = 2: each worker has a
 // helper warp for the per-task parts of an evaluation (eval_kernel's teams),
 // for rounds with few live runs where an evaluation's latency is the chain;
@@ -1301,9 +1383,12 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
           int64_t gscratch_doubles) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ Ws team[kTeam];
+  __shared__ GaInitJob ijob[1];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   GaSm sm;
+  sm.ijob = ijob;
+  sm.n_warps = kTeam;
   if (warp == 0) {
     // GA scratch after the evaluation carve (launch_ga_offspring sizes it)
     uint8_t* p = smem + carve2_bytes(cv);
@@ -1358,14 +1443,15 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
       p = carve_team_scratch(team[w], p, cv);
     }
     if (blockIdx.x == 0) atomicCAS(&c_ga.ctl[kGaCtlT0], 0ull, ga_timer());
+    ijob[0].kind = 0;
   }
   __syncthreads();
   Ws& s = team[0];
   // persistent workers: the link-class matrix is staged once
   if (warp == 0 && cv.cls_smem) stage_link_classes(P, s);
   __syncthreads();
-  if (warp > 0) {  // helper: per-task jobs of warp 0's evaluations
-    team_helper(P, cfg, team, warp);
+  if (warp > 0) {  // helper: init chunks and per-task jobs of warp 0's evaluations
+    ga_team_helper(P, cfg, team, warp, ijob);
     return;
   }
   while (true) {
@@ -1465,6 +1551,8 @@ cudaError_t ga_launch_team(const DevProblem& P, const DevCostConfig& cfg, Carve 
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   grid = n_sm * per_sm;
+  // helper warps' generation scratch follows the grid's slots (16 per SM)
+  if (kTeam > 1 && grid * kTeam > 16 * n_sm) grid = 16 * n_sm / kTeam;
   static bool mod_tables = false;
   if (!mod_tables) {
     static uint64_t mm[dev::kGaModMax + 1];

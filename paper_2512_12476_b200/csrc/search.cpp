@@ -879,8 +879,9 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
     auto ja = jump_at.find(g.gen_draws);
     if (ja == jump_at.end()) {
       ja = jump_at.emplace(g.gen_draws, static_cast<int32_t>(jumps.size())).first;
-      const std::vector<Poly256>& tb = jump_table(static_cast<uint64_t>(g.gen_draws), 31);
-      jumps.insert(jumps.end(), tb.begin(), tb.begin() + 31);
+      // x^(L*D) for L = 1..127: lane offsets and strides of a team of four
+      const std::vector<Poly256>& tb = jump_table(static_cast<uint64_t>(g.gen_draws), kGaJumps);
+      jumps.insert(jumps.end(), tb.begin(), tb.begin() + kGaJumps);
     }
     g.jump_off = ja->second;
     const int64_t it = std::max<int64_t>(
