@@ -1040,20 +1040,27 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   cuda_check(cudaMemcpyAsync(H + h_ctl, D + o_ctl, 8 * kGaCtlWords, cudaMemcpyDeviceToHost, st), "D2H ga ctl");
   cuda_check(cudaMemcpy2DAsync(H + h_best, 2 * stride, D + o_pool, run_bytes, 2 * stride, n,
                                cudaMemcpyDeviceToHost, st), "D2H ga best plans");
+  // improvements: a bounded prefix rides in the same batch (a round usually
+  // records a few per run); only a longer list costs a second round trip
+  const int64_t impr_pre = std::min<int64_t>(impr_cap, 8 * static_cast<int64_t>(n) + 64);
+  cuda_check(cudaMemcpyAsync(H + h_imp, D + o_impr, sizeof(GaImpr) * impr_pre,
+                             cudaMemcpyDeviceToHost, st), "D2H ga improvements");
   cuda_check(cudaStreamSynchronize(st), "ga_kernel");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx.ev0, ctx.ev1);
   ctx.eval_ms += ms;
   const int64_t n_impr = static_cast<int64_t>(hctl[kGaCtlImpr]);
   if (n_impr > impr_cap) throw InternalError("device GA improvement list overflow");
-  if (n_impr > 0)
-    cuda_check(cudaMemcpy(H + h_imp, D + o_impr, sizeof(GaImpr) * n_impr, cudaMemcpyDeviceToHost),
+  if (n_impr > impr_pre)
+    cuda_check(cudaMemcpy(H + h_imp + sizeof(GaImpr) * impr_pre, D + o_impr + sizeof(GaImpr) * impr_pre,
+                          sizeof(GaImpr) * (n_impr - impr_pre), cudaMemcpyDeviceToHost),
                "D2H ga improvements");
   ctx.plans_evaluated += static_cast<int64_t>(hctl[kGaCtlEvals]);
   ctx.canonical_bytes += static_cast<int64_t>(hctl[kGaCtlBytes]);
   ctx.h2d_bytes += h2d;
   ctx.d2h_bytes += static_cast<int64_t>(sizeof(GaRun)) * n + 8 * kGaCtlWords +
-                   2 * static_cast<int64_t>(stride) * n + static_cast<int64_t>(sizeof(GaImpr)) * n_impr;
+                   2 * static_cast<int64_t>(stride) * n +
+                   static_cast<int64_t>(sizeof(GaImpr)) * std::max(n_impr, impr_pre);
   const unsigned long long t0_dev = hctl[kGaCtlT0];
   auto cand_at = [&](const uint8_t* rec, int ng) {
     Cand c;
