@@ -64,29 +64,69 @@ inline const Poly256& charpoly() {
 }
 
 // a * b mod p
+// x^(256 + 8k) * v mod p for byte position k of the high half and byte
+// value v: the reduction becomes 32 table lookups (256 KB, built once)
+inline const std::vector<Poly256>& reduce_table() {
+  static const std::vector<Poly256> t = [] {
+    const Poly256& p = charpoly();
+    // x^(256 + j) mod p for j = 0..255, by repeated multiplication by x
+    std::vector<Poly256> xj(256);
+    Poly256 cur = p;  // x^256 = p (mod p) with the x^256 term dropped
+    for (int j = 0; j < 256; ++j) {
+      xj[j] = cur;
+      const uint64_t top = cur[3] >> 63;
+      for (int k = 3; k > 0; --k) cur[k] = (cur[k] << 1) | (cur[k - 1] >> 63);
+      cur[0] <<= 1;
+      if (top)
+        for (int k = 0; k < 4; ++k) cur[k] ^= p[k];
+    }
+    std::vector<Poly256> out(32 * 256, Poly256{0, 0, 0, 0});
+    for (int k = 0; k < 32; ++k)
+      for (int v = 1; v < 256; ++v) {
+        const Poly256& lo = out[k * 256 + (v & (v - 1))];
+        const Poly256& x = xj[8 * k + __builtin_ctz(static_cast<unsigned>(v))];
+        for (int w = 0; w < 4; ++w) out[k * 256 + v][w] = lo[w] ^ x[w];
+      }
+    return out;
+  }();
+  return t;
+}
+
+// a * b mod p over GF(2): 4-bit windowed carry-less product, then the high
+// 256 bits folded back through reduce_table()
 inline Poly256 mulmod(const Poly256& a, const Poly256& b) {
-  uint64_t prod[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = 0; i < 256; ++i) {
-    if (!bit(a.data(), i)) continue;
-    // prod ^= b << i
-    const int w = i >> 6, s = i & 63;
-    for (int k = 0; k < 4; ++k) {
-      prod[k + w] ^= b[k] << s;
-      if (s) prod[k + w + 1] ^= b[k] >> (64 - s);
+  uint64_t win[16][5];
+  for (int w = 0; w < 5; ++w) win[0][w] = 0;
+  for (int v = 1; v < 16; ++v) {
+    // win[v] = b * v: b shifted by each set bit of v
+    const int bitpos = 31 - __builtin_clz(static_cast<unsigned>(v));
+    const int rest = v ^ (1 << bitpos);
+    for (int w = 0; w < 5; ++w) {
+      const uint64_t bw = w < 4 ? b[w] : 0;
+      const uint64_t bl = w > 0 ? b[w - 1] : 0;
+      const uint64_t sh = bitpos ? (bw << bitpos) | (bl >> (64 - bitpos)) : bw;
+      win[v][w] = win[rest][w] ^ sh;
     }
   }
-  const Poly256& p = charpoly();
-  for (int i = 511; i >= 256; --i) {
-    if (!bit(prod, i)) continue;
-    // x^i = x^(i-256) * (p - x^256): clear bit i, xor p << (i - 256)
-    prod[i >> 6] &= ~(1ull << (i & 63));
-    const int sh = i - 256, w = sh >> 6, s = sh & 63;
-    for (int k = 0; k < 4; ++k) {
-      prod[k + w] ^= p[k] << s;
-      if (s) prod[k + w + 1] ^= p[k] >> (64 - s);
+  uint64_t prod[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < 64; ++i) {
+    const unsigned nib = static_cast<unsigned>(a[i >> 4] >> (4 * (i & 15))) & 15u;
+    if (!nib) continue;
+    const int w0 = (4 * i) >> 6, s = (4 * i) & 63;
+    for (int w = 0; w < 5; ++w) {
+      prod[w0 + w] ^= win[nib][w] << s;
+      if (s) prod[w0 + w + 1] ^= win[nib][w] >> (64 - s);
     }
   }
-  return Poly256{prod[0], prod[1], prod[2], prod[3]};
+  const std::vector<Poly256>& t = reduce_table();
+  Poly256 r{prod[0], prod[1], prod[2], prod[3]};
+  for (int k = 0; k < 32; ++k) {
+    const unsigned v = static_cast<unsigned>(prod[4 + (k >> 3)] >> (8 * (k & 7))) & 255u;
+    if (!v) continue;
+    const Poly256& x = t[k * 256 + v];
+    for (int w = 0; w < 4; ++w) r[w] ^= x[w];
+  }
+  return r;
 }
 
 }  // namespace jump_detail
