@@ -163,15 +163,21 @@ HPG_HD void rng_apply_jump(Rng& r, const uint64_t* q) {
 // x^(L*D) mod p for L = 1..n (cached per D, process-wide)
 inline const std::vector<Poly256>& jump_table(uint64_t D, int n) {
   static std::mutex m;
-  static std::map<uint64_t, std::vector<Poly256>> cache;
-  std::lock_guard<std::mutex> lk(m);
-  std::vector<Poly256>& v = cache[D];
-  if (static_cast<int>(v.size()) < n) {
-    const Poly256 q = jump_poly(D);
-    if (v.empty()) v.push_back(q);
-    while (static_cast<int>(v.size()) < n) v.push_back(jump_detail::mulmod(v.back(), q));
+  static std::map<uint64_t, std::vector<Poly256>> cache;  // nodes never move
+  {
+    std::lock_guard<std::mutex> lk(m);
+    auto it = cache.find(D);
+    if (it != cache.end() && static_cast<int>(it->second.size()) >= n) return it->second;
   }
-  return v;
+  // built outside the lock so callers can fill several tables in parallel
+  std::vector<Poly256> v;
+  const Poly256 q = jump_poly(D);
+  v.push_back(q);
+  while (static_cast<int>(v.size()) < n) v.push_back(jump_detail::mulmod(v.back(), q));
+  std::lock_guard<std::mutex> lk(m);
+  std::vector<Poly256>& slot = cache[D];
+  if (slot.size() < v.size()) slot = std::move(v);
+  return slot;
 }
 
 }  // namespace hpg

@@ -832,6 +832,20 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   std::vector<Poly256> jumps;
   std::map<int32_t, int32_t> jump_at;  // gen_draws -> first polynomial
   std::vector<GaRun> gr(n);
+  {
+    // jump tables for every draw count of this round, built in parallel
+    std::vector<int64_t> ds;
+    for (int i = 0; i < n; ++i)
+      ds.push_back(gen_draws_per_candidate(P.N, nodes_per_region.data(),
+                                           static_cast<int>(nodes_per_region.size()),
+                                           gen_item_of(*runs[i]->env)));
+    std::sort(ds.begin(), ds.end());
+    ds.erase(std::unique(ds.begin(), ds.end()), ds.end());
+    const int nd = static_cast<int>(ds.size());
+    host_parallel_for(nd, nd >= 2, [&](int i) {
+      jump_table(static_cast<uint64_t>(ds[i]), kGaJumps);
+    });
+  }
   for (int i = 0; i < n; ++i) {
     const ArmRun& r = *runs[i];
     const ArmEnv& e = *r.env;
