@@ -295,6 +295,17 @@ typedef struct {
 int hpg_sweep_resident(hpg_ctx* ctx, uint64_t seed, uint64_t k0, uint64_t count,
                        hpg_sweep_stats* stats, char* err, size_t errlen);
 
+/* Sharded config-5 sweep: plans [0, total) split into one
+ * contiguous plan-index range per rank; each rank sweeps its range resident in
+ * HBM, then one NCCL all-gather of the 32-byte (cost, k, feasible count,
+ * checksum) partials gives every rank the global argmin by (cost, lowest k).
+ * Uses the context's communicator (created on first use from nccl_id, as in
+ * hpg_search_dist). stats: best_cost/best_k/n_feasible/xor_bits are global;
+ * canonical_bytes and the times are this rank's. world == 1 needs no nccl_id. */
+int hpg_sweep_dist(hpg_ctx* ctx, uint64_t seed, uint64_t total, int rank, int world,
+                   const uint8_t nccl_id[128], hpg_sweep_stats* stats, char* err,
+                   size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1392,6 +1392,69 @@ int cmd_time_sweep(const std::string& wfp, const std::string& tpp, std::uint64_t
   return 0;
 }
 
+// Stratified config-5 sample (SURVEY.md §8 D1 CPU baseline + parity set):
+// `blocks` contiguous runs of `block_len` plans, block b starting at
+// k = b * (total / blocks), so the sample spans the whole [0, total) range.
+// All `threads` host threads share the blocks (static interleave). Prints a
+// timing line; with `out`, writes per-plan records in sample order:
+// k (u64), e2e bits (u64), memory_feasible (u64).
+int cmd_sample_sweep(const std::string& wfp, const std::string& tpp, std::uint64_t seed,
+                     std::uint64_t total, std::uint64_t blocks, std::uint64_t block_len,
+                     int threads, const std::string& out) {
+  const WorkflowGraph wf = parse_workflow_json(read_file(wfp));
+  const DeviceTopology topo = parse_topology_json(read_file(tpp));
+  const auto tgs = enumerate_task_groupings(wf);
+  const std::uint64_t stride = total / blocks;
+  std::vector<SweepStats> st(blocks);
+  std::vector<std::vector<double>> costs(blocks);
+  std::vector<std::vector<int>> feas(blocks);
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      for (std::uint64_t b = t; b < blocks; b += threads) {
+        const std::uint64_t a = b * stride;
+        sweep_range(wf, topo, tgs, seed, a, a + block_len, st[b], &costs[b], &feas[b]);
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  const double wall =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  SweepStats all;
+  for (const auto& s : st) {
+    all.feasible += s.feasible;
+    all.xor_bits ^= s.xor_bits;
+    if (s.best < all.best || (s.best == all.best && s.best_k < all.best_k)) {
+      all.best = s.best;
+      all.best_k = s.best_k;
+    }
+  }
+  if (!out.empty()) {
+    std::FILE* f = std::fopen(out.c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write " + out);
+    for (std::uint64_t b = 0; b < blocks; ++b) {
+      for (std::uint64_t i = 0; i < block_len; ++i) {
+        std::uint64_t rec[3];
+        rec[0] = b * stride + i;
+        std::memcpy(&rec[1], &costs[b][i], 8);
+        rec[2] = static_cast<std::uint64_t>(feas[b][i]);
+        std::fwrite(rec, sizeof(rec), 1, f);
+      }
+    }
+    std::fclose(f);
+  }
+  const std::uint64_t count = blocks * block_len;
+  std::printf(
+      "{\"count\": %" PRIu64 ", \"blocks\": %" PRIu64 ", \"block_len\": %" PRIu64
+      ", \"stride\": %" PRIu64 ", \"threads\": %d, \"wall_s\": %.6f, \"plans_per_s\": %.3f, "
+      "\"n_feasible\": %" PRIu64 ", \"best\": \"%s\", \"best_dec\": %.17g, \"best_k\": %" PRIu64
+      ", \"xor_bits\": \"%016" PRIx64 "\"}\n",
+      count, blocks, block_len, stride, threads, wall, count / wall, all.feasible,
+      hx(all.best).c_str(), all.best, all.best_k, all.xor_bits);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -1437,6 +1500,10 @@ int main(int argc, char** argv) {
     if (cmd == "time_search")
       return cmd_time_search(arg(2), arg(3), std::stoll(arg(4)), std::stoull(arg(5)),
                              argc > 6 ? argv[6] : "");
+    if (cmd == "sample_sweep")
+      return cmd_sample_sweep(arg(2), arg(3), std::stoull(arg(4)), std::stoull(arg(5)),
+                              std::stoull(arg(6)), std::stoull(arg(7)), std::stoi(arg(8)),
+                              argc > 9 ? argv[9] : "");
     if (cmd == "time_sweep")
       return cmd_time_sweep(arg(2), arg(3), std::stoull(arg(4)), std::stoull(arg(5)),
                             std::stoull(arg(6)), std::stoi(arg(7)));

@@ -94,7 +94,10 @@ int hpg_create(const hpg_problem* problem, int cuda_device, hpg_ctx** out, char*
 
 void hpg_destroy(hpg_ctx* ctx) {
   if (!ctx) return;
-  delete ctx->impl;
+  if (ctx->impl) {
+    const DeviceScope on_device(ctx->impl->device);
+    delete ctx->impl;
+  }
   delete ctx;
 }
 
@@ -106,6 +109,7 @@ int hpg_restage(hpg_ctx* ctx, const hpg_problem* problem, char* err, size_t errl
   return guarded(err, errlen, [&] {
     check_ctx(ctx);
     if (!problem) throw UsageError("hpg_restage: null problem");
+    const DeviceScope on_device(ctx->impl->device);
     restage(*ctx->impl, *problem);
   });
 }
@@ -126,6 +130,7 @@ int hpg_eval(hpg_ctx* ctx, const hpg_plan_table* plans, const hpg_cost_config* c
     check_ctx(ctx);
     if (!plans || !out) throw UsageError("hpg_eval: null argument");
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     const hpg_cost_config c = cfg ? *cfg : default_cost_config();
     std::vector<TablePlan> tps = unpack_table(C.prob, *plans);
     Batch b;
@@ -152,6 +157,7 @@ int hpg_check_memory(hpg_ctx* ctx, const hpg_plan_table* plans, const hpg_cost_c
     check_ctx(ctx);
     if (!plans) throw UsageError("hpg_check_memory: null argument");
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     const hpg_cost_config c = cfg ? *cfg : default_cost_config();
     std::vector<TablePlan> tps = unpack_table(C.prob, *plans);
     Batch b;
@@ -176,6 +182,7 @@ int hpg_balance(hpg_ctx* ctx, const hpg_plan_table* plans, const hpg_cost_config
     if (!plans) throw UsageError("hpg_balance: null argument");
     if (which < 1 || which > 3) throw UsageError("hpg_balance: which must be 1, 2 or 3");
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     const hpg_cost_config c = cfg ? *cfg : default_cost_config();
     std::vector<TablePlan> tps = unpack_table(C.prob, *plans);
     Batch b;

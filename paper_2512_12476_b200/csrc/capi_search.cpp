@@ -257,6 +257,7 @@ int hpg_search(hpg_ctx* ctx, const hpg_knobs* knobs, hpg_search_result** out, ch
     if (!ctx || !ctx->impl || !knobs || !out) throw UsageError("hpg_search: null argument");
     *out = nullptr;
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     const Knobs K = knobs_from_c(C.prob, *knobs);
     if (K.budget < 1) throw UsageError("search budget must be >= 1");
     *out = wrap(nested_sha_search(C, K, nullptr), C.prob);
@@ -274,6 +275,7 @@ int hpg_search_dist(hpg_ctx* ctx, const hpg_knobs* knobs, int rank, int world,
     if (!ctx || !ctx->impl || !knobs || !out) throw UsageError("hpg_search_dist: null argument");
     *out = nullptr;
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     const Knobs K = knobs_from_c(C.prob, *knobs);
     if (K.budget < 1) throw UsageError("search budget must be >= 1");
     if (world <= 1) {
@@ -298,6 +300,7 @@ int hpg_ga_search(hpg_ctx* ctx, const int32_t* task_group, int32_t n_groups,
       throw UsageError("hpg_ga_search: null argument");
     *out = nullptr;
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     const Knobs K = knobs_from_c(C.prob, *knobs);
     Grouping tg(n_groups);
     for (int s = 0; s < C.prob.T; ++s) {
@@ -316,6 +319,7 @@ int hpg_exhaustive(hpg_ctx* ctx, const hpg_knobs* knobs, hpg_search_result** out
     if (!ctx || !ctx->impl || !knobs || !out) throw UsageError("hpg_exhaustive: null argument");
     *out = nullptr;
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     *out = wrap(exhaustive_search(C, knobs_from_c(C.prob, *knobs)), C.prob);
   });
 }
@@ -326,6 +330,7 @@ int hpg_exhaustive_estimate(hpg_ctx* ctx, const hpg_knobs* knobs, double* estima
     if (!ctx || !ctx->impl || !knobs || !estimate)
       throw UsageError("hpg_exhaustive_estimate: null argument");
     Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
     *estimate = exhaustive_space_estimate(C.prob, knobs_from_c(C.prob, *knobs));
   });
 }
@@ -461,6 +466,7 @@ int hpg_sweep(hpg_ctx* ctx, uint64_t seed, uint64_t k0, uint64_t count, double* 
   return guarded(err, errlen, [&] {
     if (!ctx || !ctx->impl) throw UsageError("hpg_sweep: null context");
     SweepAcc acc;
+    const DeviceScope on_device(ctx->impl->device);
     run_sweep(*ctx->impl, seed, k0, count, costs, feasible, acc);
     if (best_cost) *best_cost = acc.best;
     if (best_k) *best_k = acc.best_k;
@@ -473,11 +479,64 @@ int hpg_sweep_resident(hpg_ctx* ctx, uint64_t seed, uint64_t k0, uint64_t count,
   return guarded(err, errlen, [&] {
     if (!ctx || !ctx->impl || !stats) throw UsageError("hpg_sweep_resident: null argument");
     SweepAcc acc;
+    const DeviceScope on_device(ctx->impl->device);
     run_sweep(*ctx->impl, seed, k0, count, nullptr, nullptr, acc);
     stats->best_cost = acc.best;
     stats->best_k = acc.best_k;
     stats->n_feasible = acc.nf;
     stats->xor_bits = acc.x;
+    stats->canonical_bytes = acc.bytes;
+    stats->total_ms = acc.total_ms;
+    stats->eval_ms = acc.eval_ms;
+    stats->gen_ms = acc.gen_ms;
+    stats->launches = acc.launches;
+  });
+}
+
+int hpg_sweep_dist(hpg_ctx* ctx, uint64_t seed, uint64_t total, int rank, int world,
+                   const uint8_t nccl_id[128], hpg_sweep_stats* stats, char* err,
+                   size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!ctx || !ctx->impl || !stats) throw UsageError("hpg_sweep_dist: null argument");
+    if (world < 1 || rank < 0 || rank >= world) throw UsageError("hpg_sweep_dist: bad rank/world");
+    Ctx& C = *ctx->impl;
+    const DeviceScope on_device(C.device);
+    // contiguous plan-index shard of this rank
+    const uint64_t k0 = static_cast<uint64_t>((static_cast<unsigned __int128>(total) * rank) / world);
+    const uint64_t k1 =
+        static_cast<uint64_t>((static_cast<unsigned __int128>(total) * (rank + 1)) / world);
+    SweepAcc acc;
+    run_sweep(C, seed, k0, k1 - k0, nullptr, nullptr, acc);
+    SweepPartial mine{acc.best, acc.best_k, acc.nf, acc.x};
+    if (world > 1) {
+      if (!C.dist.comm || C.dist.rank != rank || C.dist.world != world) {
+        if (C.dist.comm) dist_destroy(C.dist);
+        dist_init(C.dist, rank, world, nccl_id, C.device);
+      }
+      // one all-gather of the 32-byte (cost, k, feasible count, checksum) partials
+      std::vector<SweepPartial> all(static_cast<size_t>(world));
+      C.d_xch_send.reserve(sizeof(SweepPartial));
+      C.d_xch_recv.reserve(sizeof(SweepPartial) * world);
+      cuda_check(cudaMemcpyAsync(C.d_xch_send.p, &mine, sizeof(mine), cudaMemcpyHostToDevice,
+                                 C.stream), "H2D sweep partial");
+      dist_allgather(C.dist, C.d_xch_send.p, C.d_xch_recv.p, sizeof(SweepPartial), C.stream);
+      cuda_check(cudaMemcpyAsync(all.data(), C.d_xch_recv.p, sizeof(SweepPartial) * world,
+                                 cudaMemcpyDeviceToHost, C.stream), "D2H sweep partials");
+      cuda_check(cudaStreamSynchronize(C.stream), "sweep all-gather");
+      mine = SweepPartial{kInf, ~0ull, 0, 0};
+      for (const SweepPartial& p : all) {
+        mine.n_feasible += p.n_feasible;
+        mine.xor_bits ^= p.xor_bits;
+        if (p.best < mine.best || (p.best == mine.best && p.best_k < mine.best_k)) {
+          mine.best = p.best;
+          mine.best_k = p.best_k;
+        }
+      }
+    }
+    stats->best_cost = mine.best;
+    stats->best_k = mine.best_k;
+    stats->n_feasible = mine.n_feasible;
+    stats->xor_bits = mine.xor_bits;
     stats->canonical_bytes = acc.bytes;
     stats->total_ms = acc.total_ms;
     stats->eval_ms = acc.eval_ms;

@@ -173,6 +173,22 @@ struct BatchOut {
   std::vector<double> required;          // if requested
 };
 
+// Makes a context's GPU current for the duration of one C-ABI call and
+// restores the caller's device afterwards (every entry point taking a context).
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != device) cudaSetDevice(device);
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
 struct Ctx {
   Problem prob;
   int device = 0;

@@ -18,6 +18,8 @@
 // exact enumeration runs 32 trials per step instead of one.
 #include <cuda_runtime.h>
 
+#include "devstate.hpp"
+
 #include <cstdio>
 
 #include "eval_device.cuh"
@@ -862,31 +864,12 @@ template <int kTeam>
 cudaError_t grid_for(Carve cv, int n, int n_sm, int& grid) {
   auto kern = dev::eval_kernel<kTeam>;
   // opt in to the dynamic size (static + dynamic may not exceed 48 KB without
-  // it, and the kernel's own static shared memory counts)
-  static int configured_bytes = 0;
-  if (cv.bytes > configured_bytes) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
-    if (e != cudaSuccess) return e;
-    configured_bytes = cv.bytes;
-  }
-  // occupancy per dynamic-smem size (a few distinct sizes per problem)
-  static int cached_key[8] = {-1, -1, -1, -1, -1, -1, -1, -1}, cached_per_sm[8];
-  static int next_slot = 0;
-  const int key = cv.bytes * 8 + cv.n_warps;
-  int per_sm = 0, hit = -1;
-  for (int i = 0; i < 8; ++i)
-    if (cached_key[i] == key) hit = i;
-  if (hit >= 0) {
-    per_sm = cached_per_sm[hit];
-  } else {
-    cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * cv.n_warps, cv.bytes);
-    if (e != cudaSuccess) return e;
-    cached_key[next_slot] = key;
-    cached_per_sm[next_slot] = per_sm;
-    next_slot = (next_slot + 1) & 7;
-  }
+  // it, and the kernel's own static shared memory counts); per device
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), cv.bytes);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = occupancy_per_sm(reinterpret_cast<const void*>(kern), 32 * cv.n_warps, cv.bytes, &per_sm);
+  if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   grid = n < n_sm * per_sm ? n : n_sm * per_sm;
   return cudaSuccess;

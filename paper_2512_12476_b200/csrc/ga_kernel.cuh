@@ -20,14 +20,18 @@
 #include "ga_dev.hpp"
 #include "gen_ga.hpp"
 #include "rng_jump.hpp"
+#include "devstate.hpp"
 
 #define GA_BOUNDED(r, n) ga_bounded(r, n)
 
 namespace hpg {
 namespace dev {
 
-// the launch's parameters (constant bank: read by every GA function)
-__constant__ GaParams c_ga;
+// the launch's parameters: passed by value to every launch (a __grid_constant__
+// kernel argument) and copied once into this per-CTA shared copy, which every
+// GA function reads. A launch carries its own parameters, so contexts on the
+// same device (and threads driving them) never share mutable device state.
+__shared__ GaParams c_ga;
 
 __device__ __forceinline__ unsigned long long ga_timer() {
   unsigned long long t;
@@ -41,8 +45,20 @@ __device__ __forceinline__ unsigned long long ga_timer() {
 // exact for every 32-bit x) from a constant-bank table: no divide, no L2
 // round trip (the workers' L1 is mostly shared memory)
 constexpr int kGaModMax = 1024;
-__constant__ uint64_t c_mod_m[kGaModMax + 1];   // M per divisor
-__constant__ uint32_t c_mod_p32[kGaModMax + 1];  // 2^32 mod n
+struct GaModTables {
+  uint64_t m[kGaModMax + 1];    // M per divisor
+  uint32_t p32[kGaModMax + 1];  // 2^32 mod n
+};
+constexpr GaModTables ga_mod_tables() {
+  GaModTables t{};
+  for (int d = 1; d <= kGaModMax; ++d) {
+    t.m[d] = ~uint64_t(0) / static_cast<uint64_t>(d) + 1;
+    t.p32[d] = static_cast<uint32_t>((uint64_t(1) << 32) % static_cast<uint64_t>(d));
+  }
+  return t;
+}
+// initialised at compile time: part of the module image on every device
+__constant__ GaModTables c_mod = ga_mod_tables();
 
 __device__ __forceinline__ uint32_t ga_mod32(uint32_t x, uint32_t n, uint64_t m) {
   return static_cast<uint32_t>(__umul64hi(m * x, n));
@@ -52,9 +68,9 @@ __device__ __forceinline__ uint64_t ga_bounded(Rng& rng, uint64_t n) {
   const uint64_t a = rng.next();
   if (n > static_cast<uint64_t>(kGaModMax)) return a % n;
   const uint32_t d = static_cast<uint32_t>(n);
-  const uint64_t m = c_mod_m[d];
+  const uint64_t m = c_mod.m[d];
   const uint32_t hi = static_cast<uint32_t>(a >> 32), lo = static_cast<uint32_t>(a);
-  return ga_mod32(ga_mod32(hi, d, m) * c_mod_p32[d] + ga_mod32(lo, d, m), d, m);
+  return ga_mod32(ga_mod32(hi, d, m) * c_mod.p32[d] + ga_mod32(lo, d, m), d, m);
 }
 
 __device__ __forceinline__ Rng ga_ld_rng(const Rng* p) {
@@ -1380,8 +1396,16 @@ __device__ __noinline__ void ga_team_helper(const DevProblem& P, const DevCostCo
 template <int kTeam>
 __global__ void __launch_bounds__(32 * kTeam, kTeam == 4 ? 2 : 16 / kTeam)
 ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscratch,
-          int64_t gscratch_doubles) {
+          int64_t gscratch_doubles, const __grid_constant__ GaParams ga_in) {
   extern __shared__ __align__(16) uint8_t smem[];
+  {
+    static_assert(sizeof(GaParams) % 8 == 0, "GaParams copy granule");
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(&ga_in);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(&c_ga);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(GaParams) / 8); i += blockDim.x)
+      dst[i] = src[i];
+    __syncthreads();
+  }
   __shared__ Ws team[kTeam];
   __shared__ GaInitJob ijob[1];
   const int lane = threadIdx.x & 31;
@@ -1539,41 +1563,19 @@ cudaError_t ga_launch_team(const DevProblem& P, const DevCostConfig& cfg, Carve 
   cv.n_warps = kTeam;
   cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave, G.n_dev, G.n_regions,
                                                     G.n_nodes);
-  static int configured = 0;
-  cudaError_t e;
-  if (cv.bytes > configured) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cv.bytes);
-    if (e != cudaSuccess) return e;
-    configured = cv.bytes;
-  }
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), cv.bytes);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kTeam, cv.bytes);
+  e = occupancy_per_sm(reinterpret_cast<const void*>(kern), 32 * kTeam, cv.bytes, &per_sm);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   grid = n_sm * per_sm;
-  // helper warps' generation scratch follows the grid's slots (16 per SM)
-  if (kTeam > 1 && grid * kTeam > 16 * n_sm) grid = 16 * n_sm / kTeam;
-  static bool mod_tables = false;
-  if (!mod_tables) {
-    static uint64_t mm[dev::kGaModMax + 1];
-    static uint32_t p32[dev::kGaModMax + 1];
-    mm[0] = 0;
-    p32[0] = 0;
-    for (int d = 1; d <= dev::kGaModMax; ++d) {
-      mm[d] = ~uint64_t(0) / static_cast<uint64_t>(d) + 1;
-      p32[d] = static_cast<uint32_t>((uint64_t(1) << 32) % static_cast<uint64_t>(d));
-    }
-    e = cudaMemcpyToSymbol(dev::c_mod_m, mm, sizeof(mm));
-    if (e != cudaSuccess) return e;
-    e = cudaMemcpyToSymbol(dev::c_mod_p32, p32, sizeof(p32));
-    if (e != cudaSuccess) return e;
-    mod_tables = true;
-  }
+  // the workers' generation scratch (gen_scratch) has 16 warp slots per SM:
+  // clamp every team size before the launch
+  if (grid * kTeam > 16 * n_sm) grid = 16 * n_sm / kTeam;
   GaParams g2 = G;
   if (g2.split_runs < 0) g2.split_runs = grid / 16;  // ~one swap wave per run fills the workers
-  e = cudaMemcpyToSymbolAsync(dev::c_ga, &g2, sizeof(GaParams), 0, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, 32 * kTeam, cv.bytes, st>>>(P, cfg, cv, gscratch, gscratch_doubles);
+  kern<<<grid, 32 * kTeam, cv.bytes, st>>>(P, cfg, cv, gscratch, gscratch_doubles, g2);
   return cudaGetLastError();
 }
 }  // namespace

@@ -11,6 +11,8 @@
 // writes the device slots into the packed record and a compact copy.
 #include <cuda_runtime.h>
 
+#include "devstate.hpp"
+
 #include "gen_ga.hpp"
 #include "rng.hpp"
 
@@ -141,13 +143,9 @@ cudaError_t launch_gen_ga(const GenTablesDev& tb, const GenItem* d_items,
   const int threads = 64;
   const size_t smem = static_cast<size_t>(threads) * tb.smem_per_thread;
   if (smem > 48 * 1024) {
-    static size_t configured = 0;
-    if (smem > configured) {
-      const cudaError_t e = cudaFuncSetAttribute(
-          dev::gen_ga_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      configured = smem;
-    }
+    const cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(dev::gen_ga_kernel),
+                                          static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
   }
   dev::gen_ga_kernel<<<(n_cands + threads - 1) / threads, threads, smem, st>>>(
       tb, d_items, d_cand_item, d_starts, n_cands, d_recs, d_off, d_dev_out_off, d_dev_out);

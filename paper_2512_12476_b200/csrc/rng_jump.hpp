@@ -9,6 +9,7 @@
 #include <array>
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -160,23 +161,26 @@ HPG_HD void rng_apply_jump(Rng& r, const uint64_t* q) {
   r.s[3] = a3;
 }
 
-// x^(L*D) mod p for L = 1..n (cached per D, process-wide)
-inline const std::vector<Poly256>& jump_table(uint64_t D, int n) {
+// x^(L*D) mod p for L = 1..n (cached per D, process-wide). Entries are
+// immutable once published: a caller keeps its table alive through the
+// shared_ptr even if a later call for the same D publishes a longer one.
+using JumpTable = std::shared_ptr<const std::vector<Poly256>>;
+inline JumpTable jump_table(uint64_t D, int n) {
   static std::mutex m;
-  static std::map<uint64_t, std::vector<Poly256>> cache;  // nodes never move
+  static std::map<uint64_t, JumpTable> cache;
   {
     std::lock_guard<std::mutex> lk(m);
     auto it = cache.find(D);
-    if (it != cache.end() && static_cast<int>(it->second.size()) >= n) return it->second;
+    if (it != cache.end() && static_cast<int>(it->second->size()) >= n) return it->second;
   }
   // built outside the lock so callers can fill several tables in parallel
-  std::vector<Poly256> v;
+  auto v = std::make_shared<std::vector<Poly256>>();
   const Poly256 q = jump_poly(D);
-  v.push_back(q);
-  while (static_cast<int>(v.size()) < n) v.push_back(jump_detail::mulmod(v.back(), q));
+  v->push_back(q);
+  while (static_cast<int>(v->size()) < n) v->push_back(jump_detail::mulmod(v->back(), q));
   std::lock_guard<std::mutex> lk(m);
-  std::vector<Poly256>& slot = cache[D];
-  if (slot.size() < v.size()) slot = std::move(v);
+  JumpTable& slot = cache[D];
+  if (!slot || slot->size() < v->size()) slot = std::move(v);
   return slot;
 }
 

@@ -894,8 +894,8 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
     if (ja == jump_at.end()) {
       ja = jump_at.emplace(g.gen_draws, static_cast<int32_t>(jumps.size())).first;
       // x^(L*D) for L = 1..127: lane offsets and strides of a team of four
-      const std::vector<Poly256>& tb = jump_table(static_cast<uint64_t>(g.gen_draws), kGaJumps);
-      jumps.insert(jumps.end(), tb.begin(), tb.begin() + kGaJumps);
+      const JumpTable tb = jump_table(static_cast<uint64_t>(g.gen_draws), kGaJumps);
+      jumps.insert(jumps.end(), tb->begin(), tb->begin() + kGaJumps);
     }
     g.jump_off = ja->second;
     const int64_t it = std::max<int64_t>(
@@ -924,7 +924,12 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   const int64_t want_q = 2 * (static_cast<int64_t>(n) * (res_per_run + 1) + 4 * max_workers);
   uint64_t q_cap = 1024;
   while (static_cast<int64_t>(q_cap) < want_q) q_cap <<= 1;
+  // improvements: every evaluation can improve its run's best, so the device
+  // list is sized by the round's budget (32 B per unit in HBM); the pinned
+  // host staging holds only a bounded prefix (a round usually records a few
+  // per run) and a longer list is read into pageable memory
   const int64_t impr_cap = std::max<int64_t>(1, remaining);
+  const int64_t impr_pre = std::min<int64_t>(impr_cap, 8 * static_cast<int64_t>(n) + 64);
   auto al = [](int64_t x) { return (x + 255) & ~int64_t(255); };
   const int64_t o_runs = 0, o_pool = al(o_runs + static_cast<int64_t>(sizeof(GaRun)) * n),
                 o_res = al(o_pool + run_bytes * n),
@@ -949,7 +954,7 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
                 h_jump = al(h_opts + 8 * static_cast<int64_t>(opts.size())),
                 h_best = al(h_jump + 32 * static_cast<int64_t>(jumps.size())),
                 h_imp = al(h_best + 2 * static_cast<int64_t>(stride) * n),
-                h_total = al(h_imp + static_cast<int64_t>(sizeof(GaImpr)) * impr_cap);
+                h_total = al(h_imp + static_cast<int64_t>(sizeof(GaImpr)) * impr_pre);
   // staging sized generously once per context: pinned allocations are slow
   ctx.h_ga.reserve(std::max<int64_t>(h_total, int64_t{32} << 20));
   uint8_t* H = ctx.h_ga.p;
@@ -1054,9 +1059,8 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   cuda_check(cudaMemcpyAsync(H + h_ctl, D + o_ctl, 8 * kGaCtlWords, cudaMemcpyDeviceToHost, st), "D2H ga ctl");
   cuda_check(cudaMemcpy2DAsync(H + h_best, 2 * stride, D + o_pool, run_bytes, 2 * stride, n,
                                cudaMemcpyDeviceToHost, st), "D2H ga best plans");
-  // improvements: a bounded prefix rides in the same batch (a round usually
-  // records a few per run); only a longer list costs a second round trip
-  const int64_t impr_pre = std::min<int64_t>(impr_cap, 8 * static_cast<int64_t>(n) + 64);
+  // improvements: the bounded prefix rides in the same batch; only a longer
+  // list costs a second round trip
   cuda_check(cudaMemcpyAsync(H + h_imp, D + o_impr, sizeof(GaImpr) * impr_pre,
                              cudaMemcpyDeviceToHost, st), "D2H ga improvements");
   cuda_check(cudaStreamSynchronize(st), "ga_kernel");
@@ -1065,10 +1069,14 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   ctx.eval_ms += ms;
   const int64_t n_impr = static_cast<int64_t>(hctl[kGaCtlImpr]);
   if (n_impr > impr_cap) throw InternalError("device GA improvement list overflow");
-  if (n_impr > impr_pre)
-    cuda_check(cudaMemcpy(H + h_imp + sizeof(GaImpr) * impr_pre, D + o_impr + sizeof(GaImpr) * impr_pre,
+  std::vector<GaImpr> imp(reinterpret_cast<GaImpr*>(H + h_imp),
+                          reinterpret_cast<GaImpr*>(H + h_imp) + std::min(n_impr, impr_pre));
+  if (n_impr > impr_pre) {
+    imp.resize(static_cast<size_t>(n_impr));
+    cuda_check(cudaMemcpy(imp.data() + impr_pre, D + o_impr + sizeof(GaImpr) * impr_pre,
                           sizeof(GaImpr) * (n_impr - impr_pre), cudaMemcpyDeviceToHost),
                "D2H ga improvements");
+  }
   ctx.plans_evaluated += static_cast<int64_t>(hctl[kGaCtlEvals]);
   ctx.canonical_bytes += static_cast<int64_t>(hctl[kGaCtlBytes]);
   ctx.h2d_bytes += h2d;
@@ -1084,8 +1092,6 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
     c.ng = ng;
     return c;
   };
-  std::vector<GaImpr> imp(reinterpret_cast<GaImpr*>(H + h_imp),
-                          reinterpret_cast<GaImpr*>(H + h_imp) + n_impr);
   std::stable_sort(imp.begin(), imp.end(), [](const GaImpr& a, const GaImpr& b) {
     return a.run != b.run ? a.run < b.run : a.local_idx < b.local_idx;
   });

@@ -48,12 +48,20 @@ def sweep_range(total: int, rank: int, world: int):
 
 
 def merge_argmin(best_cost: float, best_k: int, n_feasible: int):
-    """global (min cost, lowest k) over the ranks' shard results; one
-    all-gather of 24 B per rank. An empty shard reports best_cost = inf."""
-    t = torch.tensor([best_cost, float(best_k), float(n_feasible)], dtype=torch.float64,
-                     device=_dev())
-    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
-    dist.all_gather(out, t)
-    rows = [(float(o[0]), int(o[1]), int(o[2])) for o in (x.cpu() for x in out)]
+    """global (min cost, lowest k) over the ranks' shard results: one all-gather
+    of the float64 cost and one of the int64 (k, n_feasible) pair per rank, so
+    plan indices keep all 64 bits (an empty shard reports inf and k = 2^64-1)."""
+    world = dist.get_world_size()
+    c = torch.tensor([best_cost], dtype=torch.float64, device=_dev())
+    k_signed = best_k - (1 << 64) if best_k >= (1 << 63) else best_k
+    i = torch.tensor([k_signed, n_feasible], dtype=torch.int64, device=_dev())
+    cs = [torch.empty_like(c) for _ in range(world)]
+    ks = [torch.empty_like(i) for _ in range(world)]
+    dist.all_gather(cs, c)
+    dist.all_gather(ks, i)
+    rows = []
+    for cc, kk in zip(cs, ks):
+        k, nf = (int(x) for x in kk.cpu().tolist())
+        rows.append((float(cc.cpu().item()), k + (1 << 64) if k < 0 else k, nf))
     best = min(rows, key=lambda r: (r[0], r[1]))
     return best[0], best[1], sum(r[2] for r in rows)

@@ -164,7 +164,7 @@ EXPORTED_SYMBOLS = [
     "hpg_result_info", "hpg_result_b_m", "hpg_result_trace", "hpg_result_arms",
     "hpg_result_halvings", "hpg_result_survivor_sizes", "hpg_result_survivors",
     "hpg_result_plan", "hpg_result_breakdown", "hpg_result_free", "hpg_sweep",
-    "hpg_sweep_resident", "hpg_exhaustive", "hpg_exhaustive_estimate",
+    "hpg_sweep_resident", "hpg_sweep_dist", "hpg_exhaustive", "hpg_exhaustive_estimate",
 ]
 
 
@@ -219,6 +219,8 @@ def load_library(path: str = LIB_PATH):
                                 P(C.c_uint8), P(C.c_double), P(C.c_uint64), P(C.c_uint64), E, L]),
         "hpg_sweep_resident": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                          P(_SweepStats), E, L]),
+        "hpg_sweep_dist": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
+                                     P(C.c_uint8), P(_SweepStats), E, L]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -732,6 +734,18 @@ class Engine:
             out["costs"] = [costs[i] for i in range(count)]
             out["feasible"] = [bool(feas[i]) for i in range(count)]
         return out
+
+    def sweep_dist(self, seed: int, total: int, rank: int, world: int,
+                   nccl_id: Optional[bytes] = None) -> dict:
+        """hpg_sweep_dist: this rank's contiguous shard of [0, total), global argmin
+        merged over the ranks with one NCCL all-gather."""
+        st = _SweepStats()
+        err = C.create_string_buffer(1024)
+        idb = (C.c_uint8 * 128)(*(nccl_id or bytes(128)))
+        rc = self.lib.hpg_sweep_dist(self._h, seed, total, rank, world, idb, C.byref(st), err,
+                                     1024)
+        _raise(rc, err)
+        return {f: getattr(st, f) for f, _ in _SweepStats._fields_}
 
     def sweep_resident(self, seed: int, k0: int, count: int) -> dict:
         st = _SweepStats()

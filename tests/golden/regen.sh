@@ -23,9 +23,16 @@ $R evalplans fixtures/n256.workflow.json fixtures/n256.topology.json 7 16 $G/eva
 $R fuzz 20251018 250 $G/fuzz_eval.json
 $R search fixtures/c1.workflow.json fixtures/c1.topology.json 1000 42 $G/search_c1_b1000.json $KNOBS
 $R search fixtures/c2.workflow.json fixtures/c2.topology.json 1000 42 $G/search_c2_b1000.json $KNOBS
+# every search config at both parity budgets (B in {10^3, 10^4})
+for c in c3 c4; do
+  $R search fixtures/$c.workflow.json fixtures/$c.topology.json 1000 42 $G/search_${c}_b1000.json $KNOBS
+done
+for c in c1 c2 c3 c4; do
+  $R search fixtures/$c.workflow.json fixtures/$c.topology.json 10000 42 $G/search_${c}_b10000.json $KNOBS
+done
 $R search fixtures/n256.workflow.json fixtures/n256.topology.json 1000 42 $G/search_n256_b1000.json $KNOBS
 $R searchfuzz 777 60 $G/searchfuzz.json
-for c in c1 c2 c3; do
+for c in c1 c2 c3 c4; do
   $R ga fixtures/$c.workflow.json fixtures/$c.topology.json $G/ga_$c.json $KNOBS
 done
 $R sweep fixtures/c4.workflow.json fixtures/c4.topology.json 42 0 2000 $G/sweep_c4.json

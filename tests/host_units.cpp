@@ -54,7 +54,8 @@ int main(int argc, char** argv) {
     const Poly256 q = jump_poly(D);
     rng_apply_jump(b0, q.data());
     for (int w = 0; w < 4; ++w) jbad += a0.s[w] != b0.s[w];
-    const std::vector<Poly256>& tb = jump_table(D, 31);
+    const JumpTable tbp = jump_table(D, 31);
+    const std::vector<Poly256>& tb = *tbp;
     for (int L : {1, 7, 31}) {
       Rng c0(jr.next()), d0 = c0;
       for (uint64_t k = 0; k < D * L; ++k) c0.next();

@@ -130,8 +130,12 @@ def check_search(res, gold, ctx=""):
     return bad
 
 
-@pytest.mark.parametrize("name", ["search_c1_b1000.json", "search_c2_b1000.json",
-                                  "search_n256_b1000.json"])
+SEARCH_GOLDENS = ["search_c1_b1000.json", "search_c2_b1000.json", "search_c3_b1000.json",
+                  "search_c4_b1000.json", "search_c1_b10000.json", "search_c2_b10000.json",
+                  "search_c3_b10000.json", "search_c4_b10000.json", "search_n256_b1000.json"]
+
+
+@pytest.mark.parametrize("name", SEARCH_GOLDENS)
 def test_search_configs_identical(name):
     from paper_2512_12476_b200 import SearchKnobs
     g = load(name)
@@ -156,7 +160,7 @@ def test_search_fuzz_identical():
     assert not bad, "\n".join(bad[:30])
 
 
-@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3"])
+@pytest.mark.parametrize("cfg_name", ["c1", "c2", "c3", "c4"])
 def test_ga_search_identical(cfg_name):
     """ga_search on its own (search.hpp:127-135): twelve arms per config with
     slices 1-400 and random seeds, feasible and infeasible; evaluations used,
@@ -279,3 +283,99 @@ def test_host_ga_paths_identical(env):
                         "search_configs or search_fuzz or ga_search"],
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_sweep_stratified_sample_vs_reference():
+    """config-5 parity at the benchmarked scale: the reference
+    end_to_end_cost (oracle/_ref/ref_dump, run here on the host CPU) on a
+    stratified 10^5-plan sample of the 10^8-plan sweep (100 blocks of 1000
+    plans, block b at k = b * 10^6) against the GPU sweep of the same plans:
+    every cost bit, every memory_feasible flag and the sample's argmin."""
+    import os
+    import struct
+    import subprocess
+    import tempfile
+    from paper_2512_12476_b200 import Engine, load_topology, load_workflow
+    from golden_util import FIXTURES
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "ref_dump")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_dump not built (needs /root/reference at build time)")
+    wf_p = os.path.join(FIXTURES, "c4.workflow.json")
+    tp_p = os.path.join(FIXTURES, "c4.topology.json")
+    total, blocks, blen = 10 ** 8, 100, 1000
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "sample.bin")
+        r = subprocess.run([exe, "sample_sweep", wf_p, tp_p, "42", str(total), str(blocks),
+                            str(blen), str(max(1, len(os.sched_getaffinity(0)))), out],
+                           capture_output=True, text=True, timeout=1200, check=True)
+        raw = open(out, "rb").read()
+    recs = [struct.unpack_from("<QQQ", raw, 24 * i) for i in range(blocks * blen)]
+    stride = total // blocks
+    bad, best = [], (float("inf"), None)
+    with Engine(load_workflow(wf_p), load_topology(tp_p)) as eng:
+        for b in range(blocks):
+            got = eng.sweep(42, b * stride, blen)
+            for i in range(blen):
+                k, bits, feas = recs[b * blen + i]
+                assert k == b * stride + i
+                gbits = struct.unpack("<Q", struct.pack("<d", got["costs"][i]))[0]
+                if gbits != bits or bool(feas) != got["feasible"][i]:
+                    bad.append(k)
+                if feas:
+                    c = struct.unpack("<d", struct.pack("<Q", bits))[0]
+                    if c < best[0]:
+                        best = (c, k)
+            if got["n_feasible"]:
+                assert got["best_k"] >= b * stride and got["best_k"] < b * stride + blen
+    assert not bad, f"{len(bad)} mismatches, first k={bad[:5]}"
+    import json
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["best_k"] == best[1] and same(line["best_dec"], best[0])
+
+
+def _search_golden_in_thread(name, device, out, key):
+    from paper_2512_12476_b200 import Engine, SearchKnobs, parse_topology, parse_workflow
+    try:
+        g = load(name)
+        with Engine(parse_workflow(g["workflow"]), parse_topology(g["topology"]),
+                    device=device) as eng:
+            for _ in range(2):
+                res = eng.nested_sha_search(SearchKnobs.from_json(g["knobs"]))
+                out.setdefault(key, []).extend(check_search(res, g, f"{name}@{device}"))
+    except Exception as e:  # surfaced by the assertion below
+        out.setdefault(key, []).append(repr(e))
+
+
+def test_two_contexts_two_threads_one_device():
+    """separate contexts are thread-safe (hpg.h): two threads drive two contexts
+    on the same GPU at once (different problems, so different shared-memory
+    sizes and launch parameters) and both reproduce the reference"""
+    import threading
+    out = {}
+    ts = [threading.Thread(target=_search_golden_in_thread, args=(n, 0, out, n))
+          for n in ("search_c1_b1000.json", "search_c2_b1000.json")]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    bad = [b for v in out.values() for b in v]
+    assert len(out) == 2 and not bad, "\n".join(bad[:20])
+
+
+def test_contexts_on_two_devices_one_process():
+    """per-device launch state: contexts on GPU 0 and GPU 1 of one process, used
+    from two threads, both reproduce the reference (needs >= 2 GPUs)"""
+    import threading
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = {}
+    ts = [threading.Thread(target=_search_golden_in_thread, args=(n, d, out, d))
+          for d, n in ((0, "search_c2_b1000.json"), (1, "search_c1_b1000.json"))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    bad = [b for v in out.values() for b in v]
+    assert len(out) == 2 and not bad, "\n".join(bad[:20])
