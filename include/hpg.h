@@ -32,7 +32,7 @@ extern "C" {
 #define HPG_INFEASIBLE 4
 #define HPG_INTERNAL 5
 
-#define HPG_ABI_VERSION 2
+#define HPG_ABI_VERSION 3
 
 /* ---- problem: workflow + topology (workflow.hpp:67-77, topology.hpp:24-104) ---- */
 
@@ -290,6 +290,7 @@ typedef struct {
   double eval_ms;            /* eval_kernel only */
   double gen_ms;
   int64_t launches;
+  uint64_t global_slab_plans; /* plans whose scratch did not fit the warp's shared slab */
 } hpg_sweep_stats;
 
 int hpg_sweep_resident(hpg_ctx* ctx, uint64_t seed, uint64_t k0, uint64_t count,

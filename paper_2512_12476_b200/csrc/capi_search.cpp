@@ -158,60 +158,72 @@ struct SweepAcc {
   uint64_t best_k = ~0ull, nf = 0, x = 0, bytes = 0;
   float gen_ms = 0, eval_ms = 0, total_ms = 0;
   int64_t launches = 0;
+  uint64_t global_slab_plans = 0;
 };
 
+// Plans [k0, k0 + count) in chunks: gen_kernel writes a chunk's compact plan
+// records into HBM, sweep_kernel scores them (end_to_end_cost, per-plan
+// carve) and folds them into per-warp (argmin, feasible count, checksum)
+// partials that persist across chunks. Chunks follow each other on the
+// context's stream with no host round trip; the partials come back once.
+// With costs/feasible requested, each chunk's per-plan results are copied out.
 void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs,
                uint8_t* feasible, SweepAcc& acc) {
   const Problem& P = C.prob;
   SweepTablesDev& tb = sweep_tables(C);
   const int64_t stride = (80 + P.T * P.N + 7) & ~int64_t(7);
-  const int64_t chunk = static_cast<int64_t>(std::min<uint64_t>(count, 1ull << 20));
+  const int64_t chunk = static_cast<int64_t>(std::min<uint64_t>(std::max<uint64_t>(count, 1), 1ull << 21));
+  const bool want = costs || feasible;
   C.d_recs.reserve(static_cast<size_t>(chunk) * stride);
-  C.d_res.reserve(chunk);
+  if (want) C.d_res.reserve(chunk);
   C.d_best.reserve(2);
-  const int red_blocks = 4 * C.n_sm;
-  DevBuf<SweepPartial> partial;
-  partial.reserve(red_blocks);
-  std::vector<SweepPartial> hp(red_blocks);
-  Carve cv{};
-  cv.n_dev = P.N;
-  cv.n_tasks = P.T;
-  cv.max_w = cv.max_sl = cv.max_slots = cv.max_cells = cv.max_dpk = P.T * P.N;
+  static const int warps_env = [] {
+    const char* v = std::getenv("HPG_SWEEP_WARPS");  // diagnostics: 2, 4 or 8 plan-warps per CTA
+    return v ? std::atoi(v) : 8;
+  }();
+  static const int slab_env = [] {
+    const char* v = std::getenv("HPG_SWEEP_SLAB");  // diagnostics: cap the per-warp slab (bytes)
+    return v ? std::atoi(v) : 0;
+  }();
+  SweepLaunch L;
+  cuda_check(sweep_plan(P.N, P.T, C.n_sm, warps_env, slab_env, L), "sweep_kernel configuration");
+  const int64_t nwarps = static_cast<int64_t>(L.grid) * L.warps;
+  C.d_sweep_gslab.reserve(static_cast<size_t>(nwarps * L.gslab_bytes));
+  C.d_sweep_part.reserve(static_cast<size_t>(nwarps) * sizeof(SweepPartial) + 16);
+  L.gslab = C.d_sweep_gslab.p;
+  L.part = reinterpret_cast<SweepPartial*>(C.d_sweep_part.p);
+  L.n_global = reinterpret_cast<unsigned long long*>(C.d_sweep_part.p +
+                                                      nwarps * sizeof(SweepPartial));
+  std::vector<SweepPartial> hp(static_cast<size_t>(nwarps), SweepPartial{kInf, ~0ull, 0, 0});
   const DevCostConfig cfg = to_dev_cfg(default_cost_config());
   cudaStream_t st = C.stream;
-  cudaEvent_t e0, e1, e2, e3;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventCreate(&e2);
-  cudaEventCreate(&e3);
+  cuda_check(cudaMemcpyAsync(L.part, hp.data(), sizeof(SweepPartial) * nwarps,
+                             cudaMemcpyHostToDevice, st), "H2D sweep partials");
+  cuda_check(cudaMemsetAsync(L.n_global, 0, 8, st), "memset");
   cuda_check(cudaMemsetAsync(C.d_best.p, 0, 16, st), "memset");
-  for (uint64_t done = 0; done < count;) {
+  // independent random plans share no rings: the ring memo would only fill
+  DevProblem sweep_prob = C.dprob;
+  sweep_prob.ring_cache = nullptr;
+  const int64_t n_chunks = (static_cast<int64_t>(count) + chunk - 1) / chunk;
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(3 * std::max<int64_t>(n_chunks, 1)));
+  for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+  std::vector<EvalResult> r;
+  int64_t ci = 0;
+  for (uint64_t done = 0; done < count; ++ci) {
     const int64_t n = static_cast<int64_t>(std::min<uint64_t>(chunk, count - done));
     const uint64_t kk = k0 + done;
-    cudaEventRecord(e0, st);
+    cudaEventRecord(ev[3 * ci], st);
     cuda_check(launch_gen(tb, seed, kk, n, C.d_recs.p, stride, C.d_best.p, st), "gen_kernel");
-    int grid = 0;
-    cuda_check(eval_grid(cv, static_cast<int>(n), C.n_sm, grid), "eval_kernel occupancy");
-    const int64_t scratch = eval_scratch_doubles(P.N, C.max_nl);
-    C.d_scratch.reserve(static_cast<size_t>(grid) * scratch);
-    cudaEventRecord(e1, st);
-    // independent random plans share no rings: the ring memo would only fill
-    DevProblem sweep_prob = C.dprob;
-    sweep_prob.ring_cache = nullptr;
-    cuda_check(launch_eval(sweep_prob, cfg, cv, 0, C.d_recs.p, nullptr, nullptr, kModeE2E,
-                           static_cast<int>(n), stride, nullptr, nullptr, C.d_res.p, nullptr, nullptr,
-                           C.d_scratch.p, scratch, grid, st),
-               "eval_kernel");
-    cudaEventRecord(e2, st);
-    cuda_check(launch_reduce(C.d_res.p, n, kk, partial.p, red_blocks, st), "reduce_kernel");
-    cudaEventRecord(e3, st);
-    acc.launches += 3;
-    C.launches += 3;
+    cudaEventRecord(ev[3 * ci + 1], st);
+    cuda_check(launch_sweep(sweep_prob, cfg, C.d_recs.p, stride, n, kk, L,
+                            want ? C.d_res.p : nullptr, st),
+               "sweep_kernel");
+    cudaEventRecord(ev[3 * ci + 2], st);
+    acc.launches += 2;
+    C.launches += 2;
     C.plans_evaluated += n;
-    cuda_check(cudaMemcpyAsync(hp.data(), partial.p, sizeof(SweepPartial) * red_blocks,
-                               cudaMemcpyDeviceToHost, st), "D2H partial");
-    if (costs || feasible) {
-      std::vector<EvalResult> r(n);
+    if (want) {
+      r.resize(static_cast<size_t>(n));
       cuda_check(cudaMemcpyAsync(r.data(), C.d_res.p, sizeof(EvalResult) * n,
                                  cudaMemcpyDeviceToHost, st), "D2H results");
       cuda_check(cudaStreamSynchronize(st), "sweep");
@@ -220,31 +232,33 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
         if (feasible) feasible[done + i] = (r[i].flags & kResFeasOut) ? 1 : 0;
       }
     }
-    cuda_check(cudaStreamSynchronize(st), "sweep");
-    float a = 0, b = 0, c = 0;
-    cudaEventElapsedTime(&a, e0, e1);
-    cudaEventElapsedTime(&b, e1, e2);
-    cudaEventElapsedTime(&c, e2, e3);
-    acc.gen_ms += a;
-    acc.eval_ms += b;
-    acc.total_ms += a + b + c;
-    for (const SweepPartial& p : hp) {
-      acc.nf += p.n_feasible;
-      acc.x ^= p.xor_bits;
-      if (p.best < acc.best || (p.best == acc.best && p.best_k < acc.best_k)) {
-        acc.best = p.best;
-        acc.best_k = p.best_k;
-      }
-    }
     done += n;
   }
-  unsigned long long bytes = 0;
-  cuda_check(cudaMemcpy(&bytes, C.d_best.p, 8, cudaMemcpyDeviceToHost), "D2H bytes");
-  acc.bytes = bytes;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
-  cudaEventDestroy(e3);
+  unsigned long long tail[2] = {0, 0};
+  cuda_check(cudaMemcpyAsync(hp.data(), L.part, sizeof(SweepPartial) * nwarps,
+                             cudaMemcpyDeviceToHost, st), "D2H sweep partials");
+  cuda_check(cudaMemcpyAsync(&tail[0], C.d_best.p, 8, cudaMemcpyDeviceToHost, st), "D2H bytes");
+  cuda_check(cudaMemcpyAsync(&tail[1], L.n_global, 8, cudaMemcpyDeviceToHost, st), "D2H spills");
+  cuda_check(cudaStreamSynchronize(st), "sweep");
+  for (int64_t c = 0; c < ci; ++c) {
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[3 * c], ev[3 * c + 1]);
+    cudaEventElapsedTime(&b, ev[3 * c + 1], ev[3 * c + 2]);
+    acc.gen_ms += a;
+    acc.eval_ms += b;
+  }
+  if (ci > 0) cudaEventElapsedTime(&acc.total_ms, ev[0], ev[3 * (ci - 1) + 2]);
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (const SweepPartial& p : hp) {
+    acc.nf += p.n_feasible;
+    acc.x ^= p.xor_bits;
+    if (p.best < acc.best || (p.best == acc.best && p.best_k < acc.best_k)) {
+      acc.best = p.best;
+      acc.best_k = p.best_k;
+    }
+  }
+  acc.bytes = tail[0];
+  acc.global_slab_plans = tail[1];
 }
 
 }  // namespace
@@ -490,6 +504,7 @@ int hpg_sweep_resident(hpg_ctx* ctx, uint64_t seed, uint64_t k0, uint64_t count,
     stats->eval_ms = acc.eval_ms;
     stats->gen_ms = acc.gen_ms;
     stats->launches = acc.launches;
+    stats->global_slab_plans = acc.global_slab_plans;
   });
 }
 
@@ -542,6 +557,7 @@ int hpg_sweep_dist(hpg_ctx* ctx, uint64_t seed, uint64_t total, int rank, int wo
     stats->eval_ms = acc.eval_ms;
     stats->gen_ms = acc.gen_ms;
     stats->launches = acc.launches;
+    stats->global_slab_plans = acc.global_slab_plans;
   });
 }
 

@@ -208,4 +208,52 @@ HPG_HD int carve2_bytes(const Carve& c) {
          (c.n_warps > 1 ? (c.n_warps - 1) * team_scratch_bytes(c) : 0);
 }
 
+// ---- end_to_end-only scratch sized per plan (the config-5 sweep kernel) ----
+//
+// end_to_end_cost of one plan touches: weights/micro-batches per replica,
+// the geometry memo per (task, replica, stage) cell, the DP-ring memo per
+// (task, stage, shard), cell pieces of the task in flight, ring scratch of the
+// largest ring, per-device residency and stage maps, and the memory tables per
+// (task, stage). The balancers' arrays are not needed. Exact sizes of one plan:
+struct E2ESizes {
+  int32_t w, sl, slots, cells, dpk;  // sums over tasks of dp, pp, dp*pp*tp, dp*pp, pp*tp
+  int32_t cell_max, ring_max;        // max over tasks of dp*pp, max(dp, tp)
+};
+
+HPG_HD E2ESizes e2e_sizes(const RecOffsets& o, const RecHeader& h, int n_tasks) {
+  E2ESizes z;
+  z.w = o.w[n_tasks];
+  z.sl = o.sl[n_tasks];
+  z.slots = o.dev[n_tasks];
+  z.cells = o.cell[n_tasks];
+  z.dpk = o.dpk[n_tasks];
+  z.cell_max = 1;
+  z.ring_max = 8;  // ring_small's 8-vertex scratch
+  for (int t = 0; t < n_tasks; ++t) {
+    const int c = h.dp[t] * h.pp[t];
+    z.cell_max = z.cell_max > c ? z.cell_max : c;
+    z.ring_max = z.ring_max > h.dp[t] ? z.ring_max : h.dp[t];
+    z.ring_max = z.ring_max > h.tp[t] ? z.ring_max : h.tp[t];
+  }
+  return z;
+}
+
+// worst case over every plan of a problem (N devices, T tasks)
+HPG_HD E2ESizes e2e_sizes_max(int N, int T) {
+  E2ESizes z;
+  z.w = z.slots = z.cells = z.dpk = T * N;
+  z.sl = T * N;
+  z.cell_max = N;
+  z.ring_max = N > 8 ? N : 8;
+  return z;
+}
+
+HPG_HD int e2e_carve_bytes(const E2ESizes& z, int N, int T) {
+  return 2 * carve_round(8 * z.w) + 3 * carve_round(8 * z.cells) + carve_round(8 * z.dpk) +
+         carve_round(4 * z.dpk) + carve_round(8 * N) + 4 * carve_round(8 * z.cell_max) +
+         carve_round(8 * z.ring_max) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
+         carve_round(8 * T * 7) + carve_round(4 * z.sl) + 2 * carve_round(8 * z.sl) +
+         carve_round(z.slots) + carve_round(T * N) + 2 * carve_round(z.ring_max);
+}
+
 }  // namespace hpg

@@ -24,6 +24,7 @@
 
 #include "eval_device.cuh"
 #include "eval_launch.hpp"
+#include "sweep.hpp"
 
 namespace hpg {
 namespace dev {
@@ -916,3 +917,4 @@ cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
 }  // namespace hpg
 
 #include "ga_kernel.cuh"
+#include "sweep_kernel.cuh"

@@ -6,8 +6,9 @@
 //                  layouts (enumerate_layouts order, search.cpp:127-150), a device
 //                  permutation and one shuffle per task; writes a compact plan
 //                  record into the HBM plan table
-//   eval_kernel    end_to_end_cost per plan (one warp per plan)
-//   reduce_kernel  argmin over memory-feasible plans by (cost, k), feasible
+//   sweep_kernel   end_to_end_cost per plan (one warp per plan, many plan-warps
+//                  per SM; sweep_kernel.cuh) folded into per-warp partials:
+//                  argmin over memory-feasible plans by (cost, k), feasible
 //                  count, XOR checksum of the cost bit patterns
 #include <cuda_runtime.h>
 
@@ -103,57 +104,6 @@ __global__ void gen_kernel(SweepTablesDev tb, uint64_t seed, uint64_t k0, int64_
   if ((threadIdx.x & 31) == 0 && my_bytes) atomicAdd(bytes_acc, static_cast<unsigned long long>(my_bytes));
 }
 
-__global__ void reduce_kernel(const EvalResult* __restrict__ res, int64_t n, uint64_t k0,
-                              SweepPartial* __restrict__ out) {
-  double best = kInf;
-  uint64_t best_k = ~0ull, nf = 0, x = 0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const EvalResult r = res[i];
-    x ^= static_cast<uint64_t>(__double_as_longlong(r.cost));
-    if (r.flags & kResFeasOut) {
-      ++nf;
-      const uint64_t k = k0 + static_cast<uint64_t>(i);
-      if (r.cost < best || (r.cost == best && k < best_k)) {
-        best = r.cost;
-        best_k = k;
-      }
-    }
-  }
-  __shared__ double sb[32];
-  __shared__ unsigned long long sk[32], sn[32], sx[32];
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const uint64_t okk = __shfl_xor_sync(0xffffffffu, best_k, o);
-    if (ob < best || (ob == best && okk < best_k)) {
-      best = ob;
-      best_k = okk;
-    }
-    nf += __shfl_xor_sync(0xffffffffu, nf, o);
-    x ^= __shfl_xor_sync(0xffffffffu, x, o);
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sb[w] = best;
-    sk[w] = best_k;
-    sn[w] = nf;
-    sx[w] = x;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    SweepPartial p{kInf, ~0ull, 0, 0};
-    for (int i = 0; i < (blockDim.x >> 5); ++i) {
-      if (sb[i] < p.best || (sb[i] == p.best && sk[i] < p.best_k)) {
-        p.best = sb[i];
-        p.best_k = sk[i];
-      }
-      p.n_feasible += sn[i];
-      p.xor_bits ^= sx[i];
-    }
-    out[blockIdx.x] = p;
-  }
-}
-
 }  // namespace dev
 
 cudaError_t launch_gen(const SweepTablesDev& tb, uint64_t seed, uint64_t k0, int64_t n,
@@ -164,12 +114,6 @@ cudaError_t launch_gen(const SweepTablesDev& tb, uint64_t seed, uint64_t k0, int
   const int64_t blocks = (n + threads - 1) / threads;
   dev::gen_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(tb, seed, k0, n, d_recs,
                                                                      stride, d_bytes);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_reduce(const EvalResult* d_res, int64_t n, uint64_t k0, SweepPartial* d_out,
-                          int blocks, cudaStream_t st) {
-  dev::reduce_kernel<<<blocks, 256, 0, st>>>(d_res, n, k0, d_out);
   return cudaGetLastError();
 }
 

@@ -25,10 +25,26 @@ struct SweepPartial {
   unsigned long long xor_bits;
 };
 
+// the sweep scoring kernel (sweep_kernel.cuh): CTAs of `warps` plan-warps,
+// each with a `slab_bytes` shared-memory slab for its plan's scratch, plus a
+// CTA-shared copy of the link-class matrix when N*N <= kClsSweepMax
+constexpr int kClsSweepMax = 16384;
+struct SweepLaunch {
+  int warps = 8;
+  int grid = 0;
+  int slab_bytes = 0;
+  int cls_bytes = 0;
+  int64_t gslab_bytes = 0;       // per-warp global fallback slab (worst-case plan)
+  uint8_t* gslab = nullptr;      // [grid * warps * gslab_bytes]
+  SweepPartial* part = nullptr;  // [grid * warps], merged in place across chunks
+  unsigned long long* n_global = nullptr;  // plans that used the global slab
+};
+cudaError_t sweep_plan(int N, int T, int n_sm, int warps, int slab_req, SweepLaunch& L);
+cudaError_t launch_sweep(const DevProblem& P, const DevCostConfig& cfg, const uint8_t* d_recs,
+                         int64_t stride, int64_t n, uint64_t k0, SweepLaunch& L,
+                         EvalResult* d_res, cudaStream_t st);
+
 cudaError_t launch_gen(const SweepTablesDev& tb, uint64_t seed, uint64_t k0, int64_t n,
                        uint8_t* d_recs, int64_t stride, unsigned long long* d_bytes,
                        cudaStream_t st);
-cudaError_t launch_reduce(const EvalResult* d_res, int64_t n, uint64_t k0, SweepPartial* d_out,
-                          int blocks, cudaStream_t st);
-
 }  // namespace hpg

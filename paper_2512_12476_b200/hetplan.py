@@ -152,7 +152,7 @@ class _SweepStats(C.Structure):
     _fields_ = [("best_cost", C.c_double), ("best_k", C.c_uint64), ("n_feasible", C.c_uint64),
                 ("xor_bits", C.c_uint64), ("canonical_bytes", C.c_uint64),
                 ("total_ms", C.c_double), ("eval_ms", C.c_double), ("gen_ms", C.c_double),
-                ("launches", C.c_int64)]
+                ("launches", C.c_int64), ("global_slab_plans", C.c_uint64)]
 
 
 _lib = None

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(LIB)
     missing = [n for n in declared_functions() if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.hpg_abi_version() == 2
+    assert lib.hpg_abi_version() == 3
 
 
 @pytest.mark.skipif(not os.path.exists(LIB), reason="libhpg.so not built")
