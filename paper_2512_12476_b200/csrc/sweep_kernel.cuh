@@ -169,6 +169,9 @@ cudaError_t sweep_plan_impl(int N, int T, int n_sm, int slab_req, SweepLaunch& L
   if (slab < 1024) return cudaErrorInvalidConfiguration;
   L.slab_bytes = slab;
   L.gslab_bytes = carve_round(e2e_carve_bytes(e2e_sizes_max(N, T), N, T));
+  // the occupancy query needs the dynamic shared-memory opt-in first
+  e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), L.cls_bytes + kWarps * L.slab_bytes);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = occupancy_per_sm(reinterpret_cast<const void*>(kern), 32 * kWarps,
                        L.cls_bytes + kWarps * L.slab_bytes, &per_sm);
