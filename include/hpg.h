@@ -194,6 +194,36 @@ int hpg_balance(hpg_ctx* ctx, const hpg_plan_table* plans, const hpg_cost_config
                 int which, int32_t* out_stage_layers, double* out_weights, double* out_e2e,
                 char* err, size_t errlen);
 
+/* ---- cost-model primitives, one call each (cost_model.hpp:49-111) ---- */
+
+/* ResolvedTask (plan.hpp:125-133): a task's layout, its micro-batches per
+ * replica (nm_replica, from resolve_plan's apportionment) and its flat
+ * (replica, stage, shard) device assignment as topology indices. */
+typedef struct {
+  int32_t task_slot;             /* workflow task index (id order) */
+  int32_t dp, pp, tp;
+  const int32_t* stage_layers;   /* [pp] */
+  const int64_t* nm_replica;     /* [dp] */
+  const int32_t* devices;        /* [dp * pp * tp] */
+} hpg_resolved_task;
+
+/* task_cost_detail / task_cost (cost_model.hpp:103-111). agg[7] = TaskCost
+ * (comp, tp, pp, dp, bubble, hbm, total); optional stage[dp * pp * 4] =
+ * StagePiece (comp, tp, pp, hbm) in [replica][stage] order; optional
+ * bubble[dp] = bubble_replica. resident_weight_bytes: optional [N] per-device
+ * residency (end_to_end_cost's path); NULL = the task's own weights (the
+ * standalone call, cost_model.cpp:320-323). */
+int hpg_task_cost(hpg_ctx* ctx, const hpg_resolved_task* task, const hpg_cost_config* cfg,
+                  const double* resident_weight_bytes, double agg[7], double* stage,
+                  double* bubble, char* err, size_t errlen);
+/* min_ring_bottleneck (cost_model.hpp:49-52): InputError for an empty set or
+ * an index outside the topology, 0 for one device. */
+int hpg_ring_bottleneck(hpg_ctx* ctx, const int32_t* devices, int32_t n, double volume_bytes,
+                        double* out, char* err, size_t errlen);
+/* min_pair_cost (cost_model.hpp:54-56): +inf when either set is empty. */
+int hpg_pair_cost(hpg_ctx* ctx, const int32_t* src, int32_t n_src, const int32_t* dst,
+                  int32_t n_dst, double volume_bytes, double* out, char* err, size_t errlen);
+
 /* nested_sha_search (search.hpp:115-118). */
 int hpg_search(hpg_ctx* ctx, const hpg_knobs* knobs, hpg_search_result** out, char* err,
                size_t errlen);

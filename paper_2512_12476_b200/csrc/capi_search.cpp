@@ -185,7 +185,12 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
     const char* v = std::getenv("HPG_SWEEP_SLAB");  // diagnostics: cap the per-warp slab (bytes)
     return v ? std::atoi(v) : 0;
   }();
+  static const int sync_env = [] {
+    const char* v = std::getenv("HPG_SWEEP_SYNC");  // diagnostics: 0/1 CTA-wide phase barriers
+    return v ? std::atoi(v) : 0;
+  }();
   SweepLaunch L;
+  L.sync = sync_env;
   cuda_check(sweep_plan(P.N, P.T, C.n_sm, warps_env, slab_env, L), "sweep_kernel configuration");
   const int64_t nwarps = static_cast<int64_t>(L.grid) * L.warps;
   C.d_sweep_gslab.reserve(static_cast<size_t>(nwarps * L.gslab_bytes));

@@ -807,6 +807,7 @@ eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
     l.n_warps = static_cast<int32_t>(blockDim.x >> 5);
     l.job_words[0] = l.job_words[1] = 0;
     l.job = l.job_words;
+    l.cta_sync = 0;
     const bool smem_cls = l.cls != nullptr;
     if (!smem_cls) l.cls = P.cls;
     for (int w = 1; w < l.n_warps; ++w) {
@@ -918,3 +919,4 @@ cudaError_t launch_eval(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
 
 #include "ga_kernel.cuh"
 #include "sweep_kernel.cuh"
+#include "prim_kernels.cuh"

@@ -89,6 +89,7 @@ struct Ws {
   unsigned long long cc_sig;  // class-cost order signature of the staged volume
   int32_t cc_sig_ok;
   double cc_vol;              // staged volume
+  int32_t cta_sync;           // sweep: CTA-wide barrier (threads) before each task's cost, 0 = none
   long long* prof;            // diagnostics: this plan's profile slots
   const uint8_t* cls;         // link class matrix [N*N]: shared-memory copy or P.cls
   // helper-warp team (one plan per CTA, warp 0 leads)
@@ -1348,6 +1349,9 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
   }
   double tot[kMaxTasks];
   for (int t = 0; t < P.n_tasks; ++t) {
+    // sweep kernel: the CTA's plan-warps enter every task's cost together, so
+    // they fetch the same code at the same time (instruction-cache sharing)
+    if (s.cta_sync) bar_sync(5, s.cta_sync);
     if (!((s.agg_ok >> t) & 1)) {
       task_cost(P, cfg, s, t, true, s.agg + 7 * t);
       if (lane == 0) s.agg_ok |= 1 << t;

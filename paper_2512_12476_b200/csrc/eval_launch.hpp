@@ -41,4 +41,13 @@ cudaError_t launch_best_half(const double* d_scores, const int32_t* d_seg_off,
                              const int32_t* d_arm_idx, int n_seg, int32_t* d_keep_flags,
                              double* d_events, cudaStream_t st);
 
+// cost-model primitives, one call each (prim_kernels.cuh)
+int task_cost_smem(const RecHeader& h, int N, int T);
+cudaError_t launch_task_cost(const DevProblem& P, const DevCostConfig& cfg, int t,
+                             const RecHeader& h, const int32_t* d_sl, const int64_t* d_nm,
+                             const uint8_t* d_dev, const double* d_resident, double* d_out,
+                             cudaStream_t st);
+cudaError_t launch_ring(const DevProblem& P, int mode, const uint8_t* d_a, int na,
+                        const uint8_t* d_b, int nb, double volume, double* d_out, cudaStream_t st);
+
 }  // namespace hpg

@@ -1461,6 +1461,7 @@ ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscrat
     l.n_warps = kTeam;
     l.job_words[0] = l.job_words[1] = 0;
     l.job = l.job_words;
+    l.cta_sync = 0;
     if (!cv.cls_smem) l.cls = P.cls;  // else carved last (the init scratch stays below it)
     for (int w = 1; w < kTeam; ++w) {
       team[w] = l;

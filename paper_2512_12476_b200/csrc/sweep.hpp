@@ -38,6 +38,7 @@ struct SweepLaunch {
   uint8_t* gslab = nullptr;      // [grid * warps * gslab_bytes]
   SweepPartial* part = nullptr;  // [grid * warps], merged in place across chunks
   unsigned long long* n_global = nullptr;  // plans that used the global slab
+  int sync = 0;  // CTA-wide barriers at plan and task boundaries (shared instruction fetch)
 };
 cudaError_t sweep_plan(int N, int T, int n_sm, int warps, int slab_req, SweepLaunch& L);
 cudaError_t launch_sweep(const DevProblem& P, const DevCostConfig& cfg, const uint8_t* d_recs,

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
 sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, int64_t stride,
              int64_t n, uint64_t k0, int slab_bytes, int cls_smem, uint8_t* __restrict__ gslab,
              int64_t gslab_bytes, EvalResult* __restrict__ res, SweepPartial* __restrict__ part,
-             unsigned long long* __restrict__ n_global) {
+             unsigned long long* __restrict__ n_global, int sync) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ Ws ws[kWarps];
   const int lane = threadIdx.x & 31;
@@ -85,6 +85,7 @@ sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, 
     s.job = s.job_words;
     s.dtab_stride = 0;
     s.cls = cls_smem ? smem : P.cls;
+    s.cta_sync = sync ? static_cast<int32_t>(blockDim.x) : 0;
   }
   __syncthreads();
   uint8_t* const slab = smem + cls_bytes + warp * slab_bytes;
@@ -92,7 +93,17 @@ sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, 
   uint8_t* const gbase = gslab + gw * gslab_bytes;
   SweepPartial acc = part[gw];
   unsigned long long spilled = 0;
-  for (int64_t p = gw; p < n; p += static_cast<int64_t>(gridDim.x) * kWarps) {
+  // with sync, every warp runs the same number of rounds (one plan or an idle
+  // pass each) so the CTA's barriers line up: one at the start of a plan and
+  // one before each task's cost (end_to_end)
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t rounds = sync ? (n + step - 1) / step : 0;
+  for (int64_t p = gw, rd = 0; sync ? rd < rounds : p < n; p += step, ++rd) {
+    if (sync) bar_sync(5, blockDim.x);
+    if (p >= n) {
+      for (int t = 0; t < T; ++t) bar_sync(5, blockDim.x);
+      continue;
+    }
     const uint8_t* rec = recs + p * stride;
     if (lane == 0) {
       RecHeader h;
@@ -143,7 +154,7 @@ cudaError_t sweep_launch_impl(const DevProblem& P, const DevCostConfig& cfg, con
   if (e != cudaSuccess) return e;
   kern<<<L.grid, 32 * kWarps, dyn, st>>>(P, cfg, d_recs, stride, n, k0, L.slab_bytes,
                                          L.cls_bytes > 0 ? 1 : 0, L.gslab, L.gslab_bytes, d_res,
-                                         L.part, L.n_global);
+                                         L.part, L.n_global, L.sync);
   return cudaGetLastError();
 }
 

@@ -86,3 +86,27 @@ def test_reference_adapter_shim():
     r = subprocess.run([exe, os.path.join(root, "fixtures")], capture_output=True, text=True,
                        timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_on_engine():
+    """the reference's own acceptance suite (proj/tests/acceptance.cpp, compiled
+    unmodified) with its end_to_end_cost / nested_sha_search / exhaustive_search
+    / balance_data / balance_layers calls served by the engine
+    (integration/engine_redirect.cpp, built by `make -C oracle
+    acceptance_engine`): 10/10 criteria must pass, and the engine must have
+    served every hot-path call"""
+    import re
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "acceptance_engine")
+    if not os.path.exists(exe):
+        pytest.skip("acceptance_engine not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1800)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith(("PASS", "FAIL"))]
+    assert len(lines) == 10 and all(ln.startswith("PASS") for ln in lines), r.stdout + r.stderr
+    m = re.search(r"end_to_end_cost (\d+), nested_sha_search (\d+), exhaustive_search (\d+), "
+                  r"balance_data (\d+), balance_layers (\d+)", r.stderr)
+    assert m and all(int(x) > 0 for x in m.groups()), r.stderr[-2000:]
+    assert r.returncode == 0
+
