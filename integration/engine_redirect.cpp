@@ -8,6 +8,8 @@
 //   hetplan::nested_sha_search (search.hpp:115-118)
 //   hetplan::exhaustive_search (search.hpp:137-150)
 //   hetplan::balance_data / balance_layers (balance.hpp:23-31)
+//   hetplan::task_cost_detail / task_cost (cost_model.hpp:103-111)
+//   hetplan::min_ring_bottleneck / min_pair_cost (cost_model.hpp:49-56)
 //
 // lands here and goes through the reference-side adapter (hetplan_b200.hpp)
 // and the C ABI (include/hpg.h) to the GPU. The checkers stay reference code:
@@ -19,13 +21,15 @@
 #include "hetplan_b200.hpp"
 
 namespace {
-int g_calls[5];
+int g_calls[9];
 struct Report {
   ~Report() {
     std::fprintf(stderr,
                  "engine_redirect: end_to_end_cost %d, nested_sha_search %d, exhaustive_search %d, "
-                 "balance_data %d, balance_layers %d calls served by the B200 engine\n",
-                 g_calls[0], g_calls[1], g_calls[2], g_calls[3], g_calls[4]);
+                 "balance_data %d, balance_layers %d, task_cost_detail %d, task_cost %d, "
+                 "min_ring_bottleneck %d, min_pair_cost %d calls served by the B200 engine\n",
+                 g_calls[0], g_calls[1], g_calls[2], g_calls[3], g_calls[4], g_calls[5],
+                 g_calls[6], g_calls[7], g_calls[8]);
   }
 } g_report;
 }  // namespace
@@ -63,6 +67,31 @@ Plan balance_layers(const Plan& plan, const WorkflowGraph& wf, const DeviceTopol
   ++g_calls[4];
   b200::Engine e(wf, topo);
   return e.balance_layers(plan, cfg);
+}
+
+TaskCostDetail task_cost_detail(const WorkflowGraph& wf, const ResolvedTask& rt,
+                                const DeviceTopology& topo, const CostModelConfig& cfg,
+                                std::span<const double> resident_weight_bytes) {
+  ++g_calls[5];
+  return b200::task_cost_detail(wf, rt, topo, cfg, resident_weight_bytes);
+}
+
+TaskCost task_cost(const WorkflowGraph& wf, const ResolvedTask& rt, const DeviceTopology& topo,
+                   const CostModelConfig& cfg) {
+  ++g_calls[6];
+  return b200::task_cost(wf, rt, topo, cfg);
+}
+
+double min_ring_bottleneck(std::span<const int> devices, double volume_bytes,
+                           const DeviceTopology& topo) {
+  ++g_calls[7];
+  return b200::min_ring_bottleneck(devices, volume_bytes, topo);
+}
+
+double min_pair_cost(std::span<const int> src, std::span<const int> dst, double volume_bytes,
+                     const DeviceTopology& topo) {
+  ++g_calls[8];
+  return b200::min_pair_cost(src, dst, volume_bytes, topo);
 }
 
 }  // namespace hetplan

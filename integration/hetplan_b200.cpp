@@ -183,6 +183,67 @@ std::vector<CostBreakdown> Engine::end_to_end_cost(const std::vector<Plan>& plan
   return r;
 }
 
+TaskCostDetail Engine::task_cost_detail(const ResolvedTask& rt, const CostModelConfig& cfg,
+                                        std::span<const double> resident_weight_bytes) {
+  int slot = -1;
+  for (size_t i = 0; i < wf_.tasks.size(); ++i)
+    if (wf_.tasks[i].id == rt.task_id) slot = static_cast<int>(i);
+  if (slot < 0 || !rt.layout) throw InputError("resolved task is not part of the workflow");
+  const ParallelLayout& l = *rt.layout;
+  hpg_resolved_task t{};
+  t.task_slot = slot;
+  t.dp = l.dp;
+  t.pp = l.pp;
+  t.tp = l.tp;
+  std::vector<int32_t> sl(l.stage_layers.begin(), l.stage_layers.end());
+  std::vector<int32_t> dv(rt.devices.begin(), rt.devices.end());
+  t.stage_layers = sl.data();
+  t.nm_replica = rt.nm_replica.data();
+  t.devices = dv.data();
+  if (!resident_weight_bytes.empty() &&
+      resident_weight_bytes.size() != static_cast<size_t>(topo_.size()))
+    throw InputError("resident weight bytes must have one entry per device");
+  const hpg_cost_config c = cfg_c(cfg);
+  double agg[7];
+  std::vector<double> stage(4 * static_cast<size_t>(l.dp) * l.pp), bubble(l.dp);
+  char err[1024];
+  check(hpg_task_cost(ctx_, &t, &c, resident_weight_bytes.empty() ? nullptr : resident_weight_bytes.data(),
+                      agg, stage.data(), bubble.data(), err, sizeof(err)),
+        err);
+  TaskCostDetail d;
+  d.agg = TaskCost{agg[0], agg[1], agg[2], agg[3], agg[4], agg[5], agg[6]};
+  d.stage.assign(l.dp, std::vector<StagePiece>(l.pp));
+  for (int i = 0; i < l.dp; ++i)
+    for (int j = 0; j < l.pp; ++j) {
+      const double* q = stage.data() + 4 * (static_cast<size_t>(i) * l.pp + j);
+      d.stage[i][j] = StagePiece{q[0], q[1], q[2], q[3]};
+    }
+  d.bubble_replica = bubble;
+  d.nm_replica = rt.nm_replica;
+  return d;
+}
+
+double Engine::min_ring_bottleneck(std::span<const int> devices, double volume_bytes) {
+  std::vector<int32_t> dv(devices.begin(), devices.end());
+  double out = 0;
+  char err[1024];
+  check(hpg_ring_bottleneck(ctx_, dv.data(), static_cast<int32_t>(dv.size()), volume_bytes, &out,
+                            err, sizeof(err)),
+        err);
+  return out;
+}
+
+double Engine::min_pair_cost(std::span<const int> src, std::span<const int> dst,
+                             double volume_bytes) {
+  std::vector<int32_t> a(src.begin(), src.end()), b(dst.begin(), dst.end());
+  double out = 0;
+  char err[1024];
+  check(hpg_pair_cost(ctx_, a.data(), static_cast<int32_t>(a.size()), b.data(),
+                      static_cast<int32_t>(b.size()), volume_bytes, &out, err, sizeof(err)),
+        err);
+  return out;
+}
+
 std::vector<MemoryViolation> Engine::check_memory(const Plan& plan, const MemoryModel& mm) {
   TableC tc;
   make_table({&plan}, wf_, topo_, tc);
@@ -379,6 +440,48 @@ ExhaustiveResult exhaustive_search(const WorkflowGraph& wf, const DeviceTopology
                                    const SearchKnobs& knobs) {
   Engine e(wf, topo);
   return e.exhaustive_search(knobs);
+}
+
+TaskCostDetail task_cost_detail(const WorkflowGraph& wf, const ResolvedTask& rt,
+                                const DeviceTopology& topo, const CostModelConfig& cfg,
+                                std::span<const double> resident_weight_bytes) {
+  Engine e(wf, topo);
+  return e.task_cost_detail(rt, cfg, resident_weight_bytes);
+}
+
+TaskCost task_cost(const WorkflowGraph& wf, const ResolvedTask& rt, const DeviceTopology& topo,
+                   const CostModelConfig& cfg) {
+  return b200::task_cost_detail(wf, rt, topo, cfg, {}).agg;
+}
+
+namespace {
+// a one-task workflow: the engine context needs one, link costs never read it
+const WorkflowGraph& placeholder_workflow() {
+  static const WorkflowGraph wf = [] {
+    WorkflowGraph w;
+    RlTask t;
+    t.id = 6;
+    t.kind = TaskKind::kTraining;
+    t.model.hidden_size = 8;
+    t.model.intermediate_size = 16;
+    t.model.num_layers = 1;
+    w.tasks.push_back(t);
+    return w;
+  }();
+  return wf;
+}
+}  // namespace
+
+double min_ring_bottleneck(std::span<const int> devices, double volume_bytes,
+                           const DeviceTopology& topo) {
+  Engine e(placeholder_workflow(), topo);
+  return e.min_ring_bottleneck(devices, volume_bytes);
+}
+
+double min_pair_cost(std::span<const int> src, std::span<const int> dst, double volume_bytes,
+                     const DeviceTopology& topo) {
+  Engine e(placeholder_workflow(), topo);
+  return e.min_pair_cost(src, dst, volume_bytes);
 }
 
 }  // namespace hetplan::b200

@@ -10,6 +10,7 @@
 
 #include <memory>
 #include <optional>
+#include <span>
 #include <vector>
 
 #include "hetplan/balance.hpp"
@@ -35,6 +36,12 @@ class Engine {
   // end_to_end_cost (cost_model.hpp:115-117), batched
   std::vector<CostBreakdown> end_to_end_cost(const std::vector<Plan>& plans,
                                              const CostModelConfig& cfg = {});
+  // task_cost_detail / task_cost (cost_model.hpp:103-111) of one resolved task
+  TaskCostDetail task_cost_detail(const ResolvedTask& rt, const CostModelConfig& cfg = {},
+                                  std::span<const double> resident_weight_bytes = {});
+  // min_ring_bottleneck / min_pair_cost (cost_model.hpp:49-56)
+  double min_ring_bottleneck(std::span<const int> devices, double volume_bytes);
+  double min_pair_cost(std::span<const int> src, std::span<const int> dst, double volume_bytes);
   // check_memory (plan.hpp:116-119)
   std::vector<MemoryViolation> check_memory(const Plan& plan, const MemoryModel& mm = {});
   // balance_data / balance_layers (balance.hpp:23-31)
@@ -62,5 +69,15 @@ SearchResult nested_sha_search(const WorkflowGraph& wf, const DeviceTopology& to
                                const std::vector<TaskGrouping>* tg_override = nullptr);
 ExhaustiveResult exhaustive_search(const WorkflowGraph& wf, const DeviceTopology& topo,
                                    const SearchKnobs& knobs);
+TaskCostDetail task_cost_detail(const WorkflowGraph& wf, const ResolvedTask& rt,
+                                const DeviceTopology& topo, const CostModelConfig& cfg = {},
+                                std::span<const double> resident_weight_bytes = {});
+TaskCost task_cost(const WorkflowGraph& wf, const ResolvedTask& rt, const DeviceTopology& topo,
+                   const CostModelConfig& cfg = {});
+// link costs depend on the topology only: staged with a placeholder workflow
+double min_ring_bottleneck(std::span<const int> devices, double volume_bytes,
+                           const DeviceTopology& topo);
+double min_pair_cost(std::span<const int> src, std::span<const int> dst, double volume_bytes,
+                     const DeviceTopology& topo);
 
 }  // namespace hetplan::b200
