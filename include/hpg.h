@@ -238,6 +238,29 @@ int hpg_search_dist(hpg_ctx* ctx, const hpg_knobs* knobs, int rank, int world,
                     const uint8_t nccl_id[128], hpg_search_result** out, char* err,
                     size_t errlen);
 
+/* The per-round exchange hpg_search_dist performs after every SHA round
+ * (SURVEY.md §8 E1), over a caller-supplied all-gather instead of NCCL, for
+ * launchers with their own process group (and the CPU tests, over gloo).
+ * allgather(user, send, recv, bytes): every rank sends `bytes`, recv gets
+ * world * bytes in rank order; returns 0 on success. The runs of the round
+ * are dealt to ranks by budget (owner[r]: longest slice first to the
+ * least-loaded rank); used[r] / best[r] are inputs for the caller's own runs
+ * and outputs for all; mine[] holds the improvements (run, 1-based local
+ * evaluation index, cost) of the caller's runs; all[] receives every run's
+ * improvements, by run, each run's in its owner's order (*n_all = count;
+ * HPG_USAGE if cap is too small). Every rank ends with identical outputs. */
+typedef int (*hpg_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
+typedef struct {
+  int64_t run;
+  int64_t local_idx;
+  double cost;
+} hpg_improvement;
+int hpg_dist_exchange(int rank, int world, hpg_allgather_fn allgather, void* user,
+                      int32_t n_runs, const int64_t* slices, int32_t* owner, int64_t* used,
+                      double* best, const hpg_improvement* mine, int64_t n_mine,
+                      hpg_improvement* all, int64_t cap, int64_t* n_all, char* err,
+                      size_t errlen);
+
 /* ga_search (search.hpp:132-135): one (task grouping, GPU grouping) arm.
  * task_group[T] and gpu_counts[n_groups]; rng_seed is the Rng seed. */
 int hpg_ga_search(hpg_ctx* ctx, const int32_t* task_group, int32_t n_groups,

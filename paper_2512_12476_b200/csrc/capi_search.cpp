@@ -148,6 +148,9 @@ SweepTablesDev& sweep_tables(Ctx& C) {
   h.tb.tg_ng = reinterpret_cast<const int8_t*>(b + o_ng);
   h.tb.opt_off = reinterpret_cast<const int32_t*>(b + o_off);
   h.tb.opt = reinterpret_cast<const int16_t*>(b + o_opt);
+  h.tb.train_mask = 0;
+  for (int s = 0; s < T; ++s)
+    if (C.dprob.task[s].kind == kTraining) h.tb.train_mask |= 1 << s;
   C.d_sweep_tables = h.blob;
   C.sweep_tb = h.tb;
   return C.sweep_tb;
@@ -189,6 +192,10 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
     const char* v = std::getenv("HPG_SWEEP_SYNC");  // diagnostics: 0/1 CTA-wide phase barriers
     return v ? std::atoi(v) : 0;
   }();
+  static const int sort_env = [] {
+    const char* v = std::getenv("HPG_SWEEP_SORT");  // diagnostics: 0/1 work-class ordering
+    return v ? std::atoi(v) : 0;
+  }();
   SweepLaunch L;
   L.sync = sync_env;
   cuda_check(sweep_plan(P.N, P.T, C.n_sm, warps_env, slab_env, L), "sweep_kernel configuration");
@@ -200,6 +207,14 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
   L.n_global = reinterpret_cast<unsigned long long*>(C.d_sweep_part.p +
                                                       nwarps * sizeof(SweepPartial));
   std::vector<SweepPartial> hp(static_cast<size_t>(nwarps), SweepPartial{kInf, ~0ull, 0, 0});
+  SweepOrder ord;
+  if (sort_env) {
+    const size_t kb = (4 * static_cast<size_t>(chunk) + 255) & ~size_t(255);
+    C.d_sweep_order.reserve(2 * kb + (sizeof(uint32_t) << kSweepKeyBits));
+    ord.keys = reinterpret_cast<uint32_t*>(C.d_sweep_order.p);
+    ord.order = reinterpret_cast<uint32_t*>(C.d_sweep_order.p + kb);
+    ord.hist = reinterpret_cast<uint32_t*>(C.d_sweep_order.p + 2 * kb);
+  }
   const DevCostConfig cfg = to_dev_cfg(default_cost_config());
   cudaStream_t st = C.stream;
   cuda_check(cudaMemcpyAsync(L.part, hp.data(), sizeof(SweepPartial) * nwarps,
@@ -218,10 +233,16 @@ void run_sweep(Ctx& C, uint64_t seed, uint64_t k0, uint64_t count, double* costs
     const int64_t n = static_cast<int64_t>(std::min<uint64_t>(chunk, count - done));
     const uint64_t kk = k0 + done;
     cudaEventRecord(ev[3 * ci], st);
-    cuda_check(launch_gen(tb, seed, kk, n, C.d_recs.p, stride, C.d_best.p, st), "gen_kernel");
+    cuda_check(launch_gen(tb, seed, kk, n, C.d_recs.p, stride, C.d_best.p,
+                          sort_env ? &ord : nullptr, st), "gen_kernel");
+    if (sort_env) {
+      cuda_check(launch_order(ord, n, st), "order kernels");
+      acc.launches += 2;
+      C.launches += 2;
+    }
     cudaEventRecord(ev[3 * ci + 1], st);
     cuda_check(launch_sweep(sweep_prob, cfg, C.d_recs.p, stride, n, kk, L,
-                            want ? C.d_res.p : nullptr, st),
+                            sort_env ? ord.order : nullptr, want ? C.d_res.p : nullptr, st),
                "sweep_kernel");
     cudaEventRecord(ev[3 * ci + 2], st);
     acc.launches += 2;

@@ -229,7 +229,7 @@ struct Ctx {
   DevBuf<double> d_costs;
   DevBuf<uint8_t> d_feas;
   DevBuf<unsigned long long> d_best;
-  DevBuf<uint8_t> d_sweep_gslab, d_sweep_part;
+  DevBuf<uint8_t> d_sweep_gslab, d_sweep_part, d_sweep_order;
   DevBuf<uint8_t> d_prim;  // cost-model primitive calls (capi_prim.cpp)  // sweep_kernel fallback slabs, per-warp partials
   // best-half
   DevBuf<double> d_scores, d_events;

@@ -3,6 +3,7 @@
 // lockstep waves against eval_kernel. Reference: proj/src/search.cpp,
 // proj/src/combinatorics.cpp, proj/include/hetplan/rng.hpp.
 #include "search.hpp"
+#include "dist_exchange.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -1421,68 +1422,54 @@ struct TgArm {
 
 // ---- multi-GPU: per-run records all-gathered after every lockstep round ----
 
-struct RunSummary {
-  int64_t used;
-  double best;
-  int64_t n_impr;
-  int64_t pad;
-};
-struct ImprRec {
-  int64_t run;
-  int64_t local_idx;
-  double cost;
-};
+// NCCL all-gather over the context's communicator, staged through HBM
+class NcclTransport : public Transport {
+ public:
+  NcclTransport(Ctx& ctx, Dist& d) : ctx_(ctx), d_(d) {}
+  int rank() const override { return d_.rank; }
+  int world() const override { return d_.world; }
+  void allgather(const void* send, void* recv, size_t bytes) override {
+    DevBuf<uint8_t>& snd = ctx_.d_xch_send;
+    DevBuf<uint8_t>& rcv = ctx_.d_xch_recv;
+    snd.reserve(bytes + 8);
+    rcv.reserve(bytes * d_.world + 8);
+    if (bytes == 0) return;
+    cuda_check(cudaMemcpyAsync(snd.p, send, bytes, cudaMemcpyHostToDevice, ctx_.stream), "H2D");
+    dist_allgather(d_, snd.p, rcv.p, bytes, ctx_.stream);
+    cuda_check(cudaMemcpyAsync(recv, rcv.p, bytes * d_.world, cudaMemcpyDeviceToHost, ctx_.stream),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(ctx_.stream), "allgather");
+    ctx_.h2d_bytes += static_cast<int64_t>(bytes);
+    ctx_.d2h_bytes += static_cast<int64_t>(bytes * d_.world);
+  }
 
-template <typename T>
-std::vector<T> allgather_host(Ctx& ctx, Dist& d, const std::vector<T>& mine) {
-  const size_t bytes = sizeof(T) * mine.size();
-  DevBuf<uint8_t>& snd = ctx.d_xch_send;
-  DevBuf<uint8_t>& rcv = ctx.d_xch_recv;
-  snd.reserve(bytes + 8);
-  rcv.reserve(bytes * d.world + 8);
-  std::vector<T> out(mine.size() * d.world);
-  if (bytes == 0) return out;
-  cuda_check(cudaMemcpyAsync(snd.p, mine.data(), bytes, cudaMemcpyHostToDevice, ctx.stream), "H2D");
-  dist_allgather(d, snd.p, rcv.p, bytes, ctx.stream);
-  cuda_check(cudaMemcpyAsync(out.data(), rcv.p, bytes * d.world, cudaMemcpyDeviceToHost,
-                             ctx.stream), "D2H");
-  cuda_check(cudaStreamSynchronize(ctx.stream), "allgather");
-  ctx.h2d_bytes += static_cast<int64_t>(bytes);
-  ctx.d2h_bytes += static_cast<int64_t>(bytes * d.world);
-  return out;
-}
+ private:
+  Ctx& ctx_;
+  Dist& d_;
+};
 
 // Every rank ends with identical (used, best, improvement list) for every run
 // of the round; improvement plans stay with the owning rank.
 void exchange_runs(Ctx& ctx, Dist& d, std::vector<ArmRun*>& all, double now) {
-  const int R = static_cast<int>(all.size());
-  std::vector<RunSummary> s(R, RunSummary{0, 0.0, 0, 0});
-  std::vector<ImprRec> imp;
-  for (int r = 0; r < R; ++r) {
-    if (r % d.world != d.rank) continue;
-    s[r] = RunSummary{all[r]->used, all[r]->best, static_cast<int64_t>(all[r]->impr.size()), 0};
-    for (const auto& im : all[r]->impr) imp.push_back(ImprRec{r, im.local_idx, im.cost});
+  const size_t R = all.size();
+  std::vector<int> owner(R);
+  std::vector<RunRecord> rec(R);
+  std::vector<std::vector<ImprRecord>> imp(R);
+  for (size_t r = 0; r < R; ++r) {
+    owner[r] = all[r]->owner;
+    rec[r] = RunRecord{all[r]->used, all[r]->best};
+    if (owner[r] == d.rank)
+      for (const auto& im : all[r]->impr)
+        imp[r].push_back(ImprRecord{static_cast<int64_t>(r), im.local_idx, im.cost});
   }
-  const std::vector<RunSummary> gs = allgather_host(ctx, d, s);
-  std::vector<int64_t> cnt{static_cast<int64_t>(imp.size())};
-  const std::vector<int64_t> gc = allgather_host(ctx, d, cnt);
-  const int64_t mx = *std::max_element(gc.begin(), gc.end());
-  imp.resize(mx, ImprRec{-1, 0, 0.0});
-  const std::vector<ImprRec> gi = allgather_host(ctx, d, imp);
-  for (int r = 0; r < R; ++r) {
-    const int owner = r % d.world;
-    if (owner == d.rank) continue;
-    const RunSummary& x = gs[static_cast<size_t>(owner) * R + r];
-    all[r]->used = x.used;
-    all[r]->best = x.best;
+  NcclTransport tr(ctx, d);
+  exchange_round(tr, owner, rec, imp);
+  for (size_t r = 0; r < R; ++r) {
+    if (owner[r] == d.rank) continue;
+    all[r]->used = rec[r].used;
+    all[r]->best = rec[r].best;
     all[r]->impr.clear();
-  }
-  for (int k = 0; k < d.world; ++k) {
-    if (k == d.rank) continue;
-    for (int64_t e = 0; e < gc[k]; ++e) {
-      const ImprRec& ir = gi[static_cast<size_t>(k) * mx + e];
-      all[ir.run]->impr.push_back(Improvement{ir.local_idx, ir.cost, Cand{}, now});
-    }
+    for (const ImprRecord& x : imp[r]) all[r]->impr.push_back(Improvement{x.local_idx, x.cost, Cand{}, now});
   }
 }
 
@@ -1632,11 +1619,14 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
         }
       }
       if (dist && dist->world > 1) {
-        // runs dealt round-robin over ranks (balanced by count; every run of
-        // one (task grouping, round) has the same slice), then all-gathered
+        // runs dealt over the ranks by budget (longest slice first to the
+        // least-loaded rank, dist_exchange.cpp deal_runs), then all-gathered
+        std::vector<int64_t> slices(batch.size());
+        for (size_t r = 0; r < batch.size(); ++r) slices[r] = batch[r]->slice;
+        const std::vector<int> owner = deal_runs(slices, dist->world);
         std::vector<ArmRun*> mine;
         for (size_t r = 0; r < batch.size(); ++r) {
-          batch[r]->owner = static_cast<int>(r % dist->world);
+          batch[r]->owner = owner[r];
           if (batch[r]->owner == dist->rank) mine.push_back(batch[r]);
         }
         run_lockstep(ctx, K, mine, clock, waves);
@@ -1742,13 +1732,15 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   if (consumed > K.budget) throw InternalError("search overspent its budget");
   if (inc_ti >= 0 && dist && dist->world > 1) {
     // the incumbent's plan lives on the rank that evaluated it
-    std::vector<int64_t> sz{dist->rank == inc_owner ? static_cast<int64_t>(inc_plan.rec.size())
-                                                    : 0};
-    const std::vector<int64_t> gsz = allgather_host(ctx, *dist, sz);
+    NcclTransport tr(ctx, *dist);
+    const int64_t sz = dist->rank == inc_owner ? static_cast<int64_t>(inc_plan.rec.size()) : 0;
+    std::vector<int64_t> gsz(dist->world);
+    tr.allgather(&sz, gsz.data(), 8);
     const int64_t bytes = gsz[inc_owner];
     std::vector<uint8_t> mine(bytes, 0);
     if (dist->rank == inc_owner) std::memcpy(mine.data(), inc_plan.rec.data(), bytes);
-    const std::vector<uint8_t> all = allgather_host(ctx, *dist, mine);
+    std::vector<uint8_t> all(static_cast<size_t>(bytes) * dist->world);
+    tr.allgather(mine.data(), all.data(), static_cast<size_t>(bytes));
     inc_plan.rec.assign(all.begin() + static_cast<int64_t>(inc_owner) * bytes,
                         all.begin() + static_cast<int64_t>(inc_owner + 1) * bytes);
     rec_offsets(inc_plan.hdr(), inc_plan.o);

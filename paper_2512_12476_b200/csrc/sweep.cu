@@ -20,9 +20,22 @@
 namespace hpg {
 namespace dev {
 
+// 3-bit work class of one task of a plan (end_to_end_cost's phases: cell
+// pieces, TP ring bounds, PP pairs, DP rings), on a log2 scale
+__device__ __forceinline__ uint32_t work_class(int dp, int pp, int tp, bool train) {
+  const int ncell = dp * pp;
+  uint32_t w = 2u * ((ncell + 31) >> 5) + static_cast<uint32_t>(((dp + 31) >> 5) * pp);
+  if (tp > 1) w += static_cast<uint32_t>(((ncell * tp + 31) >> 5) * tp);
+  if (pp > 1) w += static_cast<uint32_t>((ncell * tp * tp + 31) >> 5);
+  if (train && dp > 1) w += static_cast<uint32_t>(pp * tp * (dp == 2 ? 1 : (dp <= 8 ? 24 : 4 * dp)));
+  const int lg = 31 - __clz(w | 1u);
+  return static_cast<uint32_t>(lg < 3 ? 0 : (lg - 3 > 7 ? 7 : lg - 3));
+}
+
 __global__ void gen_kernel(SweepTablesDev tb, uint64_t seed, uint64_t k0, int64_t n,
                            uint8_t* __restrict__ recs, int64_t stride,
-                           unsigned long long* __restrict__ bytes_acc) {
+                           unsigned long long* __restrict__ bytes_acc,
+                           uint32_t* __restrict__ keys, uint32_t* __restrict__ hist) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint64_t my_bytes = 0;
   if (idx < n) {
@@ -99,21 +112,81 @@ __global__ void gen_kernel(SweepTablesDev tb, uint64_t seed, uint64_t k0, int64_
     // sum_t (3 + pp_t + slots_t) + 9 result bytes
     my_bytes = 1 + ng + 9;
     for (int s = 0; s < T; ++s) my_bytes += 3 + h.pp[s] + ro.dev[s + 1] - ro.dev[s];
+    if (keys) {
+      uint32_t key = 0;
+      for (int s = 0; s < T; ++s)
+        key = (key << 3) | work_class(h.dp[s], h.pp[s], h.tp[s], (tb.train_mask >> s) & 1);
+      keys[idx] = key;
+      atomicAdd(&hist[key], 1u);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) my_bytes += __shfl_xor_sync(0xffffffffu, my_bytes, o);
   if ((threadIdx.x & 31) == 0 && my_bytes) atomicAdd(bytes_acc, static_cast<unsigned long long>(my_bytes));
 }
 
+// exclusive scan of the key histogram in place (one CTA of 1024 threads)
+__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* __restrict__ hist, int bins) {
+  __shared__ uint32_t warp_tot[32];
+  const int per = bins / blockDim.x;
+  uint32_t* h = hist + threadIdx.x * per;
+  uint32_t sum = 0;
+  for (int i = 0; i < per; ++i) sum += h[i];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t x = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = warp_tot[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;
+  }
+  __syncthreads();
+  uint32_t run = x - sum + (w > 0 ? warp_tot[w - 1] : 0u);
+  for (int i = 0; i < per; ++i) {
+    const uint32_t c = h[i];
+    h[i] = run;
+    run += c;
+  }
+}
+
+__global__ void order_scatter_kernel(const uint32_t* __restrict__ keys, uint32_t* __restrict__ off,
+                                     uint32_t* __restrict__ order, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) order[atomicAdd(&off[keys[i]], 1u)] = static_cast<uint32_t>(i);
+}
+
 }  // namespace dev
+
+cudaError_t launch_order(const SweepOrder& ord, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  dev::order_scan_kernel<<<1, 1024, 0, st>>>(ord.hist, 1 << kSweepKeyBits);
+  const int threads = 256;
+  dev::order_scatter_kernel<<<static_cast<unsigned>((n + threads - 1) / threads), threads, 0, st>>>(
+      ord.keys, ord.hist, ord.order, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gen(const SweepTablesDev& tb, uint64_t seed, uint64_t k0, int64_t n,
                        uint8_t* d_recs, int64_t stride, unsigned long long* d_bytes,
-                       cudaStream_t st) {
+                       const SweepOrder* ord, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (ord) {
+    const cudaError_t e = cudaMemsetAsync(ord->hist, 0, sizeof(uint32_t) << kSweepKeyBits, st);
+    if (e != cudaSuccess) return e;
+  }
   const int threads = 128;
   const int64_t blocks = (n + threads - 1) / threads;
   dev::gen_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(tb, seed, k0, n, d_recs,
-                                                                     stride, d_bytes);
+                                                                     stride, d_bytes,
+                                                                     ord ? ord->keys : nullptr,
+                                                                     ord ? ord->hist : nullptr);
   return cudaGetLastError();
 }
 

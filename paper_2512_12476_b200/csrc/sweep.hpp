@@ -16,6 +16,19 @@ struct SweepTablesDev {
   const int8_t* tg_ng;      // [n_tgs]
   const int32_t* opt_off;   // [T * (N + 1) + 1] layout options of (slot, count)
   const int16_t* opt;       // [n_opt * 3] (dp, pp, tp) in enumerate_layouts order
+  int32_t train_mask;       // bit t: task slot t is a training task (DP rings)
+};
+
+// Work-class grouping of a chunk (sweep.cu): gen_kernel gives every plan a
+// key of 3-bit per-task work classes (kSweepKeyBits bits) and counts them; a
+// counting sort orders the chunk by key, so the plan-warps of one CTA score
+// plans of similar shape side by side (their per-task phase barriers then
+// wait little; see sweep_kernel.cuh).
+constexpr int kSweepKeyBits = 18;
+struct SweepOrder {
+  uint32_t* keys = nullptr;   // [chunk]
+  uint32_t* hist = nullptr;   // [1 << kSweepKeyBits], bin offsets after the scan
+  uint32_t* order = nullptr;  // [chunk] plan index in key order
 };
 
 struct SweepPartial {
@@ -43,9 +56,11 @@ struct SweepLaunch {
 cudaError_t sweep_plan(int N, int T, int n_sm, int warps, int slab_req, SweepLaunch& L);
 cudaError_t launch_sweep(const DevProblem& P, const DevCostConfig& cfg, const uint8_t* d_recs,
                          int64_t stride, int64_t n, uint64_t k0, SweepLaunch& L,
-                         EvalResult* d_res, cudaStream_t st);
+                         const uint32_t* d_order, EvalResult* d_res, cudaStream_t st);
 
 cudaError_t launch_gen(const SweepTablesDev& tb, uint64_t seed, uint64_t k0, int64_t n,
                        uint8_t* d_recs, int64_t stride, unsigned long long* d_bytes,
-                       cudaStream_t st);
+                       const SweepOrder* ord, cudaStream_t st);
+// counting sort of the chunk's plans by their gen_kernel keys (ord->order)
+cudaError_t launch_order(const SweepOrder& ord, int64_t n, cudaStream_t st);
 }  // namespace hpg

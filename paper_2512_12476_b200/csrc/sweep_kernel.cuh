@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
 sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, int64_t stride,
              int64_t n, uint64_t k0, int slab_bytes, int cls_smem, uint8_t* __restrict__ gslab,
              int64_t gslab_bytes, EvalResult* __restrict__ res, SweepPartial* __restrict__ part,
-             unsigned long long* __restrict__ n_global, int sync) {
+             unsigned long long* __restrict__ n_global, int sync,
+             const uint32_t* __restrict__ order) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ Ws ws[kWarps];
   const int lane = threadIdx.x & 31;
@@ -104,7 +105,10 @@ sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, 
       for (int t = 0; t < T; ++t) bar_sync(5, blockDim.x);
       continue;
     }
-    const uint8_t* rec = recs + p * stride;
+    // the chunk's plans in work-class order: consecutive plans (one round of
+    // a CTA) have similar per-task shapes
+    const int64_t q = order ? static_cast<int64_t>(__ldg(order + p)) : p;
+    const uint8_t* rec = recs + q * stride;
     if (lane == 0) {
       RecHeader h;
       int32_t* hw = reinterpret_cast<int32_t*>(&h);
@@ -122,8 +126,8 @@ sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, 
     const EvalResult r =
         eval_one(P, cfg, s, 0, rec, kModeE2E, nullptr, nullptr, nullptr, nullptr, nullptr);
     if (lane == 0) {
-      if (res) res[p] = r;
-      const uint64_t k = k0 + static_cast<uint64_t>(p);
+      if (res) res[q] = r;
+      const uint64_t k = k0 + static_cast<uint64_t>(q);
       acc.xor_bits ^= static_cast<unsigned long long>(__double_as_longlong(r.cost));
       if (r.flags & kResFeasOut) {
         ++acc.n_feasible;
@@ -147,14 +151,14 @@ namespace {
 template <int kWarps>
 cudaError_t sweep_launch_impl(const DevProblem& P, const DevCostConfig& cfg, const uint8_t* d_recs,
                               int64_t stride, int64_t n, uint64_t k0, SweepLaunch& L,
-                              EvalResult* d_res, cudaStream_t st) {
+                              const uint32_t* d_order, EvalResult* d_res, cudaStream_t st) {
   auto kern = dev::sweep_kernel<kWarps>;
   const int dyn = L.cls_bytes + kWarps * L.slab_bytes;
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
   if (e != cudaSuccess) return e;
   kern<<<L.grid, 32 * kWarps, dyn, st>>>(P, cfg, d_recs, stride, n, k0, L.slab_bytes,
                                          L.cls_bytes > 0 ? 1 : 0, L.gslab, L.gslab_bytes, d_res,
-                                         L.part, L.n_global, L.sync);
+                                         L.part, L.n_global, L.sync, d_order);
   return cudaGetLastError();
 }
 
@@ -201,11 +205,13 @@ cudaError_t sweep_plan(int N, int T, int n_sm, int warps, int slab_req, SweepLau
 
 cudaError_t launch_sweep(const DevProblem& P, const DevCostConfig& cfg, const uint8_t* d_recs,
                          int64_t stride, int64_t n, uint64_t k0, SweepLaunch& L,
-                         EvalResult* d_res, cudaStream_t st) {
+                         const uint32_t* d_order, EvalResult* d_res, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  if (L.warps == 4) return sweep_launch_impl<4>(P, cfg, d_recs, stride, n, k0, L, d_res, st);
-  if (L.warps == 2) return sweep_launch_impl<2>(P, cfg, d_recs, stride, n, k0, L, d_res, st);
-  return sweep_launch_impl<8>(P, cfg, d_recs, stride, n, k0, L, d_res, st);
+  if (L.warps == 4)
+    return sweep_launch_impl<4>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
+  if (L.warps == 2)
+    return sweep_launch_impl<2>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
+  return sweep_launch_impl<8>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
 }
 
 }  // namespace hpg

@@ -148,6 +148,19 @@ class _SearchInfo(C.Structure):
                 ("host_ms", C.c_double), ("batch_ms", C.c_double)]
 
 
+class _ResolvedTask(C.Structure):
+    _fields_ = [("task_slot", C.c_int32), ("dp", C.c_int32), ("pp", C.c_int32), ("tp", C.c_int32),
+                ("stage_layers", C.POINTER(C.c_int32)), ("nm_replica", C.POINTER(C.c_int64)),
+                ("devices", C.POINTER(C.c_int32))]
+
+
+class _Improvement(C.Structure):
+    _fields_ = [("run", C.c_int64), ("local_idx", C.c_int64), ("cost", C.c_double)]
+
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
 class _SweepStats(C.Structure):
     _fields_ = [("best_cost", C.c_double), ("best_k", C.c_uint64), ("n_feasible", C.c_uint64),
                 ("xor_bits", C.c_uint64), ("canonical_bytes", C.c_uint64),
@@ -165,6 +178,7 @@ EXPORTED_SYMBOLS = [
     "hpg_result_halvings", "hpg_result_survivor_sizes", "hpg_result_survivors",
     "hpg_result_plan", "hpg_result_breakdown", "hpg_result_free", "hpg_sweep",
     "hpg_sweep_resident", "hpg_sweep_dist", "hpg_exhaustive", "hpg_exhaustive_estimate",
+    "hpg_task_cost", "hpg_ring_bottleneck", "hpg_pair_cost", "hpg_dist_exchange",
 ]
 
 
@@ -221,6 +235,16 @@ def load_library(path: str = LIB_PATH):
                                          P(_SweepStats), E, L]),
         "hpg_sweep_dist": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
                                      P(C.c_uint8), P(_SweepStats), E, L]),
+        "hpg_task_cost": (C.c_int, [C.c_void_p, P(_ResolvedTask), P(_CostConfig), P(C.c_double),
+                                    P(C.c_double), P(C.c_double), P(C.c_double), E, L]),
+        "hpg_ring_bottleneck": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int32, C.c_double,
+                                          P(C.c_double), E, L]),
+        "hpg_pair_cost": (C.c_int, [C.c_void_p, P(C.c_int32), C.c_int32, P(C.c_int32), C.c_int32,
+                                    C.c_double, P(C.c_double), E, L]),
+        "hpg_dist_exchange": (C.c_int, [C.c_int, C.c_int, ALLGATHER_FN, C.c_void_p, C.c_int32,
+                                        P(C.c_int64), P(C.c_int32), P(C.c_int64), P(C.c_double),
+                                        P(_Improvement), C.c_int64, P(_Improvement), C.c_int64,
+                                        P(C.c_int64), E, L]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -735,6 +759,47 @@ class Engine:
             out["feasible"] = [bool(feas[i]) for i in range(count)]
         return out
 
+    # ---- cost-model primitives (cost_model.hpp:49-111) ----
+
+    def task_cost_detail(self, task_slot: int, dp: int, pp: int, tp: int,
+                         stage_layers: Sequence[int], nm_replica: Sequence[int],
+                         devices: Sequence[int], cfg: Optional["CostModelConfig"] = None,
+                         resident_weight_bytes: Optional[Sequence[float]] = None) -> dict:
+        """task_cost_detail of one resolved task: agg (TaskCost), stage pieces
+        [dp][pp] of (comp, tp, pp, hbm), bubble_replica."""
+        sl = _arr(C.c_int32, stage_layers)
+        nm = _arr(C.c_int64, nm_replica)
+        dv = _arr(C.c_int32, devices)
+        t = _ResolvedTask(task_slot, dp, pp, tp, sl, nm, dv)
+        agg = (C.c_double * 7)()
+        stage = (C.c_double * (4 * dp * pp))()
+        bub = (C.c_double * dp)()
+        res = _arr(C.c_double, resident_weight_bytes) if resident_weight_bytes is not None else None
+        cc = (cfg or CostModelConfig())._c()
+        err = C.create_string_buffer(1024)
+        _raise(self.lib.hpg_task_cost(self._h, C.byref(t), C.byref(cc), res, agg, stage, bub, err,
+                                      1024), err)
+        keys = ("comp", "tp", "pp", "dp", "bubble", "hbm", "total")
+        return {"agg": dict(zip(keys, list(agg))),
+                "stage": [[tuple(stage[4 * (i * pp + j): 4 * (i * pp + j) + 4]) for j in range(pp)]
+                          for i in range(dp)],
+                "bubble_replica": list(bub)}
+
+    def min_ring_bottleneck(self, devices: Sequence[int], volume_bytes: float) -> float:
+        out = C.c_double()
+        err = C.create_string_buffer(1024)
+        _raise(self.lib.hpg_ring_bottleneck(self._h, _arr(C.c_int32, devices), len(devices),
+                                            volume_bytes, C.byref(out), err, 1024), err)
+        return out.value
+
+    def min_pair_cost(self, src: Sequence[int], dst: Sequence[int], volume_bytes: float) -> float:
+        out = C.c_double()
+        err = C.create_string_buffer(1024)
+        _raise(self.lib.hpg_pair_cost(self._h, _arr(C.c_int32, src), len(src),
+                                      _arr(C.c_int32, dst), len(dst), volume_bytes, C.byref(out),
+                                      err, 1024), err)
+        return out.value
+
     def sweep_dist(self, seed: int, total: int, rank: int, world: int,
                    nccl_id: Optional[bytes] = None) -> dict:
         """hpg_sweep_dist: this rank's contiguous shard of [0, total), global argmin
@@ -828,3 +893,42 @@ class SearchResult:
                 reshard_s=rs.value, sync_s=sy.value, end_to_end_s=e2.value,
                 memory_feasible=bool(mf.value))
         lib.hpg_result_free(handle)
+
+
+def dist_exchange(rank: int, world: int, allgather, slices: Sequence[int],
+                  used: Sequence[int], best: Sequence[float], mine) -> dict:
+    """hpg_dist_exchange: the per-round record exchange of the sharded search
+    over a Python all-gather `allgather(send: bytes) -> bytes` (world * len in
+    rank order), e.g. torch.distributed over gloo. `mine` = [(run, local_idx,
+    cost)] of this rank's runs; used/best entries of other ranks' runs are
+    ignored. Returns owners, used, best and every run's improvements."""
+    lib = load_library()
+    n = len(slices)
+
+    def cb(_user, send, recv, nbytes):
+        try:
+            out = allgather(C.string_at(send, nbytes) if nbytes else b"")
+            if len(out) != nbytes * world:
+                return 1
+            if nbytes:
+                C.memmove(recv, out, len(out))
+            return 0
+        except Exception:  # surfaced as a non-zero status
+            return 1
+
+    fn = ALLGATHER_FN(cb)
+    sl = _arr(C.c_int64, slices)
+    own = (C.c_int32 * max(1, n))()
+    us = _arr(C.c_int64, used)
+    bs = _arr(C.c_double, best)
+    mi = (_Improvement * max(1, len(mine)))(*[_Improvement(*m) for m in mine])
+    cap = 1 << 16
+    al = (_Improvement * cap)()
+    n_all = C.c_int64()
+    err = C.create_string_buffer(1024)
+    rc = lib.hpg_dist_exchange(rank, world, fn, None, n, sl, own, us, bs, mi, len(mine), al, cap,
+                               C.byref(n_all), err, 1024)
+    _raise(rc, err)
+    return {"owner": list(own)[:n], "used": list(us)[:n], "best": list(bs)[:n],
+            "impr": [(al[i].run, al[i].local_idx, al[i].cost) for i in range(n_all.value)]}
+

@@ -33,7 +33,11 @@ def _worker(rank, world, port, q):
     k0, n = distutil.sweep_range(1001, rank, world)
     fake = {0: (5.0, 17, 3), 1: (5.0, 600, 4)}[rank]  # tie on cost -> lowest k wins
     merged = distutil.merge_argmin(*fake)
-    q.put((rank, got == bytes(range(128)), mx, sm, owned, (k0, n), merged))
+    # an empty shard (inf, k = 2^64 - 1 sentinel) and a plan index above 2^53
+    # keep their exact 64-bit values
+    big = {0: (7.0, (1 << 53) + 1, 2), 1: (float("inf"), (1 << 64) - 1, 0)}[rank]
+    merged2 = distutil.merge_argmin(*big)
+    q.put((rank, got == bytes(range(128)), mx, sm, owned, (k0, n), merged, merged2))
     dist.destroy_process_group()
 
 
@@ -54,6 +58,7 @@ def test_gloo_world2_plumbing():
     assert res[0][4] == [0, 2, 4, 6, 8]
     assert [r[5] for r in res] == [(0, 500), (500, 501)]   # covers [0, 1001) exactly once
     assert all(r[6] == (5.0, 17, 7) for r in res)
+    assert all(r[7] == (7.0, (1 << 53) + 1, 2) for r in res)
 
 
 @pytest.mark.gpu
@@ -110,3 +115,80 @@ def test_reference_acceptance_suite_on_engine():
     assert m and all(int(x) > 0 for x in m.groups()), r.stderr[-2000:]
     assert r.returncode == 0
 
+
+
+def _exchange_worker(rank, world, port, q):
+    """each rank owns the runs deal_runs gives it, fabricates their records and
+    improvements deterministically, and runs the engine's real C++ exchange
+    (hpg_dist_exchange) over a gloo all-gather"""
+    import random
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    from paper_2512_12476_b200 import hetplan
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def allgather(payload: bytes) -> bytes:
+        t = torch.tensor(list(payload), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t)
+        return b"".join(bytes(o.tolist()) for o in out)
+
+    try:
+        rng = random.Random(7)
+        n = 37
+        slices = [rng.choice([1, 1, 2, 5, 13, 40]) for _ in range(n)]
+        truth_used = [rng.randrange(0, s + 1) for s in slices]
+        truth_best = [rng.uniform(1.0, 9.0) for _ in range(n)]
+        truth_impr = {r: sorted({rng.randrange(1, 50) for _ in range(rng.randrange(0, 4))})
+                      for r in range(n)}
+        res0 = None
+        for rounds in range(2):  # the exchange is repeatable (same results twice)
+            # owners are computed by the engine; ask once with nothing owned
+            probe = hetplan.dist_exchange(rank, world, allgather, slices, [0] * n, [0.0] * n, [])
+            owner = probe["owner"]
+            used = [truth_used[r] if owner[r] == rank else -1 for r in range(n)]
+            best = [truth_best[r] if owner[r] == rank else -1.0 for r in range(n)]
+            mine = [(r, i, truth_best[r] + i) for r in range(n) if owner[r] == rank
+                    for i in truth_impr[r]]
+            res = hetplan.dist_exchange(rank, world, allgather, slices, used, best, mine)
+            assert res0 is None or res0 == res
+            res0 = res
+        q.put((rank, res0, slices, truth_used, truth_best, truth_impr))
+    except Exception as e:  # reported by the parent
+        q.put((rank, repr(e), None, None, None, None))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_engine_exchange():
+    """the sharded search's per-round exchange (dist_exchange.cpp, the code
+    hpg_search_dist runs over NCCL) driven over gloo by two processes: both
+    ranks end with every run's record and improvement list, and the owner
+    deal balances the round's budget"""
+    lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2512_12476_b200", "libhpg.so")
+    if not os.path.exists(lib):
+        pytest.skip("libhpg.so not built")
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=180) for _ in range(world)), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert isinstance(r[1], dict), r[1]
+    a, b = res[0][1], res[1][1]
+    assert a == b                                    # identical on every rank
+    _, _, slices, tu, tb, ti = res[0]
+    n = len(slices)
+    assert a["used"] == tu and a["best"] == tb       # every run's owner record
+    want = [(r, i, tb[r] + i) for r in range(n) for i in ti[r]]
+    assert a["impr"] == want                         # by run, owner order
+    load = [sum(s for s, o in zip(slices, a["owner"]) if o == k) for k in range(world)]
+    assert max(load) - min(load) <= max(slices)      # longest-slice-first deal
