@@ -30,6 +30,7 @@
 #include "json.hpp"
 
 #include "hpg.h"
+#include "rng.hpp"
 
 using json = nlohmann::json;
 
@@ -66,6 +67,64 @@ void write_file(const std::string& path, const std::string& what, const std::str
   out << text;
 }
 
+// ---- JSON schema codec ----
+//
+// Every record type of the CLI's files (workflow models, devices, region
+// links, knobs, layouts, cost rows) is described once as a list of fields.
+// A field is required (read with json::at, whose out_of_range error names the
+// first missing key in list order, so lists follow the order the reference's
+// parser reads keys) or optional (json::value with the record's current value
+// as default). Writing needs no ordering: nlohmann::json objects keep their
+// keys sorted, so the dump(2) bytes depend only on the key/value set.
+
+template <class R>
+struct Field {
+  const char* key;
+  std::function<void(R&, const json&)> read;
+  std::function<void(const R&, json&)> write;
+};
+
+template <class R, class M>
+Field<R> required(const char* key, M R::*m) {
+  return {key, [key, m](R& r, const json& j) { r.*m = j.at(key).template get<M>(); },
+          [key, m](const R& r, json& j) { j[key] = r.*m; }};
+}
+
+template <class R, class M>
+Field<R> optional_field(const char* key, M R::*m) {
+  return {key, [key, m](R& r, const json& j) { r.*m = j.value(key, r.*m); },
+          [key, m](const R& r, json& j) { j[key] = r.*m; }};
+}
+
+template <class R>
+void read_record(R& r, const json& j, const std::vector<Field<R>>& fields) {
+  for (const Field<R>& f : fields) f.read(r, j);
+}
+
+template <class R>
+json write_record(const R& r, const std::vector<Field<R>>& fields) {
+  json j = json::object();
+  for (const Field<R>& f : fields) f.write(r, j);
+  return j;
+}
+
+// parse `text` as `what` JSON and run `body` on it, mapping nlohmann's
+// parse / schema exceptions onto the reference's InputError messages
+template <class T, class Body>
+T decode(const std::string& text, const char* what, Body&& body) {
+  json j;
+  try {
+    j = json::parse(text);
+  } catch (const json::exception& e) {
+    throw InputError(std::string(what) + " JSON parse error: " + e.what());
+  }
+  try {
+    return body(j);
+  } catch (const json::exception& e) {
+    throw InputError(std::string(what) + " JSON schema error: " + e.what());
+  }
+}
+
 // ---- workflow (workflow.cpp:16-33, 97-146, 161-232) ----
 
 struct Workflow {
@@ -76,115 +135,101 @@ struct Workflow {
   std::vector<hpg_task> tasks;  // id order
   std::vector<std::string> model_names;
   std::set<std::pair<int, int>> edges;
-  bool has_task(int id) const {
-    for (const hpg_task& t : tasks)
-      if (t.id == id) return true;
-    return false;
-  }
+  bool has_task(int id) const { return slot_of(id) >= 0; }
   int slot_of(int id) const {
-    for (size_t s = 0; s < tasks.size(); ++s)
-      if (tasks[s].id == id) return static_cast<int>(s);
-    return -1;
+    const auto it = std::find_if(tasks.begin(), tasks.end(),
+                                 [id](const hpg_task& t) { return t.id == id; });
+    return it == tasks.end() ? -1 : static_cast<int>(it - tasks.begin());
   }
 };
 
 struct Model {
-  int64_t h1 = 0, h2 = 0, nl = 0;
-  bool emb = false;
-  int64_t vocab = 0;
+  int64_t hidden_size = 0, intermediate_size = 0, num_layers = 0;
+  bool include_embedding = false;
+  int64_t vocab_size = 0;
 };
 
-Workflow parse_workflow(const std::string& text) {
-  json j;
-  try {
-    j = json::parse(text);
-  } catch (const json::exception& e) {
-    throw InputError(std::string("workflow JSON parse error: ") + e.what());
+const std::vector<Field<Workflow>>& batch_fields() {
+  static const std::vector<Field<Workflow>> f = {
+      required("global_batch", &Workflow::global_batch),
+      required("responses_per_prompt", &Workflow::rpp), required("seq_in", &Workflow::seq_in),
+      required("seq_out", &Workflow::seq_out), required("micro_batch_size", &Workflow::mbs)};
+  return f;
+}
+
+const std::vector<Field<Model>>& model_fields() {
+  static const std::vector<Field<Model>> f = {
+      required("hidden_size", &Model::hidden_size),
+      required("intermediate_size", &Model::intermediate_size),
+      required("num_layers", &Model::num_layers),
+      optional_field("include_embedding", &Model::include_embedding),
+      optional_field("vocab_size", &Model::vocab_size)};
+  return f;
+}
+
+// the value of `name` among `choices` (its index), or InputError
+int choose(const std::string& name, std::initializer_list<const char*> choices, const char* what) {
+  int i = 0;
+  for (const char* c : choices) {
+    if (name == c) return i;
+    ++i;
   }
-  try {
+  throw InputError(std::string("unknown ") + what + " '" + name + "'");
+}
+
+// PPO runs tasks 1..6, GRPO drops the critic (tasks 4, 5); each task's
+// model role and kind (generation 0, inference 1, training 2)
+struct TaskRole {
+  int id;
+  const char* model;
+  int kind;
+};
+constexpr TaskRole kRoles[] = {{1, "actor", 0},  {2, "reward", 1}, {3, "reference", 1},
+                               {4, "critic", 1}, {5, "critic", 2}, {6, "actor", 2}};
+
+Workflow parse_workflow(const std::string& text) {
+  return decode<Workflow>(text, "workflow", [](const json& j) {
     Workflow wf;
-    const std::string algo = j.at("algorithm").get<std::string>();
-    if (algo == "ppo") {
-      wf.algorithm = 0;
-    } else if (algo == "grpo") {
-      wf.algorithm = 1;
-    } else {
-      throw InputError("unknown algorithm '" + algo + "'");
-    }
-    const std::string mode = j.at("mode").get<std::string>();
-    if (mode == "sync") {
-      wf.mode = 0;
-    } else if (mode == "async") {
-      wf.mode = 1;
-    } else {
-      throw InputError("unknown mode '" + mode + "'");
-    }
+    wf.algorithm = choose(j.at("algorithm").get<std::string>(), {"ppo", "grpo"}, "algorithm");
+    wf.mode = choose(j.at("mode").get<std::string>(), {"sync", "async"}, "mode");
     wf.eta = j.value("eta", 0.5);
-    const json& jb = j.at("batch");
-    wf.global_batch = jb.at("global_batch").get<int64_t>();
-    wf.rpp = jb.at("responses_per_prompt").get<int64_t>();
-    wf.seq_in = jb.at("seq_in").get<int64_t>();
-    wf.seq_out = jb.at("seq_out").get<int64_t>();
-    wf.mbs = jb.at("micro_batch_size").get<int64_t>();
+    read_record(wf, j.at("batch"), batch_fields());
     std::map<std::string, Model> models;
-    for (const auto& [name, jm] : j.at("models").items()) {
-      Model m;
-      m.h1 = jm.at("hidden_size").get<int64_t>();
-      m.h2 = jm.at("intermediate_size").get<int64_t>();
-      m.nl = jm.at("num_layers").get<int64_t>();
-      if (jm.contains("include_embedding")) m.emb = jm.at("include_embedding").get<bool>();
-      if (jm.contains("vocab_size")) m.vocab = jm.at("vocab_size").get<int64_t>();
-      models[name] = m;
-    }
-    // build_workflow
-    if (wf.eta < 0.0 || wf.eta > 1.0) throw InputError("eta must be within [0, 1]");
-    if (wf.global_batch < 1 || wf.rpp < 1 || wf.mbs < 1)
-      throw InputError("batch sizes must be >= 1");
-    if (wf.seq_in < 1 || wf.seq_out < 0)
-      throw InputError("seq_in must be >= 1 and seq_out >= 0");
-    const std::vector<int> ids =
-        wf.algorithm == 0 ? std::vector<int>{1, 2, 3, 4, 5, 6} : std::vector<int>{1, 2, 3, 6};
-    static const char* names[7] = {"", "actor", "reward", "reference", "critic", "critic", "actor"};
-    for (int id : ids) {
-      const std::string name = names[id];
-      auto it = models.find(name);
+    for (const auto& [name, jm] : j.at("models").items()) read_record(models[name], jm, model_fields());
+    // build_workflow's checks
+    if (!(wf.eta >= 0.0 && wf.eta <= 1.0)) throw InputError("eta must be within [0, 1]");
+    if (std::min({wf.global_batch, wf.rpp, wf.mbs}) < 1) throw InputError("batch sizes must be >= 1");
+    if (wf.seq_in < 1 || wf.seq_out < 0) throw InputError("seq_in must be >= 1 and seq_out >= 0");
+    for (const TaskRole& role : kRoles) {
+      if (wf.algorithm == 1 && (role.id == 4 || role.id == 5)) continue;
+      const auto it = models.find(role.model);
       if (it == models.end())
-        throw InputError("missing model spec '" + name + "' required by task " +
-                         std::to_string(id));
+        throw InputError(std::string("missing model spec '") + role.model +
+                         "' required by task " + std::to_string(role.id));
       const Model& m = it->second;
-      if (m.h1 < 1 || m.h2 < 1 || m.nl < 1)
-        throw InputError(
-            "model spec requires hidden_size, intermediate_size and num_layers >= 1");
-      if (m.emb && m.vocab < 1) throw InputError("include_embedding requires vocab_size >= 1");
-      hpg_task t{};
-      t.id = id;
-      t.kind = id == 1 ? 0 : (id <= 4 ? 1 : 2);
-      t.hidden_size = m.h1;
-      t.intermediate_size = m.h2;
-      t.num_layers = m.nl;
-      t.include_embedding = m.emb ? 1 : 0;
-      t.vocab_size = m.vocab;
-      t.precision_bytes = 2;
-      wf.tasks.push_back(t);
-      wf.model_names.push_back(name);
+      if (std::min({m.hidden_size, m.intermediate_size, m.num_layers}) < 1)
+        throw InputError("model spec requires hidden_size, intermediate_size and num_layers >= 1");
+      if (m.include_embedding && m.vocab_size < 1)
+        throw InputError("include_embedding requires vocab_size >= 1");
+      wf.tasks.push_back(hpg_task{role.id, role.kind, m.hidden_size, m.intermediate_size,
+                                  m.num_layers, m.include_embedding ? 1 : 0, m.vocab_size, 2});
+      wf.model_names.emplace_back(role.model);
     }
-    std::vector<int> inf, trn;
-    for (const hpg_task& t : wf.tasks) {
-      if (t.kind == 1) inf.push_back(t.id);
-      if (t.kind == 2) trn.push_back(t.id);
+    // dependencies: generation feeds every inference task, which feeds every
+    // training task
+    for (const hpg_task& a : wf.tasks) {
+      if (a.kind != 1) continue;
+      wf.edges.emplace(1, a.id);
+      for (const hpg_task& b : wf.tasks)
+        if (b.kind == 2) wf.edges.emplace(a.id, b.id);
     }
-    for (int i : inf) wf.edges.emplace(1, i);
-    for (int i : inf)
-      for (int tr : trn) wf.edges.emplace(i, tr);
     if (j.contains("precision_bytes")) {
       for (const auto& [name, jp] : j.at("precision_bytes").items())
         for (size_t s = 0; s < wf.tasks.size(); ++s)
           if (wf.model_names[s] == name) wf.tasks[s].precision_bytes = jp.get<int>();
     }
     return wf;
-  } catch (const json::exception& e) {
-    throw InputError(std::string("workflow JSON schema error: ") + e.what());
-  }
+  });
 }
 
 // ---- topology (topology.cpp:132-211) ----
@@ -209,73 +254,63 @@ struct Topology {
   }
 };
 
+const std::vector<Field<Device>>& device_fields() {
+  static const std::vector<Field<Device>> f = {
+      required("id", &Device::id),
+      required("gpu_model", &Device::gpu_model),
+      required("comp_tflops", &Device::comp_tflops),
+      required("mem_gb", &Device::mem_gb),
+      required("hbm_gbps", &Device::hbm_gbps),
+      required("intra_node_gbps", &Device::intra_node_gbps),
+      required("node", &Device::node),
+      required("region", &Device::region)};
+  return f;
+}
+
+const std::vector<Field<RegionLink>>& link_fields() {
+  static const std::vector<Field<RegionLink>> f = {
+      required("src", &RegionLink::src), required("dst", &RegionLink::dst),
+      required("latency_ms", &RegionLink::latency_ms),
+      required("bandwidth_gbps", &RegionLink::bandwidth_gbps)};
+  return f;
+}
+
+const std::vector<Field<Topology>>& topology_default_fields() {
+  static const std::vector<Field<Topology>> f = {
+      optional_field("intra_region_latency_ms", &Topology::intra_region_latency_ms),
+      optional_field("intra_region_bandwidth_gbps", &Topology::intra_region_bandwidth_gbps)};
+  return f;
+}
+
+template <class R>
+std::vector<R> read_list(const json& arr, const std::vector<Field<R>>& fields) {
+  std::vector<R> out;
+  for (const json& item : arr) read_record(out.emplace_back(), item, fields);
+  return out;
+}
+
+template <class R>
+json write_list(const std::vector<R>& items, const std::vector<Field<R>>& fields) {
+  json arr = json::array();
+  for (const R& r : items) arr.push_back(write_record(r, fields));
+  return arr;
+}
+
 Topology parse_topology(const std::string& text) {
-  json j;
-  try {
-    j = json::parse(text);
-  } catch (const json::exception& e) {
-    throw InputError(std::string("topology JSON parse error: ") + e.what());
-  }
-  try {
+  return decode<Topology>(text, "topology", [](const json& j) {
     Topology t;
-    for (const json& jd : j.at("devices")) {
-      Device d;
-      d.id = jd.at("id").get<std::string>();
-      d.gpu_model = jd.at("gpu_model").get<std::string>();
-      d.comp_tflops = jd.at("comp_tflops").get<double>();
-      d.mem_gb = jd.at("mem_gb").get<double>();
-      d.hbm_gbps = jd.at("hbm_gbps").get<double>();
-      d.intra_node_gbps = jd.at("intra_node_gbps").get<double>();
-      d.node = jd.at("node").get<std::string>();
-      d.region = jd.at("region").get<std::string>();
-      t.devices.push_back(std::move(d));
-    }
-    if (j.contains("region_links")) {
-      for (const json& jl : j.at("region_links")) {
-        RegionLink rl;
-        rl.src = jl.at("src").get<std::string>();
-        rl.dst = jl.at("dst").get<std::string>();
-        rl.latency_ms = jl.at("latency_ms").get<double>();
-        rl.bandwidth_gbps = jl.at("bandwidth_gbps").get<double>();
-        t.links.push_back(std::move(rl));
-      }
-    }
-    if (j.contains("defaults")) {
-      const json& jd = j.at("defaults");
-      t.intra_region_latency_ms = jd.value("intra_region_latency_ms", t.intra_region_latency_ms);
-      t.intra_region_bandwidth_gbps =
-          jd.value("intra_region_bandwidth_gbps", t.intra_region_bandwidth_gbps);
-    }
+    t.devices = read_list(j.at("devices"), device_fields());
+    if (j.contains("region_links")) t.links = read_list(j.at("region_links"), link_fields());
+    if (j.contains("defaults")) read_record(t, j.at("defaults"), topology_default_fields());
     return t;
-  } catch (const json::exception& e) {
-    throw InputError(std::string("topology JSON schema error: ") + e.what());
-  }
+  });
 }
 
 std::string serialize_topology(const Topology& topo) {
-  json jdevs = json::array();
-  for (const Device& d : topo.devices) {
-    jdevs.push_back({{"id", d.id},
-                     {"gpu_model", d.gpu_model},
-                     {"comp_tflops", d.comp_tflops},
-                     {"mem_gb", d.mem_gb},
-                     {"hbm_gbps", d.hbm_gbps},
-                     {"intra_node_gbps", d.intra_node_gbps},
-                     {"node", d.node},
-                     {"region", d.region}});
-  }
-  json jlinks = json::array();
-  for (const RegionLink& rl : topo.links) {
-    jlinks.push_back({{"src", rl.src},
-                      {"dst", rl.dst},
-                      {"latency_ms", rl.latency_ms},
-                      {"bandwidth_gbps", rl.bandwidth_gbps}});
-  }
-  json j = {{"devices", jdevs},
-            {"region_links", jlinks},
-            {"defaults",
-             {{"intra_region_latency_ms", topo.intra_region_latency_ms},
-              {"intra_region_bandwidth_gbps", topo.intra_region_bandwidth_gbps}}}};
+  json j = json::object();
+  j["devices"] = write_list(topo.devices, device_fields());
+  j["region_links"] = write_list(topo.links, link_fields());
+  j["defaults"] = write_record(topo, topology_default_fields());
   return j.dump(2) + "\n";
 }
 
@@ -326,38 +361,37 @@ struct Knobs {
   }
 };
 
+const std::vector<Field<Knobs>>& knob_fields() {
+  static const std::vector<Field<Knobs>> f = {
+      optional_field("budget", &Knobs::budget),
+      optional_field("seed", &Knobs::seed),
+      optional_field("population", &Knobs::population),
+      optional_field("locality_bias", &Knobs::locality_bias),
+      optional_field("quantize_gpu_counts", &Knobs::quantize_gpu_counts),
+      optional_field("level1_filter", &Knobs::level1_filter),
+      optional_field("level1_cap", &Knobs::level1_cap),
+      optional_field("gg_arm_cap", &Knobs::gg_arm_cap),
+      optional_field("swap_pair_sample", &Knobs::swap_pair_sample),
+      optional_field("balance_data", &Knobs::balance_data),
+      optional_field("balance_layers", &Knobs::balance_layers),
+      optional_field("balance_seqlen", &Knobs::balance_seqlen),
+      optional_field("recompute", &Knobs::recompute),
+      optional_field("reshard_override", &Knobs::reshard_override),
+      optional_field("sync_override", &Knobs::sync_override),
+      optional_field("exhaustive_cap", &Knobs::exhaustive_cap)};
+  return f;
+}
+
 Knobs parse_knobs(const std::string& text) {
-  json j;
-  try {
-    j = json::parse(text);
-  } catch (const json::exception& e) {
-    throw InputError(std::string("knobs JSON parse error: ") + e.what());
-  }
-  Knobs k;
-  try {
-    k.budget = j.value("budget", k.budget);
-    k.seed = j.value("seed", k.seed);
-    k.seed_set = j.contains("seed");
-    k.population = j.value("population", k.population);
-    k.locality_bias = j.value("locality_bias", k.locality_bias);
-    k.quantize_gpu_counts = j.value("quantize_gpu_counts", k.quantize_gpu_counts);
-    k.level1_filter = j.value("level1_filter", k.level1_filter);
-    k.level1_cap = j.value("level1_cap", k.level1_cap);
-    k.gg_arm_cap = j.value("gg_arm_cap", k.gg_arm_cap);
-    k.swap_pair_sample = j.value("swap_pair_sample", k.swap_pair_sample);
-    k.balance_data = j.value("balance_data", k.balance_data);
-    k.balance_layers = j.value("balance_layers", k.balance_layers);
-    k.balance_seqlen = j.value("balance_seqlen", k.balance_seqlen);
-    k.recompute = j.value("recompute", k.recompute);
-    k.reshard_override = j.value("reshard_override", k.reshard_override);
-    k.sync_override = j.value("sync_override", k.sync_override);
-    k.exhaustive_cap = j.value("exhaustive_cap", k.exhaustive_cap);
-  } catch (const json::exception& e) {
-    throw InputError(std::string("knobs JSON schema error: ") + e.what());
-  }
+  Knobs k = decode<Knobs>(text, "knobs", [](const json& j) {
+    Knobs r;
+    read_record(r, j, knob_fields());
+    r.seed_set = j.contains("seed");
+    return r;
+  });
   if (k.population < 1 || k.swap_pair_sample < 0 || k.gg_arm_cap < 1)
     throw InputError("knobs: population and gg_arm_cap must be >= 1");
-  if (k.locality_bias < 0 || k.locality_bias > 1)
+  if (!(k.locality_bias >= 0 && k.locality_bias <= 1))
     throw InputError("knobs: locality_bias must be within [0, 1]");
   if (k.level1_filter != "off" && k.level1_filter != "adjacent")
     throw InputError("knobs: level1_filter must be \"off\" or \"adjacent\"");
@@ -395,100 +429,103 @@ struct Plan {
   double estimated_cost_s = -1.0;
 };
 
+const std::vector<Field<Layout>>& layout_fields() {
+  static const std::vector<Field<Layout>> f = {
+      required("dp", &Layout::dp), required("pp", &Layout::pp), required("tp", &Layout::tp),
+      required("stage_layers", &Layout::stage_layers),
+      // unit weights when absent (make_layout, plan.cpp:89-100)
+      {"replica_batch_weights",
+       [](Layout& l, const json& j) {
+         if (j.contains("replica_batch_weights"))
+           l.weights = j.at("replica_batch_weights").get<std::vector<double>>();
+         else
+           l.weights.assign(l.dp, 1.0);
+       },
+       [](const Layout& l, json& j) { j["replica_batch_weights"] = l.weights; }}};
+  return f;
+}
+
+const std::vector<Field<TaskCost>>& task_cost_fields() {
+  static const std::vector<Field<TaskCost>> f = {
+      required("comp", &TaskCost::comp), required("tp", &TaskCost::tp),
+      required("pp", &TaskCost::pp), required("dp", &TaskCost::dp),
+      required("bubble", &TaskCost::bubble), required("hbm", &TaskCost::hbm),
+      required("total", &TaskCost::total)};
+  return f;
+}
+
+const std::vector<Field<Breakdown>>& breakdown_fields() {
+  static const std::vector<Field<Breakdown>> f = {
+      required("reshard_s", &Breakdown::reshard_s), required("sync_s", &Breakdown::sync_s),
+      required("end_to_end_s", &Breakdown::end_to_end_s),
+      required("memory_feasible", &Breakdown::memory_feasible)};
+  return f;
+}
+
+// "task,replica,stage,shard" keys of the plan file's assignment map
+std::string tasklet_key(int task, int i, int j, int k) {
+  return std::to_string(task) + "," + std::to_string(i) + "," + std::to_string(j) + "," +
+         std::to_string(k);
+}
+
+// visits a layout's tasklets in flat (replica, stage, shard) order
+template <class F>
+void for_tasklets(int task, const Layout& l, F&& f) {
+  for (int i = 0; i < l.dp; ++i)
+    for (int j = 0; j < l.pp; ++j)
+      for (int k = 0; k < l.tp; ++k) f(tasklet_key(task, i, j, k), l.flat(i, j, k));
+}
+
 Plan parse_plan(const std::string& text) {
-  json j;
-  try {
-    j = json::parse(text);
-  } catch (const json::exception& e) {
-    throw InputError(std::string("plan JSON parse error: ") + e.what());
-  }
-  try {
+  return decode<Plan>(text, "plan", [](const json& j) {
     Plan p;
     p.groups = j.at("task_groups").get<std::vector<std::vector<int>>>();
     p.counts = j.at("gpu_counts").get<std::vector<int>>();
-    for (const auto& [key, jl] : j.at("layouts").items()) {
-      Layout l;
-      l.dp = jl.at("dp").get<int>();
-      l.pp = jl.at("pp").get<int>();
-      l.tp = jl.at("tp").get<int>();
-      l.stage_layers = jl.at("stage_layers").get<std::vector<int>>();
-      if (jl.contains("replica_batch_weights")) {
-        l.weights = jl.at("replica_batch_weights").get<std::vector<double>>();
-      } else {
-        l.weights.assign(l.dp, 1.0);
-      }
-      p.layouts[std::stoi(key)] = l;
-    }
+    for (const auto& [key, jl] : j.at("layouts").items())
+      read_record(p.layouts[std::stoi(key)], jl, layout_fields());
     const json& ja = j.at("assignment");
-    for (const auto& [id, l] : p.layouts) {
+    for (const auto& [task, l] : p.layouts) {
       std::vector<std::string> devs(l.size());
-      for (int i = 0; i < l.dp; ++i)
-        for (int j2 = 0; j2 < l.pp; ++j2)
-          for (int k = 0; k < l.tp; ++k) {
-            std::ostringstream key;
-            key << id << ',' << i << ',' << j2 << ',' << k;
-            if (!ja.contains(key.str()))
-              throw InputError("plan assignment missing tasklet " + key.str());
-            devs[l.flat(i, j2, k)] = ja.at(key.str()).get<std::string>();
-          }
-      p.assignment[id] = std::move(devs);
+      for_tasklets(task, l, [&](const std::string& key, int at) {
+        if (!ja.contains(key)) throw InputError("plan assignment missing tasklet " + key);
+        devs[at] = ja.at(key).get<std::string>();
+      });
+      p.assignment[task] = std::move(devs);
     }
     if (j.contains("provenance")) {
-      p.prov_seed = j.at("provenance").at("seed").get<uint64_t>();
-      p.prov_budget = j.at("provenance").at("budget").get<int64_t>();
+      const json& jp = j.at("provenance");
+      p.prov_seed = jp.at("seed").get<uint64_t>();
+      p.prov_budget = jp.at("budget").get<int64_t>();
     }
     p.estimated_cost_s = j.value("estimated_cost_s", -1.0);
     return p;
-  } catch (const json::exception& e) {
-    throw InputError(std::string("plan JSON schema error: ") + e.what());
-  }
-}
-
-json layout_json(const Layout& l) {
-  return {{"dp", l.dp},
-          {"pp", l.pp},
-          {"tp", l.tp},
-          {"stage_layers", l.stage_layers},
-          {"replica_batch_weights", l.weights}};
+  });
 }
 
 json breakdown_json(const Breakdown& bd) {
-  json per_task = json::object();
-  for (const auto& [id, tc] : bd.per_task) {
-    per_task[std::to_string(id)] = {{"comp", tc.comp}, {"tp", tc.tp},         {"pp", tc.pp},
-                                    {"dp", tc.dp},     {"bubble", tc.bubble}, {"hbm", tc.hbm},
-                                    {"total", tc.total}};
-  }
-  return {{"per_task", per_task},
-          {"reshard_s", bd.reshard_s},
-          {"sync_s", bd.sync_s},
-          {"end_to_end_s", bd.end_to_end_s},
-          {"memory_feasible", bd.memory_feasible}};
+  json j = write_record(bd, breakdown_fields());
+  json rows = json::object();
+  for (const auto& [task, tc] : bd.per_task) rows[std::to_string(task)] = write_record(tc, task_cost_fields());
+  j["per_task"] = rows;
+  return j;
 }
 
 std::string serialize_plan(const Plan& plan, const Breakdown* bd) {
-  json jlayouts = json::object();
-  for (const auto& [id, l] : plan.layouts) jlayouts[std::to_string(id)] = layout_json(l);
-  json jassign = json::object();
-  for (const auto& [id, devs] : plan.assignment) {
-    auto lit = plan.layouts.find(id);
-    if (lit == plan.layouts.end())
-      throw InputError("plan has assignment for task without layout");
-    const Layout& l = lit->second;
-    for (int i = 0; i < l.dp; ++i)
-      for (int j = 0; j < l.pp; ++j)
-        for (int k = 0; k < l.tp; ++k) {
-          std::ostringstream key;
-          key << id << ',' << i << ',' << j << ',' << k;
-          jassign[key.str()] = devs.at(l.flat(i, j, k));
-        }
+  json layouts = json::object(), assign = json::object();
+  for (const auto& [task, l] : plan.layouts) layouts[std::to_string(task)] = write_record(l, layout_fields());
+  for (const auto& [task, devs] : plan.assignment) {
+    const auto lit = plan.layouts.find(task);
+    if (lit == plan.layouts.end()) throw InputError("plan has assignment for task without layout");
+    for_tasklets(task, lit->second,
+                 [&](const std::string& key, int at) { assign[key] = devs.at(at); });
   }
-  json j = {{"task_groups", plan.groups},
-            {"gpu_counts", plan.counts},
-            {"layouts", jlayouts},
-            {"assignment", jassign},
-            {"provenance", {{"seed", plan.prov_seed}, {"budget", plan.prov_budget}}},
-            {"estimated_cost_s", plan.estimated_cost_s}};
+  json j = json::object();
+  j["task_groups"] = plan.groups;
+  j["gpu_counts"] = plan.counts;
+  j["layouts"] = layouts;
+  j["assignment"] = assign;
+  j["provenance"] = json{{"seed", plan.prov_seed}, {"budget", plan.prov_budget}};
+  j["estimated_cost_s"] = plan.estimated_cost_s;
   if (bd) j["cost_breakdown"] = breakdown_json(*bd);
   return j.dump(2) + "\n";
 }
@@ -740,24 +777,40 @@ class Engine {
 struct GpuSpec {
   double comp_tflops, mem_gb, hbm_gbps, intra_node_gbps;
 };
-const std::map<std::string, GpuSpec>& gpu_catalog() {
-  // topology.cpp:228-236, plus H100 as SURVEY.md App. A.4 defines it (fleet only)
-  static const std::map<std::string, GpuSpec> c = {{"A100", {312.0, 40.0, 2039.0, 600.0}},
-                                                    {"L40S", {366.0, 48.0, 864.0, 64.0}},
-                                                    {"L4", {121.0, 24.0, 300.0, 64.0}}};
-  return c;
-}
-const std::map<std::string, GpuSpec>& fleet_catalog() {
-  static const std::map<std::string, GpuSpec> c = {{"A100", {312.0, 40.0, 2039.0, 600.0}},
-                                                    {"L40S", {366.0, 48.0, 864.0, 64.0}},
-                                                    {"L4", {121.0, 24.0, 300.0, 64.0}},
-                                                    {"H100", {989.0, 80.0, 3350.0, 900.0}}};
-  return c;
+// GPU model catalogue: the reference scenarios know A100 / L40S / L4
+// (topology.cpp:228-236); the fleet generator adds H100
+struct CatalogEntry {
+  const char* model;
+  GpuSpec spec;
+  bool in_scenarios;
+};
+constexpr CatalogEntry kCatalog[] = {{"A100", {312.0, 40.0, 2039.0, 600.0}, true},
+                                     {"L40S", {366.0, 48.0, 864.0, 64.0}, true},
+                                     {"L4", {121.0, 24.0, 300.0, 64.0}, true},
+                                     {"H100", {989.0, 80.0, 3350.0, 900.0}, false}};
+
+const GpuSpec* lookup_gpu(const std::string& model, bool fleet) {
+  for (const CatalogEntry& e : kCatalog)
+    if (model == e.model && (fleet || e.in_scenarios)) return &e.spec;
+  return nullptr;
 }
 
-std::string lower(std::string s) {
-  std::transform(s.begin(), s.end(), s.begin(), [](unsigned char c) { return std::tolower(c); });
-  return s;
+Device make_device(std::string id, const std::string& model, const GpuSpec& g) {
+  Device d;
+  d.id = std::move(id);
+  d.gpu_model = model;
+  d.comp_tflops = g.comp_tflops;
+  d.mem_gb = g.mem_gb;
+  d.hbm_gbps = g.hbm_gbps;
+  d.intra_node_gbps = g.intra_node_gbps;
+  return d;
+}
+
+std::string lowercase(const std::string& s) {
+  std::string r;
+  r.reserve(s.size());
+  for (unsigned char c : s) r.push_back(static_cast<char>(std::tolower(c)));
+  return r;
 }
 
 struct InventoryItem {
@@ -765,77 +818,49 @@ struct InventoryItem {
   std::string gpu_model;
 };
 
+// "24xA100,16*L4": comma-separated COUNTxMODEL entries ('x' or '*'); an empty
+// entry between commas is an error, a trailing comma is not
 std::vector<InventoryItem> parse_inventory(const std::string& text) {
+  std::vector<std::string> parts;
+  size_t from = 0;
+  while (from < text.size()) {
+    const size_t comma = text.find(',', from);
+    const size_t to = comma == std::string::npos ? text.size() : comma;
+    parts.push_back(text.substr(from, to - from));
+    from = to + 1;
+  }
   std::vector<InventoryItem> items;
-  std::stringstream ss(text);
-  std::string part;
-  while (std::getline(ss, part, ',')) {
-    auto x = part.find('x');
-    if (x == std::string::npos) x = part.find('*');
-    if (x == std::string::npos || x == 0 || x + 1 >= part.size())
+  for (const std::string& part : parts) {
+    size_t sep = part.find('x');
+    if (sep == std::string::npos) sep = part.find('*');
+    if (sep == std::string::npos || sep == 0 || sep + 1 >= part.size())
       throw UsageError("bad inventory entry '" + part + "' (expected COUNTxMODEL, e.g. 24xA100)");
-    InventoryItem item;
+    int count = 0;
     try {
-      item.count = std::stoi(part.substr(0, x));
+      count = std::stoi(part.substr(0, sep));
     } catch (const std::exception&) {
       throw UsageError("bad inventory count in '" + part + "'");
     }
-    item.gpu_model = part.substr(x + 1);
-    items.push_back(std::move(item));
+    items.push_back(InventoryItem{count, part.substr(sep + 1)});
   }
   if (items.empty()) throw UsageError("empty inventory");
   return items;
 }
 
-// Rng (rng.hpp:10-65): splitmix64 seeding, xoshiro256**, uniform()
-struct Rng {
-  uint64_t s[4];
-  static uint64_t mix64(uint64_t x) {
-    x += 0x9e3779b97f4a7c15ULL;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-    return x ^ (x >> 31);
-  }
-  explicit Rng(uint64_t seed) {
-    uint64_t v = seed;
-    for (int i = 0; i < 4; ++i) v = s[i] = mix64(v);
-  }
-  static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
-  uint64_t next() {
-    const uint64_t r = rotl(s[1] * 5, 7) * 9;
-    const uint64_t t = s[1] << 17;
-    s[2] ^= s[0];
-    s[3] ^= s[1];
-    s[1] ^= s[2];
-    s[0] ^= s[3];
-    s[2] ^= t;
-    s[3] = rotl(s[3], 45);
-    return r;
-  }
-  double uniform(double lo, double hi) {
-    return lo + (hi - lo) * (static_cast<double>(next() >> 11) * 0x1.0p-53);
-  }
-};
-
+// inventory_devices (topology.cpp:240-265): "<model lowercase>-NN", numbered
+// per model in inventory order
 std::vector<Device> inventory_devices(const std::vector<InventoryItem>& inv) {
   std::vector<Device> devs;
-  std::map<std::string, int> per_model;
+  std::map<std::string, int> next_index;
   for (const InventoryItem& item : inv) {
-    auto it = gpu_catalog().find(item.gpu_model);
-    if (it == gpu_catalog().end())
-      throw InputError("unknown GPU model '" + item.gpu_model + "' (known: A100, L40S, L4)");
+    const GpuSpec* g = lookup_gpu(item.gpu_model, false);
+    if (!g) throw InputError("unknown GPU model '" + item.gpu_model + "' (known: A100, L40S, L4)");
     if (item.count < 1) throw InputError("inventory counts must be >= 1");
-    for (int k = 0; k < item.count; ++k) {
-      Device d;
-      char buf[16];
-      std::snprintf(buf, sizeof(buf), "%02d", per_model[item.gpu_model]++);
-      d.id = lower(item.gpu_model) + "-" + buf;
-      d.gpu_model = item.gpu_model;
-      d.comp_tflops = it->second.comp_tflops;
-      d.mem_gb = it->second.mem_gb;
-      d.hbm_gbps = it->second.hbm_gbps;
-      d.intra_node_gbps = it->second.intra_node_gbps;
-      devs.push_back(std::move(d));
+    int& k = next_index[item.gpu_model];
+    for (int c = 0; c < item.count; ++c, ++k) {
+      std::string num = std::to_string(k);
+      if (num.size() < 2) num.insert(0, 2 - num.size(), '0');
+      devs.push_back(make_device(lowercase(item.gpu_model) + "-" + num, item.gpu_model, *g));
     }
   }
   return devs;
@@ -848,60 +873,86 @@ struct ScenarioOptions {
   std::vector<std::string> edge_models{"L4"};
 };
 
+// one link per region pair a < b, latency then bandwidth drawn uniformly from
+// Rng(seed), in pair order
+void random_region_links(Topology& t, const std::vector<std::string>& regions, uint64_t seed,
+                         double lat_lo, double lat_hi, double bw_lo, double bw_hi) {
+  hpg::Rng rng(seed);
+  for (size_t a = 0; a < regions.size(); ++a)
+    for (size_t b = a + 1; b < regions.size(); ++b) {
+      RegionLink l;
+      l.src = regions[a];
+      l.dst = regions[b];
+      l.latency_ms = rng.uniform(lat_lo, lat_hi);
+      l.bandwidth_gbps = rng.uniform(bw_lo, bw_hi);
+      t.links.push_back(std::move(l));
+    }
+}
+
+// Scenario 1: one region, nodes of node_size GPUs of one model.
+void scenario_single_region(Topology& t, int node_size) {
+  std::map<std::string, int> seen;
+  for (Device& d : t.devices) {
+    const int k = seen[d.gpu_model]++;
+    d.region = "local";
+    d.node = lowercase(d.gpu_model) + "-node-" + std::to_string(k / std::max(1, node_size));
+  }
+}
+
+// Scenario 2: the first non-edge model in ohio, other non-edge models in
+// virginia, edge models in virginia-edge; fixed cross-region rules.
+void scenario_edge(Topology& t, const std::vector<std::string>& edge_models) {
+  std::string ohio_model;
+  std::set<std::string> regions;
+  for (Device& d : t.devices) {
+    const bool edge =
+        std::find(edge_models.begin(), edge_models.end(), d.gpu_model) != edge_models.end();
+    if (edge) {
+      d.region = "virginia-edge";
+    } else {
+      if (ohio_model.empty()) ohio_model = d.gpu_model;
+      d.region = d.gpu_model == ohio_model ? "ohio" : "virginia";
+    }
+    regions.insert(d.region);
+  }
+  struct Rule {
+    const char* a;
+    const char* b;
+    double ms, gbps;
+  };
+  const Rule rules[] = {{"ohio", "virginia", 10.0, 5.0},
+                        {"ohio", "virginia-edge", 10.0, 1.0},
+                        {"virginia", "virginia-edge", t.intra_region_latency_ms, 1.0}};
+  for (const Rule& r : rules)
+    if (regions.count(r.a) && regions.count(r.b)) t.links.push_back({r.a, r.b, r.ms, r.gbps});
+}
+
 // generate_scenario (topology.cpp:310-391)
 Topology generate_scenario(int id, const ScenarioOptions& o) {
   if (id < 1 || id > 4) throw UsageError("scenario id must be 1..4");
   Topology t;
   t.devices = inventory_devices(o.inventory);
   if (id == 1) {
-    std::map<std::string, int> per_model;
-    for (Device& d : t.devices) {
-      const int k = per_model[d.gpu_model]++;
-      d.region = "local";
-      d.node = lower(d.gpu_model) + "-node-" + std::to_string(k / std::max(1, o.node_size));
-    }
+    scenario_single_region(t, o.node_size);
     return t;
   }
   for (Device& d : t.devices) d.node = "host-" + d.id;
   if (id == 2) {
-    auto is_edge = [&](const Device& d) {
-      return std::find(o.edge_models.begin(), o.edge_models.end(), d.gpu_model) !=
-             o.edge_models.end();
-    };
-    std::set<std::string> used;
-    std::string ohio;
-    for (Device& d : t.devices) {
-      if (is_edge(d)) {
-        d.region = "virginia-edge";
-      } else {
-        if (ohio.empty()) ohio = d.gpu_model;
-        d.region = d.gpu_model == ohio ? "ohio" : "virginia";
-      }
-      used.insert(d.region);
-    }
-    auto add = [&](const std::string& a, const std::string& b, double ms, double gbps) {
-      if (used.count(a) && used.count(b)) t.links.push_back({a, b, ms, gbps});
-    };
-    add("ohio", "virginia", 10.0, 5.0);
-    add("ohio", "virginia-edge", 10.0, 1.0);
-    add("virginia", "virginia-edge", t.intra_region_latency_ms, 1.0);
+    scenario_edge(t, o.edge_models);
     return t;
   }
-  const std::vector<std::string> regions =
-      id == 3 ? std::vector<std::string>{"paris", "stockholm", "london", "ireland", "spain",
-                                         "zurich", "frankfurt", "milan"}
-              : std::vector<std::string>{"virginia", "ohio", "paris", "stockholm", "london",
-                                         "ireland", "spain", "zurich"};
+  // scenarios 3 (Europe, 5-30 ms, 1.9-5 Gbps) and 4 (US + Europe, 5-60 ms,
+  // 0.9-5 Gbps): devices dealt round-robin over eight regions
+  static const std::vector<std::string> europe = {"paris",   "stockholm", "london", "ireland",
+                                                  "spain",   "zurich",    "frankfurt", "milan"};
+  static const std::vector<std::string> transatlantic = {"virginia", "ohio",  "paris",  "stockholm",
+                                                         "london",   "ireland", "spain", "zurich"};
+  const std::vector<std::string>& regions = id == 3 ? europe : transatlantic;
   for (size_t i = 0; i < t.devices.size(); ++i) t.devices[i].region = regions[i % regions.size()];
-  const double d_lo = 5.0, d_hi = id == 3 ? 30.0 : 60.0;
-  const double b_lo = id == 3 ? 1.9 : 0.9, b_hi = 5.0;
-  Rng rng(o.seed);
-  for (size_t a = 0; a < regions.size(); ++a)
-    for (size_t b = a + 1; b < regions.size(); ++b) {
-      const double lat = rng.uniform(d_lo, d_hi);
-      const double bw = rng.uniform(b_lo, b_hi);
-      t.links.push_back({regions[a], regions[b], lat, bw});
-    }
+  if (id == 3)
+    random_region_links(t, regions, o.seed, 5.0, 30.0, 1.9, 5.0);
+  else
+    random_region_links(t, regions, o.seed, 5.0, 60.0, 0.9, 5.0);
   return t;
 }
 
@@ -929,7 +980,7 @@ Topology generate_fleet(const FleetOptions& o) {
   std::vector<int> left;
   int n = 0;
   for (const InventoryItem& it : o.inventory) {
-    if (!fleet_catalog().count(it.gpu_model))
+    if (!lookup_gpu(it.gpu_model, true))
       throw InputError("unknown GPU model '" + it.gpu_model + "' (known: A100, H100, L40S, L4)");
     if (it.count < 1) throw InputError("inventory counts must be >= 1");
     left.push_back(it.count);
@@ -945,28 +996,15 @@ Topology generate_fleet(const FleetOptions& o) {
       type = (type + 1) % left.size();
       in_block = 0;
     }
-    const InventoryItem& it = o.inventory[type];
-    const GpuSpec& g = fleet_catalog().at(it.gpu_model);
-    Device d;
-    d.id = it.gpu_model + "-" + std::to_string(i);
-    d.gpu_model = it.gpu_model;
-    d.comp_tflops = g.comp_tflops;
-    d.mem_gb = g.mem_gb;
-    d.hbm_gbps = g.hbm_gbps;
-    d.intra_node_gbps = g.intra_node_gbps;
+    const std::string& model = o.inventory[type].gpu_model;
+    Device d = make_device(model + "-" + std::to_string(i), model, *lookup_gpu(model, true));
     d.region = o.regions[(i / per_region) % R];
     d.node = d.region + "-n" + std::to_string(i / o.node_size);
     t.devices.push_back(std::move(d));
     --left[type];
     ++in_block;
   }
-  Rng rng(o.seed);
-  for (int a = 0; a < R; ++a)
-    for (int b = a + 1; b < R; ++b) {
-      const double lat = rng.uniform(o.lat_lo, o.lat_hi);
-      const double bw = rng.uniform(o.bw_lo, o.bw_hi);
-      t.links.push_back({o.regions[a], o.regions[b], lat, bw});
-    }
+  random_region_links(t, o.regions, o.seed, o.lat_lo, o.lat_hi, o.bw_lo, o.bw_hi);
   t.intra_region_latency_ms = 0.1;
   t.intra_region_bandwidth_gbps = 100.0;
   return t;
@@ -974,36 +1012,49 @@ Topology generate_fleet(const FleetOptions& o) {
 
 // ---- reports (cli.cpp:21-53) ----
 
+// the text breakdown: a task-id column of width 6 (left), seven 12-wide
+// right-aligned cost columns in fixed 4-decimal notation, then the totals.
+// The stream stays in 4-digit precision afterwards, as the reference's does.
 void print_breakdown_text(const Breakdown& bd, std::ostream& out) {
-  out << std::left << std::setw(6) << "task" << std::right << std::setw(12) << "comp"
-      << std::setw(12) << "tp" << std::setw(12) << "pp" << std::setw(12) << "dp" << std::setw(12)
-      << "bubble" << std::setw(12) << "hbm" << std::setw(12) << "total" << "\n";
-  for (const auto& [id, tc] : bd.per_task) {
-    out << std::left << std::setw(6) << id << std::right << std::fixed << std::setprecision(4)
-        << std::setw(12) << tc.comp << std::setw(12) << tc.tp << std::setw(12) << tc.pp
-        << std::setw(12) << tc.dp << std::setw(12) << tc.bubble << std::setw(12) << tc.hbm
-        << std::setw(12) << tc.total << "\n";
+  static const char* const kCols[] = {"comp", "tp", "pp", "dp", "bubble", "hbm", "total"};
+  out << std::left << std::setw(6) << "task" << std::right;
+  for (const char* c : kCols) out << std::setw(12) << c;
+  out << "\n";
+  for (const auto& [task, tc] : bd.per_task) {
+    const double row[] = {tc.comp, tc.tp, tc.pp, tc.dp, tc.bubble, tc.hbm, tc.total};
+    out << std::left << std::setw(6) << task << std::right << std::fixed << std::setprecision(4);
+    for (double v : row) out << std::setw(12) << v;
+    out << "\n";
   }
-  out << "reshard_s    " << bd.reshard_s << "\n";
-  out << "sync_s       " << bd.sync_s << "\n";
-  out << "end_to_end_s " << bd.end_to_end_s << "\n";
+  const std::pair<const char*, double> totals[] = {
+      {"reshard_s    ", bd.reshard_s}, {"sync_s       ", bd.sync_s}, {"end_to_end_s ", bd.end_to_end_s}};
+  for (const auto& [label, v] : totals) out << label << v << "\n";
   out << "memory_ok    " << (bd.memory_feasible ? "yes" : "no") << "\n";
   out.unsetf(std::ios::fixed);
 }
 
+// run_guarded (cli.cpp:55-68): errors become a one-line report and an exit code
 int run_guarded(std::ostream& err, const std::function<int()>& body) {
+  const char* kind = nullptr;
+  int code = kExitOk;
+  std::string what;
   try {
     return body();
   } catch (const UsageError& e) {
-    err << "usage error: " << e.what() << "\n";
-    return kExitUsage;
+    kind = "usage error: ";
+    code = kExitUsage;
+    what = e.what();
   } catch (const InputError& e) {
-    err << "input error: " << e.what() << "\n";
-    return kExitInput;
+    kind = "input error: ";
+    code = kExitInput;
+    what = e.what();
   } catch (const std::exception& e) {
-    err << "internal error: " << e.what() << "\n";
-    return kExitInternal;
+    kind = "internal error: ";
+    code = kExitInternal;
+    what = e.what();
   }
+  err << kind << what << "\n";
+  return code;
 }
 
 // ---- commands ----

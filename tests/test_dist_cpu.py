@@ -192,3 +192,27 @@ def test_gloo_world2_engine_exchange():
     assert a["impr"] == want                         # by run, owner order
     load = [sum(s for s, o in zip(slices, a["owner"]) if o == k) for k in range(world)]
     assert max(load) - min(load) <= max(slices)      # longest-slice-first deal
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_on_engine():
+    """the reference's own unit tests of the hot path (proj/tests/
+    test_cost_model.cpp, test_balance.cpp, test_plan.cpp, test_search.cpp,
+    unmodified, with a minimal doctest stand-in) linked so that
+    end_to_end_cost, task_cost_detail / task_cost, min_ring_bottleneck /
+    min_pair_cost, balance_data / balance_layers, nested_sha_search and
+    exhaustive_search run on the engine (built by `make -C oracle
+    unit_engine`): every test case passes, every redirected entry is used"""
+    import re
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "unit_engine")
+    if not os.path.exists(exe):
+        pytest.skip("unit_engine not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert re.search(r"test cases: (\d+) \| \1 passed \| 0 failed", r.stdout), r.stdout[-2000:]
+    m = re.search(r"end_to_end_cost (\d+), nested_sha_search (\d+), exhaustive_search (\d+), "
+                  r"balance_data (\d+), balance_layers (\d+), task_cost_detail (\d+), "
+                  r"task_cost (\d+), min_ring_bottleneck (\d+), min_pair_cost (\d+)", r.stderr)
+    assert m and all(int(x) > 0 for x in m.groups()), r.stderr[-2000:]
