@@ -5,6 +5,8 @@
 #include "search.hpp"
 #include "dist_exchange.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <chrono>
 #include <coroutine>
@@ -1585,6 +1587,10 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
     int max_rounds = 0;
     for (auto& p : ps) max_rounds = std::max(max_rounds, p.rounds);
     for (int n = 0; n < max_rounds; ++n) {
+      // one NVTX range per SHA round (outer m, inner n): nsys / ncu --nvtx
+      char range_name[48];
+      std::snprintf(range_name, sizeof(range_name), "hpg SHA round m=%d n=%d", m, n);
+      nvtxRangePushA(range_name);
       std::vector<ArmRun*> batch;
       for (auto& p : ps) {
         p.runs.emplace_back();
@@ -1666,6 +1672,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
           owners[s]->surv_sets.push_back(keep[s]);
         }
       }
+      nvtxRangePop();
     }
     {
       std::vector<Segment> segs;
