@@ -242,6 +242,8 @@ struct Ctx {
   double eval_ms = 0.0;
   double host_ms = 0.0;   // GA coroutine time (candidate generation, bookkeeping)
   double batch_ms = 0.0;  // run_batch wall time (pack, copies, kernel, sync)
+  double best_half_ms = 0.0;  // diagnostics: best_half_batch wall time
+  int64_t best_half_calls = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // kernel timing, buffer set 0
   cudaEvent_t ev2 = nullptr, ev3 = nullptr;  // kernel timing, buffer set 1
   cudaEvent_t ev_done[2] = {nullptr, nullptr};  // wave results landed, per set

@@ -1379,6 +1379,7 @@ void best_half_batch(Ctx& ctx, std::vector<Segment>& segs, int level,
   }
   const int nk = static_cast<int>(seg_of.size());
   if (nk == 0) return;
+  const double t_bh = now_s();
   const size_t n = sc.size();
   ctx.d_scores.reserve(n);
   ctx.d_arm_idx.reserve(n);
@@ -1398,6 +1399,8 @@ void best_half_batch(Ctx& ctx, std::vector<Segment>& segs, int level,
   cuda_check(cudaMemcpyAsync(keep.data(), ctx.d_keep.p, 4 * n, cudaMemcpyDeviceToHost, st), "D2H");
   cuda_check(cudaMemcpyAsync(ev.data(), ctx.d_events.p, 16 * nk, cudaMemcpyDeviceToHost, st), "D2H");
   cuda_check(cudaStreamSynchronize(st), "best_half");
+  ctx.best_half_ms += 1e3 * (now_s() - t_bh);
+  ++ctx.best_half_calls;
   for (int k = 0; k < nk; ++k) {
     const int s = seg_of[k];
     for (int i = off[k]; i < off[k + 1]; ++i)
@@ -1537,6 +1540,9 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
     arms.push_back(std::move(arm));
   }
 
+  const double t_setup = now_s();
+  const double bh0 = ctx.best_half_ms;
+  const int64_t bhc0 = ctx.best_half_calls;
   double incumbent = kInf;
   Cand inc_plan;
   int inc_owner = 0;
@@ -1736,6 +1742,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
     }
   }
   S.consumed = consumed;
+  const double t_rounds = now_s();
   if (consumed > K.budget) throw InternalError("search overspent its budget");
   if (inc_ti >= 0 && dist && dist->world > 1) {
     // the incumbent's plan lives on the rank that evaluated it
@@ -1783,6 +1790,18 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   S.eval_ms = ctx.eval_ms - ems0;
   S.host_ms = ctx.host_ms - hms0;
   S.batch_ms = ctx.batch_ms - bms0;
+  static const char* phase_log = std::getenv("HPG_GA_LOG");  // diagnostics only
+  if (phase_log) {
+    if (FILE* f = std::fopen(phase_log, "a")) {
+      std::fprintf(f,
+                   "search: setup %.3f ms, rounds %.3f ms (best_half %.3f ms in %lld calls, "
+                   "device GA %.3f ms), final %.3f ms, total %.3f ms\n",
+                   1e3 * (t_setup - t0), 1e3 * (t_rounds - t_setup), ctx.best_half_ms - bh0,
+                   static_cast<long long>(ctx.best_half_calls - bhc0), S.eval_ms,
+                   1e3 * (now_s() - t_rounds), 1e3 * S.wall_s);
+      std::fclose(f);
+    }
+  }
   return S;
 }
 
