@@ -786,7 +786,8 @@ __device__ __forceinline__ EvalResult eval_one(const DevProblem& P, const DevCos
 // kTeam = kMaxTeam: up to four warps per plan, uncapped (small waves)
 template <int kTeam>
 __global__ void __launch_bounds__(32 * kTeam, kTeam == 1 ? 16 : (kTeam == 2 ? 8 : 2))
-eval_kernel(DevProblem P, DevCostConfig cfg, Carve cv, int32_t kb_flags,
+eval_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCostConfig cfg,
+            const __grid_constant__ Carve cv, int32_t kb_flags,
             const uint8_t* __restrict__ recs, const int64_t* __restrict__ off,
             const int32_t* __restrict__ modes, int32_t uniform_mode, int n, int64_t stride,
             uint8_t* __restrict__ out_ws, const int64_t* __restrict__ out_off,

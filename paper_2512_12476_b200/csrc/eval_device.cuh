@@ -1348,7 +1348,9 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
     if (__popc(pending) >= 2) team_task_costs(P, cfg, s, pending);
   }
   double tot[kMaxTasks];
-  for (int t = 0; t < P.n_tasks; ++t) {
+#pragma unroll
+  for (int t = 0; t < kMaxTasks; ++t) {
+    if (t >= P.n_tasks) break;
     // sweep kernel: the CTA's plan-warps enter every task's cost together, so
     // they fetch the same code at the same time (instruction-cache sharing)
     if (s.cta_sync) bar_sync(5, s.cta_sync);
@@ -1394,17 +1396,27 @@ __device__ __noinline__ E2E end_to_end(const DevProblem& P, const DevCostConfig&
   } else {
     r.sync = transfer;
   }
-  // compose_end_to_end (cost_model.cpp:403-429): kinds staged, phi within a kind
-  double gens[kMaxTasks], infs[kMaxTasks], trains[kMaxTasks];
-  int ng = 0, ni = 0, ntr = 0;
-  for (int t = 0; t < P.n_tasks; ++t) {
-    if (P.task[t].kind == kGeneration) gens[ng++] = tot[t];
-    else if (P.task[t].kind == kInference) infs[ni++] = tot[t];
-    else trains[ntr++] = tot[t];
+  // compose_end_to_end (cost_model.cpp:403-429): kinds staged, phi within a
+  // kind. aggregate_phi's max and sequential sum are folded in task order as
+  // the tasks come (the same operations as over the per-kind lists), so no
+  // per-kind arrays live in local memory.
+  double k_mx[3] = {-kInf, -kInf, -kInf}, k_sum[3] = {0.0, 0.0, 0.0};
+  int k_n[3] = {0, 0, 0};
+#pragma unroll
+  for (int t = 0; t < kMaxTasks; ++t) {
+    if (t >= P.n_tasks) break;
+    const int kd = P.task[t].kind;  // kGeneration 0, kInference 1, kTraining 2
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (q != kd) continue;
+      k_mx[q] = smax(k_mx[q], tot[t]);
+      k_sum[q] += tot[t];
+      ++k_n[q];
+    }
   }
-  const double gen = ng == 0 ? 0.0 : phi(gens, ng, P.eta);
-  const double inf = ni == 0 ? 0.0 : phi(infs, ni, P.eta);
-  const double trn = ntr == 0 ? 0.0 : phi(trains, ntr, P.eta);
+  const double gen = k_n[0] == 0 ? 0.0 : k_mx[0] + (1.0 - P.eta) * (k_sum[0] - k_mx[0]);
+  const double inf = k_n[1] == 0 ? 0.0 : k_mx[1] + (1.0 - P.eta) * (k_sum[1] - k_mx[1]);
+  const double trn = k_n[2] == 0 ? 0.0 : k_mx[2] + (1.0 - P.eta) * (k_sum[2] - k_mx[2]);
   if (P.mode == 0) {
     r.e2e = gen + inf + trn + transfer;
   } else {

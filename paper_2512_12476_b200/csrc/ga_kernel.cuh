@@ -1395,7 +1395,8 @@ __device__ __noinline__ void ga_team_helper(const DevProblem& P, const DevCostCo
 // kTeam = 4: three helpers, registers uncapped (the last, narrowest rounds)
 template <int kTeam>
 __global__ void __launch_bounds__(32 * kTeam, kTeam == 4 ? 2 : 16 / kTeam)
-ga_kernel(DevProblem P, DevCostConfig cfg, Carve cv, double* __restrict__ gscratch,
+ga_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCostConfig cfg,
+          const __grid_constant__ Carve cv, double* __restrict__ gscratch,
           int64_t gscratch_doubles, const __grid_constant__ GaParams ga_in) {
   extern __shared__ __align__(16) uint8_t smem[];
   {

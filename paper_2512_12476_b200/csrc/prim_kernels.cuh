@@ -17,7 +17,8 @@ namespace dev {
 // out: agg[7] (comp, tp, pp, dp, bubble, hbm, total) | pieces [dp][pp][4]
 // (comp, tp, pp, hbm) | bubble [dp]
 __global__ void __launch_bounds__(32, 1)
-task_cost_kernel(DevProblem P, DevCostConfig cfg, int t, RecHeader h,
+task_cost_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCostConfig cfg,
+                 int t, const __grid_constant__ RecHeader h,
                  const int32_t* __restrict__ sl_in, const int64_t* __restrict__ nm_in,
                  const uint8_t* __restrict__ dev_in, const double* __restrict__ resident_in,
                  double* __restrict__ out) {
@@ -82,7 +83,7 @@ task_cost_kernel(DevProblem P, DevCostConfig cfg, int t, RecHeader h,
 
 // mode 0: min_ring_bottleneck over a[0..na); mode 1: min_pair_cost a x b
 __global__ void __launch_bounds__(32, 1)
-ring_kernel(DevProblem P, int mode, const uint8_t* __restrict__ a_in, int na,
+ring_kernel(const __grid_constant__ DevProblem P, int mode, const uint8_t* __restrict__ a_in, int na,
             const uint8_t* __restrict__ b_in, int nb, double volume, double* __restrict__ out) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ Ws ws[1];

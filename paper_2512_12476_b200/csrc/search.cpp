@@ -1541,6 +1541,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   }
 
   const double t_setup = now_s();
+  double t_env = 0, t_run = 0, t_inc = 0;  // diagnostics: round phases (s)
   const double bh0 = ctx.best_half_ms;
   const int64_t bhc0 = ctx.best_half_calls;
   double incumbent = kInf;
@@ -1597,6 +1598,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
       char range_name[48];
       std::snprintf(range_name, sizeof(range_name), "hpg SHA round m=%d n=%d", m, n);
       nvtxRangePushA(range_name);
+      const double t_round0 = now_s();
       std::vector<ArmRun*> batch;
       for (auto& p : ps) {
         p.runs.emplace_back();
@@ -1630,6 +1632,8 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
           }
         }
       }
+      const double t_env_done = now_s();
+      t_env += t_env_done - t_round0;
       if (dist && dist->world > 1) {
         // runs dealt over the ranks by budget (longest slice first to the
         // least-loaded rank, dist_exchange.cpp deal_runs), then all-gathered
@@ -1646,6 +1650,8 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
       } else {
         run_lockstep(ctx, K, batch, clock, waves);
       }
+      const double t_run_done = now_s();
+      t_run += t_run_done - t_env_done;
       // fold run results into the arm records
       for (auto& p : ps) {
         if (n >= p.rounds) continue;
@@ -1700,6 +1706,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
         }
       }
     }
+    const double t_inc0 = now_s();
     // sequential order: task groupings in survivor order, rounds, arms
     for (auto& p : ps) {
       for (size_t i = 0; i < p.events.size(); ++i) {
@@ -1723,6 +1730,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
         }
       }
     }
+    t_inc += now_s() - t_inc0;
     // level-1 halving over task groupings (tg score = min over all gg arms)
     std::vector<Segment> segs(1);
     segs[0].arms = surv;
@@ -1794,9 +1802,11 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   if (phase_log) {
     if (FILE* f = std::fopen(phase_log, "a")) {
       std::fprintf(f,
-                   "search: setup %.3f ms, rounds %.3f ms (best_half %.3f ms in %lld calls, "
-                   "device GA %.3f ms), final %.3f ms, total %.3f ms\n",
-                   1e3 * (t_setup - t0), 1e3 * (t_rounds - t_setup), ctx.best_half_ms - bh0,
+                   "search: setup %.3f ms, rounds %.3f ms (run set-up %.3f, GA rounds %.3f, "
+                   "incumbent merge %.3f, best_half %.3f ms in %lld calls, device GA %.3f ms), "
+                   "final %.3f ms, total %.3f ms\n",
+                   1e3 * (t_setup - t0), 1e3 * (t_rounds - t_setup), 1e3 * t_env, 1e3 * t_run,
+                   1e3 * t_inc, ctx.best_half_ms - bh0,
                    static_cast<long long>(ctx.best_half_calls - bhc0), S.eval_ms,
                    1e3 * (now_s() - t_rounds), 1e3 * S.wall_s);
       std::fclose(f);

@@ -54,7 +54,8 @@ __device__ __forceinline__ void carve_e2e(Ws& s, uint8_t* base, const E2ESizes& 
 
 template <int kWarps>
 __global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
-sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, int64_t stride,
+sweep_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCostConfig cfg,
+             const uint8_t* __restrict__ recs, int64_t stride,
              int64_t n, uint64_t k0, int slab_bytes, int cls_smem, uint8_t* __restrict__ gslab,
              int64_t gslab_bytes, EvalResult* __restrict__ res, SweepPartial* __restrict__ part,
              unsigned long long* __restrict__ n_global, int sync,
@@ -86,7 +87,8 @@ sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, 
     s.job = s.job_words;
     s.dtab_stride = 0;
     s.cls = cls_smem ? smem : P.cls;
-    s.cta_sync = sync ? static_cast<int32_t>(blockDim.x) : 0;
+    s.cta_sync = sync == 1 ? static_cast<int32_t>(blockDim.x) : 0;  // per-task barriers
+
   }
   __syncthreads();
   uint8_t* const slab = smem + cls_bytes + warp * slab_bytes;
@@ -95,28 +97,28 @@ sweep_kernel(DevProblem P, DevCostConfig cfg, const uint8_t* __restrict__ recs, 
   SweepPartial acc = part[gw];
   unsigned long long spilled = 0;
   // with sync, every warp runs the same number of rounds (one plan or an idle
-  // pass each) so the CTA's barriers line up: one at the start of a plan and
-  // one before each task's cost (end_to_end)
+  // pass each) so the CTA's barriers line up: one at the start of a plan
+  // (sync >= 1) and one before each task's cost (end_to_end; sync == 1)
   const int64_t step = static_cast<int64_t>(gridDim.x) * kWarps;
   const int64_t rounds = sync ? (n + step - 1) / step : 0;
   for (int64_t p = gw, rd = 0; sync ? rd < rounds : p < n; p += step, ++rd) {
     if (sync) bar_sync(5, blockDim.x);
     if (p >= n) {
-      for (int t = 0; t < T; ++t) bar_sync(5, blockDim.x);
+      if (sync == 1)
+        for (int t = 0; t < T; ++t) bar_sync(5, blockDim.x);
       continue;
     }
     // the chunk's plans in work-class order: consecutive plans (one round of
     // a CTA) have similar per-task shapes
     const int64_t q = order ? static_cast<int64_t>(__ldg(order + p)) : p;
     const uint8_t* rec = recs + q * stride;
+    // the header and offsets go straight into the warp's shared Ws (eval_one
+    // restages them): no per-thread copies in local memory
+    if (lane < 20) reinterpret_cast<int32_t*>(&s.h)[lane] = __ldcg(reinterpret_cast<const int32_t*>(rec) + lane);
+    __syncwarp();
     if (lane == 0) {
-      RecHeader h;
-      int32_t* hw = reinterpret_cast<int32_t*>(&h);
-#pragma unroll
-      for (int i = 0; i < 20; ++i) hw[i] = __ldcg(reinterpret_cast<const int32_t*>(rec) + i);
-      RecOffsets o;
-      rec_offsets(h, o);
-      const E2ESizes z = e2e_sizes(o, h, T);
+      rec_offsets(s.h, s.o);
+      const E2ESizes z = e2e_sizes(s.o, s.h, T);
       const int need = e2e_carve_bytes(z, N, T);
       const bool fits = need <= slab_bytes;
       spilled += fits ? 0 : 1;
