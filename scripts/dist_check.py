@@ -27,7 +27,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    names = sys.argv[1:] or ["search_c1_b1000.json", "search_c2_b1000.json"]
+    names = sys.argv[1:] or ["search_c1_b1000.json", "search_c2_b1000.json",
+                             "search_c2_b10000.json", "search_c4_b10000.json"]
     ok = True
     for name in names:
         g = load(name)
@@ -45,6 +46,26 @@ def main():
         print(json.dumps({"rank": rank, "world": world, "case": name, "ok": not bad,
                           "bad": bad[:3], "wall_s": dt, "consumed": res.consumed}), flush=True)
         eng.close()
+    # sharded config-5 sweep (hpg_sweep_dist): global argmin / count / checksum
+    # equal to one GPU sweeping the whole range
+    from paper_2512_12476_b200 import load_topology, load_workflow
+    fx = os.path.join(ROOT, "fixtures")
+    eng = Engine(load_workflow(f"{fx}/c4.workflow.json"), load_topology(f"{fx}/c4.topology.json"),
+                 device=local)
+    idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        idt.copy_(torch.tensor(list(eng.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idt, 0)
+    total = 400000
+    st = eng.sweep_dist(42, total, rank, world, bytes(idt.cpu().tolist()))
+    one = eng.sweep_resident(42, 0, total)
+    keys = ("best_cost", "best_k", "n_feasible", "xor_bits")
+    sweep_ok = all(st[k] == one[k] for k in keys)
+    ok = ok and sweep_ok
+    print(json.dumps({"rank": rank, "world": world, "case": "sweep_dist", "ok": sweep_ok,
+                      "dist": {k: st[k] for k in keys}, "single": {k: one[k] for k in keys}}),
+          flush=True)
+    eng.close()
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
