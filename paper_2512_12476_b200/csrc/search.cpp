@@ -1499,9 +1499,11 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   S.task_groupings = static_cast<int64_t>(tgs.size());
 
   const int n_devices = P.N;
-  std::vector<TgArm> arms;
-  for (size_t ti = 0; ti < tgs.size(); ++ti) {
-    TgArm arm;
+  // level-2 arms of every task grouping: independent per grouping (each
+  // sampled from its own fork of the base stream), built on the host pool
+  std::vector<TgArm> arms(tgs.size());
+  host_parallel_for(static_cast<int>(tgs.size()), tgs.size() >= 16, [&](int ti) {
+    TgArm& arm = arms[ti];
     arm.tg = tgs[ti];
     const int k = static_cast<int>(arm.tg.size());
     if (k <= n_devices) {
@@ -1529,6 +1531,10 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
       }
     }
     arm.best.assign(arm.ggs.size(), kInf);
+  });
+  // arm records in (task grouping, GPU grouping) order
+  for (size_t ti = 0; ti < arms.size(); ++ti) {
+    TgArm& arm = arms[ti];
     for (size_t gi = 0; gi < arm.ggs.size(); ++gi) {
       arm.alive.push_back(static_cast<int64_t>(gi));
       arm.rec.push_back(static_cast<int64_t>(S.arms.size()));
@@ -1537,7 +1543,6 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
       r.gg = static_cast<int64_t>(gi);
       S.arms.push_back(r);
     }
-    arms.push_back(std::move(arm));
   }
 
   const double t_setup = now_s();
@@ -1600,37 +1605,49 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
       nvtxRangePushA(range_name);
       const double t_round0 = now_s();
       std::vector<ArmRun*> batch;
+      // the round's runs in sequential order: (part, gi, slice); their state
+      // (RNG fork, layout options) is built on the host pool below
+      struct RunSpec {
+        Part* p;
+        int64_t gi, slice;
+      };
+      std::vector<RunSpec> specs;
       for (auto& p : ps) {
         p.runs.emplace_back();
         if (n >= p.rounds) continue;
-        auto& list = p.runs.back();
-        auto add = [&](int64_t gi, int64_t slice) {
-          auto r = std::make_unique<ArmRun>();
-          r->ti = p.ti;
-          r->gi = gi;
-          r->slice = slice;
-          const uint64_t salt = (static_cast<uint64_t>(p.ti) << 40) |
-                                (static_cast<uint64_t>(gi) << 16) |
-                                (static_cast<uint64_t>(m) << 8) | static_cast<uint64_t>(n);
-          r->rng = base_rng.fork(salt);
-          TgArm& arm = arms[p.ti];
-          r->env.reset(new ArmEnv{P, K, arm.tg, arm.ggs[gi], build_arm_layouts(P, arm.tg, arm.ggs[gi])});
-          batch.push_back(r.get());
-          list.push_back(std::move(r));
-        };
         const int64_t b_mn = p.b / (static_cast<int64_t>(p.cur.size()) * p.denom_in);
         if (b_mn >= 1) {
-          for (int64_t gi : p.cur) add(gi, b_mn);
+          for (int64_t gi : p.cur) specs.push_back({&p, gi, b_mn});
         } else {
           int64_t rb = p.b / p.denom_in;
           if (rb == 0 && n == 0) rb = p.b;
           int64_t spent = 0;
           for (int64_t gi : p.cur) {
             if (spent >= rb) break;
-            add(gi, 1);
+            specs.push_back({&p, gi, 1});
             ++spent;
           }
         }
+      }
+      std::vector<std::unique_ptr<ArmRun>> made(specs.size());
+      host_parallel_for(static_cast<int>(specs.size()), specs.size() >= 32, [&](int i) {
+        const RunSpec& sp = specs[i];
+        auto r = std::make_unique<ArmRun>();
+        r->ti = sp.p->ti;
+        r->gi = sp.gi;
+        r->slice = sp.slice;
+        const uint64_t salt = (static_cast<uint64_t>(sp.p->ti) << 40) |
+                              (static_cast<uint64_t>(sp.gi) << 16) |
+                              (static_cast<uint64_t>(m) << 8) | static_cast<uint64_t>(n);
+        r->rng = base_rng.fork(salt);
+        const TgArm& arm = arms[sp.p->ti];
+        r->env.reset(new ArmEnv{P, K, arm.tg, arm.ggs[sp.gi],
+                                build_arm_layouts(P, arm.tg, arm.ggs[sp.gi])});
+        made[i] = std::move(r);
+      });
+      for (size_t i = 0; i < specs.size(); ++i) {
+        batch.push_back(made[i].get());
+        specs[i].p->runs.back().push_back(std::move(made[i]));
       }
       const double t_env_done = now_s();
       t_env += t_env_done - t_round0;
