@@ -148,6 +148,8 @@ SweepTablesDev& sweep_tables(Ctx& C) {
   h.tb.tg_ng = reinterpret_cast<const int8_t*>(b + o_ng);
   h.tb.opt_off = reinterpret_cast<const int32_t*>(b + o_off);
   h.tb.opt = reinterpret_cast<const int16_t*>(b + o_opt);
+  h.tb.gen_slot = C.dprob.gen_slot;
+  h.tb.train6_slot = C.dprob.train6_slot;
   h.tb.train_mask = 0;
   for (int s = 0; s < T; ++s)
     if (C.dprob.task[s].kind == kTraining) h.tb.train_mask |= 1 << s;

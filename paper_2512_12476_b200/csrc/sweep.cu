@@ -20,16 +20,24 @@
 namespace hpg {
 namespace dev {
 
-// 3-bit work class of one task of a plan (end_to_end_cost's phases: cell
-// pieces, TP ring bounds, PP pairs, DP rings), on a log2 scale
-__device__ __forceinline__ uint32_t work_class(int dp, int pp, int tp, bool train) {
+// Work estimate of one task of a plan (end_to_end_cost's phases: cell
+// pieces, TP ring bounds, PP pairs, DP rings) and its class on a log2 scale
+// with `halves` sub-steps per octave, clamped to `levels` classes
+__device__ __forceinline__ uint32_t work_estimate(int dp, int pp, int tp, bool train) {
   const int ncell = dp * pp;
   uint32_t w = 2u * ((ncell + 31) >> 5) + static_cast<uint32_t>(((dp + 31) >> 5) * pp);
   if (tp > 1) w += static_cast<uint32_t>(((ncell * tp + 31) >> 5) * tp);
   if (pp > 1) w += static_cast<uint32_t>((ncell * tp * tp + 31) >> 5);
   if (train && dp > 1) w += static_cast<uint32_t>(pp * tp * (dp == 2 ? 1 : (dp <= 8 ? 24 : 4 * dp)));
+  return w;
+}
+__device__ __forceinline__ uint32_t work_class(uint32_t w, int halves, int levels) {
+  // floor(halves * log2(w)) from the leading bit and the next one
   const int lg = 31 - __clz(w | 1u);
-  return static_cast<uint32_t>(lg < 3 ? 0 : (lg - 3 > 7 ? 7 : lg - 3));
+  int c = halves * lg;
+  if (halves == 2 && lg > 0 && ((w >> (lg - 1)) & 1u)) ++c;
+  c -= 3 * halves;  // w < 8: class 0
+  return static_cast<uint32_t>(c < 0 ? 0 : (c >= levels ? levels - 1 : c));
 }
 
 __global__ void gen_kernel(SweepTablesDev tb, uint64_t seed, uint64_t k0, int64_t n,
@@ -113,9 +121,27 @@ __global__ void gen_kernel(SweepTablesDev tb, uint64_t seed, uint64_t k0, int64_
     my_bytes = 1 + ng + 9;
     for (int s = 0; s < T; ++s) my_bytes += 3 + h.pp[s] + ro.dev[s + 1] - ro.dev[s];
     if (keys) {
+      // most significant first: the training tasks (DP rings: the largest and
+      // most variable share of a plan; 16 half-octave classes each), the
+      // generation -> actor-training bridge (na * nb edge costs; 8 classes),
+      // the generation task (8 classes), the inference tasks (4 classes each)
       uint32_t key = 0;
       for (int s = 0; s < T; ++s)
-        key = (key << 3) | work_class(h.dp[s], h.pp[s], h.tp[s], (tb.train_mask >> s) & 1);
+        if ((tb.train_mask >> s) & 1)
+          key = (key << 4) | work_class(work_estimate(h.dp[s], h.pp[s], h.tp[s], true), 2, 16);
+      if (tb.gen_slot >= 0 && tb.train6_slot >= 0) {
+        const int g = tb.gen_slot, a = tb.train6_slot;
+        const uint32_t na = static_cast<uint32_t>(h.dp[g] * h.pp[g] * h.tp[g]);
+        const uint32_t nb = static_cast<uint32_t>(h.dp[a] * h.pp[a] * h.tp[a]);
+        key = (key << 3) | work_class((na * nb + 31) >> 5, 1, 8);
+      }
+      for (int s = 0; s < T; ++s) {
+        if ((tb.train_mask >> s) & 1) continue;
+        const bool gen = s == tb.gen_slot;
+        key = (key << (gen ? 3 : 2)) |
+              work_class(work_estimate(h.dp[s], h.pp[s], h.tp[s], false), 1, gen ? 8 : 4);
+      }
+      key &= (1u << kSweepKeyBits) - 1u;
       keys[idx] = key;
       atomicAdd(&hist[key], 1u);
     }

@@ -17,14 +17,15 @@ struct SweepTablesDev {
   const int32_t* opt_off;   // [T * (N + 1) + 1] layout options of (slot, count)
   const int16_t* opt;       // [n_opt * 3] (dp, pp, tp) in enumerate_layouts order
   int32_t train_mask;       // bit t: task slot t is a training task (DP rings)
+  int32_t gen_slot, train6_slot;  // generation / actor-training slots (bridge), -1 if absent
 };
 
 // Work-class grouping of a chunk (sweep.cu): gen_kernel gives every plan a
-// key of 3-bit per-task work classes (kSweepKeyBits bits) and counts them; a
+// key of per-task work classes (kSweepKeyBits bits) and counts them; a
 // counting sort orders the chunk by key, so the plan-warps of one CTA score
 // plans of similar shape side by side (their per-task phase barriers then
 // wait little; see sweep_kernel.cuh).
-constexpr int kSweepKeyBits = 18;
+constexpr int kSweepKeyBits = 20;  // PPO: 2 x 4 (training) + 3 (bridge) + 3 (generation) + 3 x 2
 struct SweepOrder {
   uint32_t* keys = nullptr;   // [chunk]
   uint32_t* hist = nullptr;   // [1 << kSweepKeyBits], bin offsets after the scan
