@@ -90,6 +90,7 @@ struct Ws {
   int32_t cc_sig_ok;
   double cc_vol;              // staged volume
   int32_t cta_sync;           // sweep: CTA-wide barrier (threads) before each task's cost, 0 = none
+  unsigned long long ring_best;  // ring_small: the warp's best cycle so far (bits of a cost >= 0)
   long long* prof;            // diagnostics: this plan's profile slots
   const uint8_t* cls;         // link class matrix [N*N]: shared-memory copy or P.cls
   // helper-warp team (one plan per CTA, warp 0 leads)
@@ -643,10 +644,47 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
     double cached;
     if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
   }
+  // a better upper bound before the search: lane v < n builds the
+  // nearest-neighbour tour from vertex v; the warp keeps the best of them
+  if (lane < n) {
+    unsigned used = 1u << lane;
+    int cur = lane;
+    double mx = 0.0;
+    for (int step = 1; step < n; ++step) {
+      double bc = kInf;
+      int bi = 0;
+      for (int u = 0; u < n; ++u) {
+        if ((used >> u) & 1u) continue;
+        const double c = rm[cur * n + u];
+        if (c < bc) {
+          bc = c;
+          bi = u;
+        }
+      }
+      used |= 1u << bi;
+      mx = smax(mx, bc);
+      cur = bi;
+    }
+    ub = smin(ub, smax(mx, rm[cur * n + lane]));
+  }
+  ub = warp_min(ub);
+  // lb <= optimum <= ub: a tour at the lower bound is optimal
+  if (ub <= lb) {
+    double stored;
+    if (P.ring_cache && ring_payload_of(P, s, key, ub, stored)) ring_insert(P, key, stored);
+    return ub;
+  }
   double best = ub;
+  // the lanes share their best complete cycle through the warp's shared slot
+  // (costs are >= 0, so their bit patterns order like the values): every
+  // lane prunes against the best found by any lane. Exact min either way.
+  volatile unsigned long long* shared_best = &s.ring_best;
+  if (lane == 0) *shared_best = static_cast<unsigned long long>(__double_as_longlong(best));
+  __syncwarp();
   const int m = n - 1;
   const int nprefix = m * (m - 1);
   for (int p = lane; p < nprefix; p += 32) {
+    best = smin(best, __longlong_as_double(static_cast<long long>(*shared_best)));
     const int a = 1 + p / (m - 1);
     const int bi = p % (m - 1);
     const int b = 1 + bi + ((1 + bi) >= a ? 1 : 0);
@@ -668,7 +706,12 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
     nxt[3] = 1;
     while (d >= 3) {
       if (d == n) {
-        best = smin(best, smax(cmx[n - 1], rm[path[n - 1] * n]));
+        const double cyc = smax(cmx[n - 1], rm[path[n - 1] * n]);
+        if (cyc < best) {
+          best = cyc;
+          atomicMin(const_cast<unsigned long long*>(shared_best),
+                    static_cast<unsigned long long>(__double_as_longlong(cyc)));
+        }
         --d;
         used &= ~(1u << path[d]);
         continue;
@@ -681,6 +724,7 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
         continue;
       }
       nxt[d] = v + 1;
+      best = smin(best, __longlong_as_double(static_cast<long long>(*shared_best)));
       const double c = smax(cmx[d - 1], rm[path[d - 1] * n + v]);
       if (c >= best) continue;
       path[d] = v;
@@ -690,6 +734,8 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
       nxt[d] = 1;
     }
   }
+  __syncwarp();
+  best = smin(best, __longlong_as_double(static_cast<long long>(*shared_best)));
   best = warp_min(best);
   double stored;
   if (P.ring_cache && ring_payload_of(P, s, key, best, stored)) ring_insert(P, key, stored);
