@@ -835,84 +835,103 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   std::vector<Poly256> jumps;
   std::map<int32_t, int32_t> jump_at;  // gen_draws -> first polynomial
   std::vector<GaRun> gr(n);
-  {
-    // jump tables for every draw count of this round, built in parallel
-    std::vector<int64_t> ds;
-    for (int i = 0; i < n; ++i)
-      ds.push_back(gen_draws_per_candidate(P.N, nodes_per_region.data(),
-                                           static_cast<int>(nodes_per_region.size()),
-                                           gen_item_of(*runs[i]->env)));
-    std::sort(ds.begin(), ds.end());
-    ds.erase(std::unique(ds.begin(), ds.end()), ds.end());
-    const int nd = static_cast<int>(ds.size());
-    host_parallel_for(nd, nd >= 2, [&](int i) {
-      jump_table(static_cast<uint64_t>(ds[i]), kGaJumps);
-    });
-  }
-  for (int i = 0; i < n; ++i) {
-    const ArmRun& r = *runs[i];
-    const ArmEnv& e = *r.env;
-    GaRun& g = gr[i];
-    std::memset(static_cast<void*>(&g), 0, sizeof(g));
-    g.slice = r.slice;
-    g.ng = static_cast<int32_t>(e.tg.size());
-    int k = 0, mw = 0, msl = 0, mslots = 0, mcells = 0, mdpk = 0, mrec = 0;
-    g.opt_base = static_cast<int64_t>(opts.size());
+  // pass 1 (host pool): per run, its layout-option count, draw count per
+  // candidate and record bounds
+  struct RunPrep {
+    int64_t n_opts = 0, gen_draws = 0;
+    int mw = 0, msl = 0, mslots = 0, mcells = 0, mdpk = 0, mrec = 0;
+  };
+  std::vector<RunPrep> rp(n);
+  host_parallel_for(n, n >= 64, [&](int i) {
+    const ArmEnv& e = *runs[i]->env;
+    RunPrep& q = rp[i];
     for (size_t gi = 0; gi < e.tg.size(); ++gi) {
-      g.gstart[gi] = k;
-      g.counts[gi] = e.counts[gi];
       for (int s : e.tg[gi]) {
-        g.gslot[k] = s;
-        g.opt_off[k] = static_cast<int32_t>(opts.size() - g.opt_base);
         int xdp = 0, xpp = 0, xcell = 0, xdpk = 0, xrec = 0;
         for (const Layout& l : e.al.options[s]) {
-          opts.push_back(make_short4(static_cast<short>(l.dp), static_cast<short>(l.pp),
-                                     static_cast<short>(l.tp), 0));
           xdp = std::max(xdp, l.dp);
           xpp = std::max(xpp, l.pp);
           xcell = std::max(xcell, l.dp * l.pp);
           xdpk = std::max(xdpk, l.pp * l.tp);
           xrec = std::max(xrec, 8 * l.dp + 4 * l.pp);
         }
-        mw += xdp;
-        msl += xpp;
-        mcells += xcell;
-        mdpk += xdpk;
-        mrec += xrec;
-        mslots += e.counts[gi];
+        q.n_opts += static_cast<int64_t>(e.al.options[s].size());
+        q.mw += xdp;
+        q.msl += xpp;
+        q.mcells += xcell;
+        q.mdpk += xdpk;
+        q.mrec += xrec;
+        q.mslots += e.counts[gi];
+      }
+    }
+    q.gen_draws = gen_draws_per_candidate(P.N, nodes_per_region.data(),
+                                          static_cast<int>(nodes_per_region.size()), gen_item_of(e));
+  });
+  // round-wide bounds, option offsets, jump tables per distinct draw count
+  // (first-appearance order; the tables themselves built in parallel)
+  std::vector<int64_t> opt_base(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    const RunPrep& q = rp[i];
+    opt_base[i + 1] = opt_base[i] + q.n_opts;
+    stride = std::max(stride, (static_cast<int>(sizeof(RecHeader)) + q.mrec + q.mslots + 15) & ~15);
+    cv.max_w = std::max(cv.max_w, q.mw);
+    cv.max_sl = std::max(cv.max_sl, q.msl);
+    cv.max_slots = std::max(cv.max_slots, q.mslots);
+    cv.max_cells = std::max(cv.max_cells, q.mcells);
+    cv.max_dpk = std::max(cv.max_dpk, q.mdpk);
+    remaining += runs[i]->slice;
+  }
+  std::vector<int64_t> ds;
+  for (int i = 0; i < n; ++i)
+    if (jump_at.emplace(static_cast<int32_t>(rp[i].gen_draws), 0).second) ds.push_back(rp[i].gen_draws);
+  std::vector<JumpTable> tables(ds.size());
+  host_parallel_for(static_cast<int>(ds.size()), ds.size() >= 2, [&](int i) {
+    tables[i] = jump_table(static_cast<uint64_t>(ds[i]), kGaJumps);
+  });
+  for (size_t i = 0; i < ds.size(); ++i) {
+    // x^(L*D) for L = 1..127: lane offsets and strides of a team of four
+    jump_at[static_cast<int32_t>(ds[i])] = static_cast<int32_t>(jumps.size());
+    jumps.insert(jumps.end(), tables[i]->begin(), tables[i]->begin() + kGaJumps);
+  }
+  opts.resize(static_cast<size_t>(opt_base[n]));
+  // pass 2 (host pool): the GaRun of every run and its layout options
+  host_parallel_for(n, n >= 64, [&](int i) {
+    const ArmRun& r = *runs[i];
+    const ArmEnv& e = *r.env;
+    GaRun& g = gr[i];
+    std::memset(static_cast<void*>(&g), 0, sizeof(g));
+    g.slice = r.slice;
+    g.ng = static_cast<int32_t>(e.tg.size());
+    g.opt_base = opt_base[i];
+    int k = 0;
+    int64_t at = opt_base[i];
+    for (size_t gi = 0; gi < e.tg.size(); ++gi) {
+      g.gstart[gi] = k;
+      g.counts[gi] = e.counts[gi];
+      for (int s : e.tg[gi]) {
+        g.gslot[k] = s;
+        g.opt_off[k] = static_cast<int32_t>(at - g.opt_base);
+        for (const Layout& l : e.al.options[s])
+          opts[at++] = make_short4(static_cast<short>(l.dp), static_cast<short>(l.pp),
+                                   static_cast<short>(l.tp), 0);
         ++k;
       }
     }
     g.gstart[e.tg.size()] = k;
-    g.opt_off[k] = static_cast<int32_t>(opts.size() - g.opt_base);
-    stride = std::max(stride, (static_cast<int>(sizeof(RecHeader)) + mrec + mslots + 15) & ~15);
-    cv.max_w = std::max(cv.max_w, mw);
-    cv.max_sl = std::max(cv.max_sl, msl);
-    cv.max_slots = std::max(cv.max_slots, mslots);
-    cv.max_cells = std::max(cv.max_cells, mcells);
-    cv.max_dpk = std::max(cv.max_dpk, mdpk);
-    g.gen_draws = static_cast<int32_t>(gen_draws_per_candidate(
-        P.N, nodes_per_region.data(), static_cast<int>(nodes_per_region.size()), gen_item_of(e)));
-    auto ja = jump_at.find(g.gen_draws);
-    if (ja == jump_at.end()) {
-      ja = jump_at.emplace(g.gen_draws, static_cast<int32_t>(jumps.size())).first;
-      // x^(L*D) for L = 1..127: lane offsets and strides of a team of four
-      const JumpTable tb = jump_table(static_cast<uint64_t>(g.gen_draws), kGaJumps);
-      jumps.insert(jumps.end(), tb->begin(), tb->begin() + kGaJumps);
-    }
-    g.jump_off = ja->second;
+    g.opt_off[k] = static_cast<int32_t>(at - g.opt_base);
+    g.gen_draws = static_cast<int32_t>(rp[i].gen_draws);
+    g.jump_off = jump_at.at(g.gen_draws);
     const int64_t it = std::max<int64_t>(
         1, std::min({r.slice, static_cast<int64_t>(K.population), r.slice / 2}));
     g.init_target = static_cast<int32_t>(it);
     g.attempt_cap = 64 + 16 * it;
-    init_cap = std::max<int>(init_cap, static_cast<int>(g.attempt_cap));
     g.rng = r.rng;
     g.best = kInf;
     g.best_member_cost = kInf;
     g.state = kGaInit;
     for (int m = 0; m < pop_cap; ++m) g.pop_slot[m] = 2 + m;
-    remaining += r.slice;
-  }
+  });
+  for (int i = 0; i < n; ++i) init_cap = std::max<int>(init_cap, static_cast<int>(gr[i].attempt_cap));
   const int res_per_run = std::max(2 * max_wave, init_cap);
   const int64_t gen_bytes =
       (2 * (gt.n_regions + gt.max_nodes_per_region + 4 * gt.n_nodes) + 2 * gt.n_dev + 15) & ~15;
