@@ -84,6 +84,8 @@ struct DevProblem {
   const double* bw;    // [n_classes] bytes/s (inf for self)
   RingSlot* ring_cache;       // nullptr = disabled
   unsigned long long ring_mask;  // slots - 1 (power of two)
+  int32_t ring_nn_min;        // ring_small: nearest-neighbour bound + lane sharing from this size
+  int32_t pad_;
 };
 
 // ---- packed plan record ----

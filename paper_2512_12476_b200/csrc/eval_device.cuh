@@ -651,7 +651,7 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
   // bound before the search: lane v < n builds the nearest-neighbour tour
   // from vertex v, the warp keeps the best of them, and the lanes share their
   // best cycle during the search. Smaller rings search directly.
-  const bool big = n >= 7;
+  const bool big = n >= P.ring_nn_min;
   if (big && lane < n) {
     unsigned used = 1u << lane;
     int cur = lane;
