@@ -85,7 +85,7 @@ struct DevProblem {
   RingSlot* ring_cache;       // nullptr = disabled
   unsigned long long ring_mask;  // slots - 1 (power of two)
   int32_t ring_nn_min;        // ring_small: nearest-neighbour bound + lane sharing from this size
-  int32_t pad_;
+  int32_t ring_redux;         // ring_heuristic: NN step as a 32-bit (class rank, index) warp min
 };
 
 // ---- packed plan record ----

@@ -414,7 +414,8 @@ void stage_problem(Ctx& ctxr, Problem&& P) {
     // ring size up (9 = never); HPG_RING_NN_MIN overrides (A/B measurements)
     const char* nn = std::getenv("HPG_RING_NN_MIN");
     D.ring_nn_min = nn ? std::atoi(nn) : 7;
-    D.pad_ = 0;
+    const char* rx = std::getenv("HPG_RING_REDUX");
+    D.ring_redux = rx ? std::atoi(rx) : 0;
     if (use_rc) {
       ctx->d_ring.reserve(kSlots * sizeof(RingSlot));
       cuda_check(cudaMemsetAsync(ctx->d_ring.p, 0, kSlots * sizeof(RingSlot), ctx->stream),

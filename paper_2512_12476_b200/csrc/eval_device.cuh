@@ -787,41 +787,69 @@ __device__ __noinline__ double ring_heuristic(const DevProblem& P, Ws& s, const 
   const int lane = threadIdx.x & 31;
   uint8_t* tour = s.tour;
   double* edge = s.edge;
-  // every edge cost is the staged cost of its link class, so "cheapest next
-  // vertex, earliest index among equals" is the minimum of (rank of the class
-  // cost, index): one 32-bit warp reduction per step. Ranks count the
-  // strictly cheaper classes, so equal costs share a rank.
-  for (int c = lane; c < P.n_classes; c += 32) {
-    int rank = 0;
-    const double cc = s.cc[c];
-    for (int q = 0; q < P.n_classes; ++q) rank += s.cc[q] < cc ? 1 : 0;
-    s.crank[c] = static_cast<uint8_t>(rank);
-  }
-  __syncwarp();
-  const uint8_t* cls = s.cls;
-  const uint8_t* crank = s.crank;
-  const int N = P.n_dev;
   bool used[8] = {false, false, false, false, false, false, false, false};
   if (lane == 0) used[0] = true;
   int last = devs[0];
   if (lane == 0) tour[0] = devs[0];
-  for (int step = 1; step < n; ++step) {
-    unsigned key = 0xffffffffu;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int i = lane + 32 * r;
-      if (i >= n) break;
-      if (!used[r]) {
-        const unsigned k = (static_cast<unsigned>(crank[cls[last * N + devs[i]]]) << 8) |
-                           static_cast<unsigned>(i);
-        key = k < key ? k : key;
-      }
+  if (P.ring_redux) {
+    // every edge cost is the staged cost of its link class, so "cheapest next
+    // vertex, earliest index among equals" is the minimum of (rank of the
+    // class cost, index): one 32-bit warp reduction per step. Ranks count
+    // the strictly cheaper classes, so equal costs share a rank.
+    for (int c = lane; c < P.n_classes; c += 32) {
+      int rank = 0;
+      const double cc = s.cc[c];
+      for (int q = 0; q < P.n_classes; ++q) rank += s.cc[q] < cc ? 1 : 0;
+      s.crank[c] = static_cast<uint8_t>(rank);
     }
-    key = __reduce_min_sync(kFull, key);
-    const int bi = static_cast<int>(key & 0xffu);
-    if ((bi & 31) == lane) used[bi >> 5] = true;
-    last = devs[bi];
-    if (lane == 0) tour[step] = static_cast<uint8_t>(last);
+    __syncwarp();
+    const uint8_t* cls = s.cls;
+    const uint8_t* crank = s.crank;
+    const int N = P.n_dev;
+    for (int step = 1; step < n; ++step) {
+      unsigned key = 0xffffffffu;
+      for (int r = 0; r < 8; ++r) {
+        const int i = lane + 32 * r;
+        if (i >= n) break;
+        if (!used[r]) {
+          const unsigned k = (static_cast<unsigned>(crank[cls[last * N + devs[i]]]) << 8) |
+                             static_cast<unsigned>(i);
+          key = k < key ? k : key;
+        }
+      }
+      key = __reduce_min_sync(kFull, key);
+      const int bi = static_cast<int>(key & 0xffu);
+      if ((bi & 31) == lane) used[bi >> 5] = true;
+      last = devs[bi];
+      if (lane == 0) tour[step] = static_cast<uint8_t>(last);
+    }
+  } else {
+    for (int step = 1; step < n; ++step) {
+      double bc = kInf;
+      int bi = 0x7fffffff;
+      for (int r = 0; r < 8; ++r) {
+        const int i = lane + 32 * r;
+        if (i >= n) break;
+        if (!used[r]) {
+          const double c = ecost(P, s, last, devs[i]);
+          if (c < bc) {
+            bc = c;
+            bi = i;
+          }
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oc = __shfl_xor_sync(kFull, bc, o);
+        const int oi = __shfl_xor_sync(kFull, bi, o);
+        if (oc < bc || (oc == bc && oi < bi)) {
+          bc = oc;
+          bi = oi;
+        }
+      }
+      if ((bi & 31) == lane) used[bi >> 5] = true;
+      last = devs[bi];
+      if (lane == 0) tour[step] = static_cast<uint8_t>(last);
+    }
   }
   __syncwarp();
   double bott = 0.0;

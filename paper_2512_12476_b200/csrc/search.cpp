@@ -8,6 +8,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <chrono>
 #include <coroutine>
 #include <cstring>
@@ -1077,7 +1078,11 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   ++ctx.eval_launches;
   // results: run states and control words, the two kept plans per run, then
   // the improvements
-  cuda_check(cudaMemcpyAsync(H + h_runs, D + o_runs, sizeof(GaRun) * n, cudaMemcpyDeviceToHost, st), "D2H ga runs");
+  // only the run summary the host reads (used, best, counters, flags): the
+  // GaRun prefix before the population and stage state
+  constexpr size_t kRunSummary = offsetof(GaRun, pop_slot);
+  cuda_check(cudaMemcpy2DAsync(H + h_runs, sizeof(GaRun), D + o_runs, sizeof(GaRun), kRunSummary, n,
+                               cudaMemcpyDeviceToHost, st), "D2H ga runs");
   cuda_check(cudaMemcpyAsync(H + h_ctl, D + o_ctl, 8 * kGaCtlWords, cudaMemcpyDeviceToHost, st), "D2H ga ctl");
   cuda_check(cudaMemcpy2DAsync(H + h_best, 2 * stride, D + o_pool, run_bytes, 2 * stride, n,
                                cudaMemcpyDeviceToHost, st), "D2H ga best plans");
@@ -1102,7 +1107,7 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   ctx.plans_evaluated += static_cast<int64_t>(hctl[kGaCtlEvals]);
   ctx.canonical_bytes += static_cast<int64_t>(hctl[kGaCtlBytes]);
   ctx.h2d_bytes += h2d;
-  ctx.d2h_bytes += static_cast<int64_t>(sizeof(GaRun)) * n + 8 * kGaCtlWords +
+  ctx.d2h_bytes += static_cast<int64_t>(offsetof(GaRun, pop_slot)) * n + 8 * kGaCtlWords +
                    2 * static_cast<int64_t>(stride) * n +
                    static_cast<int64_t>(sizeof(GaImpr)) * std::max(n_impr, impr_pre);
   const unsigned long long t0_dev = hctl[kGaCtlT0];
