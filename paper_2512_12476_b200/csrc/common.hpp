@@ -84,8 +84,6 @@ struct DevProblem {
   const double* bw;    // [n_classes] bytes/s (inf for self)
   RingSlot* ring_cache;       // nullptr = disabled
   unsigned long long ring_mask;  // slots - 1 (power of two)
-  int32_t ring_nn_min;        // ring_small: nearest-neighbour bound + lane sharing from this size
-  int32_t ring_redux;         // ring_heuristic: NN step as a 32-bit (class rank, index) warp min
 };
 
 // ---- packed plan record ----
@@ -182,7 +180,7 @@ HPG_HD int carve_bytes(const Carve& c) {
   const int N = c.n_dev, T = c.n_tasks;
   int b = 0;
   b += 2 * carve_round(8 * c.max_w) + 2 * carve_round(8 * c.max_cells) + carve_round(8 * c.max_dpk);
-  b += 7 * carve_round(8 * N) + carve_round(9 * kMaxClasses) + carve_round(8 * 64) +
+  b += 7 * carve_round(8 * N) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
        carve_round(8 * T * 7);
   b += 2 * carve_round(4 * c.max_sl) + carve_round(4 * c.max_dpk) + carve_round(4 * N);
   b += carve_round(c.max_slots) + carve_round(T * N) + 2 * carve_round(N);
@@ -199,7 +197,7 @@ constexpr int kClsSmemMax = 16384;
 // per-warp scratch of a helper warp (cell pieces, ring scratch, class costs)
 HPG_HD int team_scratch_bytes(const Carve& c) {
   const int N = c.n_dev;
-  return 5 * carve_round(8 * N) + carve_round(9 * kMaxClasses) + carve_round(8 * 64) +
+  return 5 * carve_round(8 * N) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
          2 * carve_round(N);
 }
 
@@ -253,7 +251,7 @@ HPG_HD E2ESizes e2e_sizes_max(int N, int T) {
 HPG_HD int e2e_carve_bytes(const E2ESizes& z, int N, int T) {
   return 2 * carve_round(8 * z.w) + 3 * carve_round(8 * z.cells) + carve_round(8 * z.dpk) +
          carve_round(4 * z.dpk) + carve_round(8 * N) + 4 * carve_round(8 * z.cell_max) +
-         carve_round(8 * z.ring_max) + carve_round(9 * kMaxClasses) + carve_round(8 * 64) +
+         carve_round(8 * z.ring_max) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
          carve_round(8 * T * 7) + carve_round(4 * z.sl) + 2 * carve_round(8 * z.sl) +
          carve_round(z.slots) + carve_round(T * N) + 2 * carve_round(z.ring_max);
 }

@@ -410,12 +410,6 @@ void stage_problem(Ctx& ctxr, Problem&& P) {
     constexpr size_t kSlots = size_t(1) << 20;
     D.ring_cache = nullptr;
     D.ring_mask = kSlots - 1;
-    // ring_small's nearest-neighbour bound and lane sharing apply from this
-    // ring size up (9 = never); HPG_RING_NN_MIN overrides (A/B measurements)
-    const char* nn = std::getenv("HPG_RING_NN_MIN");
-    D.ring_nn_min = nn ? std::atoi(nn) : 7;
-    const char* rx = std::getenv("HPG_RING_REDUX");
-    D.ring_redux = rx ? std::atoi(rx) : 0;
     if (use_rc) {
       ctx->d_ring.reserve(kSlots * sizeof(RingSlot));
       cuda_check(cudaMemsetAsync(ctx->d_ring.p, 0, kSlots * sizeof(RingSlot), ctx->stream),

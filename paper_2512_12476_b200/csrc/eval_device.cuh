@@ -63,7 +63,6 @@ struct Ws {
   double* edge;      // [N]
   double* wnew;      // [N]
   double* cc;        // [kMaxClasses] class costs at the volume in flight
-  uint8_t* crank;    // [kMaxClasses] rank of each class cost (ties share a rank), ring_heuristic
   double* rm;        // [64] small-ring cost matrix
   double* agg;       // [T*7]
   int32_t* sl_save;  // [sum pp]
@@ -91,7 +90,6 @@ struct Ws {
   int32_t cc_sig_ok;
   double cc_vol;              // staged volume
   int32_t cta_sync;           // sweep: CTA-wide barrier (threads) before each task's cost, 0 = none
-  unsigned long long ring_best;  // ring_small: the warp's best cycle so far (bits of a cost >= 0)
   long long* prof;            // diagnostics: this plan's profile slots
   const uint8_t* cls;         // link class matrix [N*N]: shared-memory copy or P.cls
   // helper-warp team (one plan per CTA, warp 0 leads)
@@ -162,8 +160,7 @@ __device__ inline uint8_t* carve(Ws& s, uint8_t* base, const Carve& c) {
   s.c_hbm = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
   s.edge = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
   s.wnew = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
-  s.cc = reinterpret_cast<double*>(carve_ptr(p, 9 * kMaxClasses));  // + class ranks
-  s.crank = reinterpret_cast<uint8_t*>(s.cc + kMaxClasses);
+  s.cc = reinterpret_cast<double*>(carve_ptr(p, 8 * kMaxClasses));
   s.rm = reinterpret_cast<double*>(carve_ptr(p, 8 * 64));
   s.agg = reinterpret_cast<double*>(carve_ptr(p, 8 * T * 7));
   s.sl = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * c.max_sl));
@@ -192,8 +189,7 @@ __device__ inline uint8_t* carve_team_scratch(Ws& s, uint8_t* p, const Carve& c)
   s.c_pp = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
   s.c_hbm = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
   s.edge = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
-  s.cc = reinterpret_cast<double*>(carve_ptr(p, 9 * kMaxClasses));  // + class ranks
-  s.crank = reinterpret_cast<uint8_t*>(s.cc + kMaxClasses);
+  s.cc = reinterpret_cast<double*>(carve_ptr(p, 8 * kMaxClasses));
   s.rm = reinterpret_cast<double*>(carve_ptr(p, 8 * 64));
   s.tour = carve_ptr(p, N);
   s.peers = carve_ptr(p, N);
@@ -647,50 +643,10 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
     double cached;
     if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
   }
-  // large rings (7, 8 vertices: up to 360 / 2520 cycles) get a better upper
-  // bound before the search: lane v < n builds the nearest-neighbour tour
-  // from vertex v, the warp keeps the best of them, and the lanes share their
-  // best cycle during the search. Smaller rings search directly.
-  const bool big = n >= P.ring_nn_min;
-  if (big && lane < n) {
-    unsigned used = 1u << lane;
-    int cur = lane;
-    double mx = 0.0;
-    for (int step = 1; step < n; ++step) {
-      double bc = kInf;
-      int bi = 0;
-      for (int u = 0; u < n; ++u) {
-        if ((used >> u) & 1u) continue;
-        const double c = rm[cur * n + u];
-        if (c < bc) {
-          bc = c;
-          bi = u;
-        }
-      }
-      used |= 1u << bi;
-      mx = smax(mx, bc);
-      cur = bi;
-    }
-    ub = smin(ub, smax(mx, rm[cur * n + lane]));
-  }
-  if (big) ub = warp_min(ub);
-  // lb <= optimum <= ub: a tour at the lower bound is optimal
-  if (big && ub <= lb) {
-    double stored;
-    if (P.ring_cache && ring_payload_of(P, s, key, ub, stored)) ring_insert(P, key, stored);
-    return ub;
-  }
   double best = ub;
-  // the lanes share their best complete cycle through the warp's shared slot
-  // (costs are >= 0, so their bit patterns order like the values): every
-  // lane prunes against the best found by any lane. Exact min either way.
-  volatile unsigned long long* shared_best = &s.ring_best;
-  if (lane == 0) *shared_best = static_cast<unsigned long long>(__double_as_longlong(best));
-  __syncwarp();
   const int m = n - 1;
   const int nprefix = m * (m - 1);
   for (int p = lane; p < nprefix; p += 32) {
-    if (big) best = smin(best, __longlong_as_double(static_cast<long long>(*shared_best)));
     const int a = 1 + p / (m - 1);
     const int bi = p % (m - 1);
     const int b = 1 + bi + ((1 + bi) >= a ? 1 : 0);
@@ -712,13 +668,7 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
     nxt[3] = 1;
     while (d >= 3) {
       if (d == n) {
-        const double cyc = smax(cmx[n - 1], rm[path[n - 1] * n]);
-        if (cyc < best) {
-          best = cyc;
-          if (big)
-            atomicMin(const_cast<unsigned long long*>(shared_best),
-                      static_cast<unsigned long long>(__double_as_longlong(cyc)));
-        }
+        best = smin(best, smax(cmx[n - 1], rm[path[n - 1] * n]));
         --d;
         used &= ~(1u << path[d]);
         continue;
@@ -731,7 +681,6 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
         continue;
       }
       nxt[d] = v + 1;
-      if (big) best = smin(best, __longlong_as_double(static_cast<long long>(*shared_best)));
       const double c = smax(cmx[d - 1], rm[path[d - 1] * n + v]);
       if (c >= best) continue;
       path[d] = v;
@@ -741,8 +690,6 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
       nxt[d] = 1;
     }
   }
-  __syncwarp();
-  if (big) best = smin(best, __longlong_as_double(static_cast<long long>(*shared_best)));
   best = warp_min(best);
   double stored;
   if (P.ring_cache && ring_payload_of(P, s, key, best, stored)) ring_insert(P, key, stored);
@@ -791,65 +738,31 @@ __device__ __noinline__ double ring_heuristic(const DevProblem& P, Ws& s, const 
   if (lane == 0) used[0] = true;
   int last = devs[0];
   if (lane == 0) tour[0] = devs[0];
-  if (P.ring_redux) {
-    // every edge cost is the staged cost of its link class, so "cheapest next
-    // vertex, earliest index among equals" is the minimum of (rank of the
-    // class cost, index): one 32-bit warp reduction per step. Ranks count
-    // the strictly cheaper classes, so equal costs share a rank.
-    for (int c = lane; c < P.n_classes; c += 32) {
-      int rank = 0;
-      const double cc = s.cc[c];
-      for (int q = 0; q < P.n_classes; ++q) rank += s.cc[q] < cc ? 1 : 0;
-      s.crank[c] = static_cast<uint8_t>(rank);
-    }
-    __syncwarp();
-    const uint8_t* cls = s.cls;
-    const uint8_t* crank = s.crank;
-    const int N = P.n_dev;
-    for (int step = 1; step < n; ++step) {
-      unsigned key = 0xffffffffu;
-      for (int r = 0; r < 8; ++r) {
-        const int i = lane + 32 * r;
-        if (i >= n) break;
-        if (!used[r]) {
-          const unsigned k = (static_cast<unsigned>(crank[cls[last * N + devs[i]]]) << 8) |
-                             static_cast<unsigned>(i);
-          key = k < key ? k : key;
+  for (int step = 1; step < n; ++step) {
+    double bc = kInf;
+    int bi = 0x7fffffff;
+    for (int r = 0; r < 8; ++r) {
+      const int i = lane + 32 * r;
+      if (i >= n) break;
+      if (!used[r]) {
+        const double c = ecost(P, s, last, devs[i]);
+        if (c < bc) {
+          bc = c;
+          bi = i;
         }
       }
-      key = __reduce_min_sync(kFull, key);
-      const int bi = static_cast<int>(key & 0xffu);
-      if ((bi & 31) == lane) used[bi >> 5] = true;
-      last = devs[bi];
-      if (lane == 0) tour[step] = static_cast<uint8_t>(last);
     }
-  } else {
-    for (int step = 1; step < n; ++step) {
-      double bc = kInf;
-      int bi = 0x7fffffff;
-      for (int r = 0; r < 8; ++r) {
-        const int i = lane + 32 * r;
-        if (i >= n) break;
-        if (!used[r]) {
-          const double c = ecost(P, s, last, devs[i]);
-          if (c < bc) {
-            bc = c;
-            bi = i;
-          }
-        }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oc = __shfl_xor_sync(kFull, bc, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      if (oc < bc || (oc == bc && oi < bi)) {
+        bc = oc;
+        bi = oi;
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double oc = __shfl_xor_sync(kFull, bc, o);
-        const int oi = __shfl_xor_sync(kFull, bi, o);
-        if (oc < bc || (oc == bc && oi < bi)) {
-          bc = oc;
-          bi = oi;
-        }
-      }
-      if ((bi & 31) == lane) used[bi >> 5] = true;
-      last = devs[bi];
-      if (lane == 0) tour[step] = static_cast<uint8_t>(last);
     }
+    if ((bi & 31) == lane) used[bi >> 5] = true;
+    last = devs[bi];
+    if (lane == 0) tour[step] = static_cast<uint8_t>(last);
   }
   __syncwarp();
   double bott = 0.0;

@@ -34,8 +34,7 @@ __device__ __forceinline__ void carve_e2e(Ws& s, uint8_t* base, const E2ESizes& 
   s.c_pp = reinterpret_cast<double*>(carve_ptr(p, 8 * z.cell_max));
   s.c_hbm = reinterpret_cast<double*>(carve_ptr(p, 8 * z.cell_max));
   s.edge = reinterpret_cast<double*>(carve_ptr(p, 8 * z.ring_max));
-  s.cc = reinterpret_cast<double*>(carve_ptr(p, 9 * kMaxClasses));  // + class ranks
-  s.crank = reinterpret_cast<uint8_t*>(s.cc + kMaxClasses);
+  s.cc = reinterpret_cast<double*>(carve_ptr(p, 8 * kMaxClasses));
   s.rm = reinterpret_cast<double*>(carve_ptr(p, 8 * 64));
   s.agg = reinterpret_cast<double*>(carve_ptr(p, 8 * T * 7));
   s.sl = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * z.sl));
