@@ -601,26 +601,6 @@ __device__ __noinline__ void ring_insert(const DevProblem& P, const RingKey& k, 
   }
 }
 
-// Depth-first completion of a ring over N vertices from a fixed prefix
-// (0, a, b, ...), depth D next: candidates in ascending vertex order, a
-// branch pruned once its running maximum reaches the best cycle so far, the
-// cycle closed back to vertex 0 at depth N. The depth is a template
-// parameter, so the path lives in registers (no local-memory arrays).
-template <int N, int D>
-__device__ __forceinline__ void ring_dfs(const double* rm, unsigned used, int prev, double cmx,
-                                         double& best) {
-  if constexpr (D == N) {
-    best = smin(best, smax(cmx, rm[prev * N]));
-  } else {
-    for (int v = 1; v < N; ++v) {
-      if ((used >> v) & 1u) continue;
-      const double c = smax(cmx, rm[prev * N + v]);
-      if (c >= best) continue;
-      ring_dfs<N, D + 1>(rm, used | (1u << v), v, c, best);
-    }
-  }
-}
-
 // Exact min-bottleneck Hamiltonian cycle, 3 <= n <= 8 (the reference's
 // RingSearch::dfs regime, cost_model.cpp:94-125, 196-206). The answer is a min
 // of maxes of the same doubles, so any exact method returns identical bits:
@@ -676,13 +656,38 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
       best = smin(best, smax(c2, rm[b * n]));
       continue;
     }
-    const unsigned used = 1u | (1u << a) | (1u << b);
-    switch (n) {
-      case 4: ring_dfs<4, 3>(rm, used, b, c2, best); break;
-      case 5: ring_dfs<5, 3>(rm, used, b, c2, best); break;
-      case 6: ring_dfs<6, 3>(rm, used, b, c2, best); break;
-      case 7: ring_dfs<7, 3>(rm, used, b, c2, best); break;
-      default: ring_dfs<8, 3>(rm, used, b, c2, best); break;
+    int path[8];
+    double cmx[8];
+    int nxt[9];
+    path[0] = 0;
+    path[1] = a;
+    path[2] = b;
+    cmx[2] = c2;
+    unsigned used = 1u | (1u << a) | (1u << b);
+    int d = 3;
+    nxt[3] = 1;
+    while (d >= 3) {
+      if (d == n) {
+        best = smin(best, smax(cmx[n - 1], rm[path[n - 1] * n]));
+        --d;
+        used &= ~(1u << path[d]);
+        continue;
+      }
+      int v = nxt[d];
+      while (v < n && ((used >> v) & 1u)) ++v;
+      if (v >= n) {
+        --d;
+        if (d >= 3) used &= ~(1u << path[d]);
+        continue;
+      }
+      nxt[d] = v + 1;
+      const double c = smax(cmx[d - 1], rm[path[d - 1] * n + v]);
+      if (c >= best) continue;
+      path[d] = v;
+      cmx[d] = c;
+      used |= 1u << v;
+      ++d;
+      nxt[d] = 1;
     }
   }
   best = warp_min(best);
