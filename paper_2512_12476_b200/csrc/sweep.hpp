@@ -45,6 +45,7 @@ struct SweepPartial {
 constexpr int kClsSweepMax = 16384;
 struct SweepLaunch {
   int warps = 8;
+  int blocks = 2;  // CTAs per SM
   int grid = 0;
   int slab_bytes = 0;
   int cls_bytes = 0;

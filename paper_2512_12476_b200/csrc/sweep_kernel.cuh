@@ -52,8 +52,9 @@ __device__ __forceinline__ void carve_e2e(Ws& s, uint8_t* base, const E2ESizes& 
   s.ccell = nullptr;
 }
 
-template <int kWarps>
-__global__ void __launch_bounds__(32 * kWarps, 16 / kWarps)
+// kWarps plan-warps per CTA, kBlocks CTAs per SM (the register budget)
+template <int kWarps, int kBlocks>
+__global__ void __launch_bounds__(32 * kWarps, kBlocks)
 sweep_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCostConfig cfg,
              const uint8_t* __restrict__ recs, int64_t stride,
              int64_t n, uint64_t k0, int slab_bytes, int cls_smem, uint8_t* __restrict__ gslab,
@@ -150,11 +151,11 @@ sweep_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCo
 }  // namespace dev
 
 namespace {
-template <int kWarps>
+template <int kWarps, int kBlocks>
 cudaError_t sweep_launch_impl(const DevProblem& P, const DevCostConfig& cfg, const uint8_t* d_recs,
                               int64_t stride, int64_t n, uint64_t k0, SweepLaunch& L,
                               const uint32_t* d_order, EvalResult* d_res, cudaStream_t st) {
-  auto kern = dev::sweep_kernel<kWarps>;
+  auto kern = dev::sweep_kernel<kWarps, kBlocks>;
   const int dyn = L.cls_bytes + kWarps * L.slab_bytes;
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), dyn);
   if (e != cudaSuccess) return e;
@@ -164,9 +165,9 @@ cudaError_t sweep_launch_impl(const DevProblem& P, const DevCostConfig& cfg, con
   return cudaGetLastError();
 }
 
-template <int kWarps>
+template <int kWarps, int kBlocks>
 cudaError_t sweep_plan_impl(int N, int T, int n_sm, int slab_req, SweepLaunch& L) {
-  auto kern = dev::sweep_kernel<kWarps>;
+  auto kern = dev::sweep_kernel<kWarps, kBlocks>;
   cudaFuncAttributes fa{};
   cudaError_t e = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return e;
@@ -175,11 +176,11 @@ cudaError_t sweep_plan_impl(int N, int T, int n_sm, int slab_req, SweepLaunch& L
   cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   L.warps = kWarps;
+  L.blocks = kBlocks;
   L.cls_bytes = N * N <= kClsSweepMax ? carve_round(N * N) : 0;
-  const int blocks = 16 / kWarps;  // 16 plan-warps per SM (128 registers per thread)
   // per-CTA budget: the SM's shared memory split over the resident CTAs, less
   // the static Ws array and the 1 KB the driver reserves per CTA
-  int per_cta = smem_sm / blocks - static_cast<int>(fa.sharedSizeBytes) - 1024;
+  int per_cta = smem_sm / kBlocks - static_cast<int>(fa.sharedSizeBytes) - 1024;
   if (per_cta > smem_blk - static_cast<int>(fa.sharedSizeBytes)) per_cta = smem_blk - static_cast<int>(fa.sharedSizeBytes);
   int slab = ((per_cta - L.cls_bytes) / kWarps) & ~15;
   if (slab_req > 0 && slab_req < slab) slab = slab_req & ~15;
@@ -199,21 +200,31 @@ cudaError_t sweep_plan_impl(int N, int T, int n_sm, int slab_req, SweepLaunch& L
 }
 }  // namespace
 
+// shapes (warps x CTAs per SM): 8x2 (default), 16x1 and 8x1 (every warp of
+// an SM in one CTA, phase-aligned), 4x4, 2x8
 cudaError_t sweep_plan(int N, int T, int n_sm, int warps, int slab_req, SweepLaunch& L) {
-  if (warps == 4) return sweep_plan_impl<4>(N, T, n_sm, slab_req, L);
-  if (warps == 2) return sweep_plan_impl<2>(N, T, n_sm, slab_req, L);
-  return sweep_plan_impl<8>(N, T, n_sm, slab_req, L);
+  switch (warps) {
+    case 16: return sweep_plan_impl<16, 1>(N, T, n_sm, slab_req, L);
+    case 81: return sweep_plan_impl<8, 1>(N, T, n_sm, slab_req, L);
+    case 4: return sweep_plan_impl<4, 4>(N, T, n_sm, slab_req, L);
+    case 2: return sweep_plan_impl<2, 8>(N, T, n_sm, slab_req, L);
+    default: return sweep_plan_impl<8, 2>(N, T, n_sm, slab_req, L);
+  }
 }
 
 cudaError_t launch_sweep(const DevProblem& P, const DevCostConfig& cfg, const uint8_t* d_recs,
                          int64_t stride, int64_t n, uint64_t k0, SweepLaunch& L,
                          const uint32_t* d_order, EvalResult* d_res, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (L.warps == 16)
+    return sweep_launch_impl<16, 1>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
+  if (L.warps == 8 && L.blocks == 1)
+    return sweep_launch_impl<8, 1>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
   if (L.warps == 4)
-    return sweep_launch_impl<4>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
+    return sweep_launch_impl<4, 4>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
   if (L.warps == 2)
-    return sweep_launch_impl<2>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
-  return sweep_launch_impl<8>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
+    return sweep_launch_impl<2, 8>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
+  return sweep_launch_impl<8, 2>(P, cfg, d_recs, stride, n, k0, L, d_order, d_res, st);
 }
 
 }  // namespace hpg
