@@ -1192,6 +1192,54 @@ __device__ __noinline__ void task_cost(const DevProblem& P, const DevCostConfig&
             s.dpr[k0 + j * tp + k] = ecost(P, s, dv[flat(0, j, k, pp, tp)], dv[flat(1, j, k, pp, tp)]);
             s.dpr_sl[k0 + j * tp + k] = nl_j;
           }
+        } else if (dp <= 8 && tp <= 32) {
+          // the stage's tp exact rings at once: one lane per (ring k, vertex
+          // v) computes v's identity-tour edge (UB) and 2nd-cheapest incident
+          // edge (LB), folded per ring with 64-bit atomicMax on the bit
+          // patterns (costs >= 0) in the ring scratch; LB == UB settles the
+          // ring (ring_small's own fast path), the rest go to ring_small
+          // with their UB. Same decisions, same bits, one pass for all rings.
+          unsigned long long* ubb = reinterpret_cast<unsigned long long*>(s.rm);
+          unsigned long long* lbb = ubb + 32;
+          __syncwarp();
+          for (int k = lane; k < tp; k += 32) ubb[k] = lbb[k] = 0ull;
+          __syncwarp();
+          for (int it = lane; it < tp * dp; it += 32) {
+            const int k = it / dp, v = it - (it / dp) * dp;
+            const int a = dv[flat(v, j, k, pp, tp)];
+            const double ub = ecost(P, s, a, dv[flat(v + 1 < dp ? v + 1 : 0, j, k, pp, tp)]);
+            double m1 = kInf, m2 = kInf;
+            for (int u = 0; u < dp; ++u) {
+              if (u == v) continue;
+              const double x = ecost(P, s, a, dv[flat(u, j, k, pp, tp)]);
+              if (x < m1) {
+                m2 = m1;
+                m1 = x;
+              } else if (x < m2) {
+                m2 = x;
+              }
+            }
+            atomicMax(&ubb[k], static_cast<unsigned long long>(__double_as_longlong(ub)));
+            atomicMax(&lbb[k], static_cast<unsigned long long>(__double_as_longlong(m2)));
+          }
+          __syncwarp();
+          // lane k keeps ring k's bounds (the scratch is ring_small's matrix)
+          const double my_ub = lane < tp ? __longlong_as_double(static_cast<long long>(ubb[lane])) : 0.0;
+          const double my_lb = lane < tp ? __longlong_as_double(static_cast<long long>(lbb[lane])) : 0.0;
+          const unsigned open = __ballot_sync(kFull, lane < tp && my_ub != my_lb);
+          if (lane < tp) {
+            s.dpr[k0 + j * tp + lane] = my_ub;
+            s.dpr_sl[k0 + j * tp + lane] = nl_j;
+          }
+          for (unsigned rest = open; rest; rest &= rest - 1) {
+            const int k = __ffs(rest) - 1;
+            const double ub = __shfl_sync(kFull, my_ub, k);
+            __syncwarp();
+            for (int i = lane; i < dp; i += 32) s.peers[i] = dv[flat(i, j, k, pp, tp)];
+            __syncwarp();
+            const double r = ring_small(P, s, s.peers, dp, ub);
+            if (lane == 0) s.dpr[k0 + j * tp + k] = r;
+          }
         } else {
           for (int k = 0; k < tp; ++k) {
             __syncwarp();
