@@ -835,7 +835,12 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   std::vector<short4> opts;
   std::vector<Poly256> jumps;
   std::map<int32_t, int32_t> jump_at;  // gen_draws -> first polynomial
-  std::vector<GaRun> gr(n);
+  // the host writes (and ships) only a run's head: its set-up fields, the GA
+  // scalars and the population slot map; the population costs, mutation /
+  // speculation stages and swap snapshots behind it are written by the
+  // device before they are read
+  constexpr size_t kRunHead = offsetof(GaRun, pop_cost);
+  std::unique_ptr<GaRun[]> gr(new GaRun[static_cast<size_t>(std::max(n, 1))]);
   // pass 1 (host pool): per run, its layout-option count, draw count per
   // candidate and record bounds
   struct RunPrep {
@@ -900,7 +905,7 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
     const ArmRun& r = *runs[i];
     const ArmEnv& e = *r.env;
     GaRun& g = gr[i];
-    std::memset(static_cast<void*>(&g), 0, sizeof(g));
+    std::memset(static_cast<void*>(&g), 0, kRunHead);
     g.slice = r.slice;
     g.ng = static_cast<int32_t>(e.tg.size());
     g.opt_base = opt_base[i];
@@ -981,7 +986,8 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   // staging sized generously once per context: pinned allocations are slow
   ctx.h_ga.reserve(std::max<int64_t>(h_total, int64_t{32} << 20));
   uint8_t* H = ctx.h_ga.p;
-  std::memcpy(H + h_runs, gr.data(), sizeof(GaRun) * n);
+  for (int i = 0; i < n; ++i)
+    std::memcpy(H + h_runs + static_cast<int64_t>(sizeof(GaRun)) * i, &gr[i], kRunHead);
   GaRun* hr = reinterpret_cast<GaRun*>(H + h_runs);
   unsigned long long* hctl = reinterpret_cast<unsigned long long*>(H + h_ctl);
   std::memset(hctl, 0, 8 * kGaCtlWords);
@@ -1000,7 +1006,8 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   std::memcpy(H + h_opts, opts.data(), 8 * opts.size());
   std::memcpy(H + h_jump, jumps.data(), 32 * jumps.size());
   cudaStream_t st = ctx.stream;
-  cuda_check(cudaMemcpyAsync(D + o_runs, H + h_runs, sizeof(GaRun) * n, cudaMemcpyHostToDevice, st), "H2D ga runs");
+  cuda_check(cudaMemcpy2DAsync(D + o_runs, sizeof(GaRun), H + h_runs, sizeof(GaRun), kRunHead, n,
+                               cudaMemcpyHostToDevice, st), "H2D ga runs");
   cuda_check(cudaMemcpyAsync(D + o_ctl, H + h_ctl, 8 * kGaCtlWords, cudaMemcpyHostToDevice, st), "H2D ga ctl");
   cuda_check(cudaMemcpyAsync(D + o_rank, H + h_rank, 8 * 256, cudaMemcpyHostToDevice, st), "H2D ga ranks");
   cuda_check(cudaMemsetAsync(D + o_qseq, 0, 8 * q_cap, st), "ga queue clear");
@@ -1064,7 +1071,7 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   G.prof = ga_log ? 1 : 0;
   const int64_t scratch = eval_scratch_doubles(P.N, ctx.max_nl);
   ctx.d_scratch.reserve(static_cast<size_t>(32 * ctx.n_sm) * scratch);
-  const int64_t h2d = static_cast<int64_t>(sizeof(GaRun)) * n + 8 * kGaCtlWords + 8 * 256 +
+  const int64_t h2d = static_cast<int64_t>(kRunHead) * n + 8 * kGaCtlWords + 8 * 256 +
                       16 * static_cast<int64_t>(n) + 8 * static_cast<int64_t>(opts.size()) +
                       32 * static_cast<int64_t>(jumps.size());
   const double t_launch = now_s();
