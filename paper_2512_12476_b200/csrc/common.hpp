@@ -16,6 +16,22 @@
 #define HPG_HD inline
 #endif
 
+// Device-side bounds checks of the checked build (libhpg_checked.so, make
+// checked): a failed check prints the condition and traps the kernel, which
+// surfaces as a CUDA error on the host. Compiled out of libhpg.so.
+#if defined(HPG_CHECKED) && defined(__CUDA_ARCH__)
+#include <cstdio>
+#define HPG_DCHECK(cond)                                                              \
+  do {                                                                                \
+    if (!(cond)) {                                                                    \
+      printf("HPG_DCHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);         \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define HPG_DCHECK(cond) ((void)0)
+#endif
+
 namespace hpg {
 
 constexpr int kMaxTasks = 6;        // PPO: tasks 1..6 (workflow.cpp:64-69)

@@ -801,6 +801,7 @@ eval_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCos
   if (threadIdx.x == 0) {
     Ws& l = team[0];
     uint8_t* p = carve(l, smem, cv);
+    HPG_DCHECK(p - smem <= cv.bytes);
     l.dtab = gscratch + static_cast<int64_t>(blockIdx.x) * gscratch_doubles;
     l.dtab_stride = 0;
     l.prof = nullptr;

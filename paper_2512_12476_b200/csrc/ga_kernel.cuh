@@ -135,8 +135,12 @@ struct GaView {
   int opt_off[kMaxTasks + 1];
   int64_t opt_base;
   GaSm sm;
-  __device__ uint8_t* slot(int k) const { return pool + static_cast<int64_t>(k) * stride; }
+  __device__ uint8_t* slot(int k) const {
+    HPG_DCHECK(k >= 0 && k < 2 + c_ga.pop_cap + c_ga.res_per_run);
+    return pool + static_cast<int64_t>(k) * stride;
+  }
   __device__ uint8_t* wave_slot(int buf, int i) const {
+    HPG_DCHECK(buf >= 0 && buf <= 1 && i >= 0 && buf * c_ga.max_wave + i < c_ga.res_per_run);
     return slot(2 + c_ga.pop_cap + buf * c_ga.max_wave + i);
   }
 };
@@ -595,6 +599,7 @@ __device__ void ga_init_part(const GaView& v, const Rng& rng, int64_t combo0, in
     const long long a = c_ga.prof ? clock64() : 0;
     if (c > tl) rng_apply_jump(r, jumps + 4 * (L - 2));
     if (c_ga.prof) tj += clock64() - a;
+    HPG_DCHECK(c < c_ga.init_cap);
     ga_lane_make(v, combo0 + c, r, v.wave_slot(0, c), sc);
     snaps[c] = r;
   }
@@ -772,6 +777,7 @@ __device__ void ga_score(const GaView& v, GaHot& h, const uint8_t* rec_g, double
     h.impr_time = ga_timer();
     if ((threadIdx.x & 31) == 0) {
       const unsigned long long k = atomicAdd(&c_ga.ctl[kGaCtlImpr], 1ull);
+      HPG_DCHECK(static_cast<int64_t>(k) < c_ga.impr_cap);
       if (static_cast<int64_t>(k) < c_ga.impr_cap)
         c_ga.impr[k] = GaImpr{v.run, 0, h.used, cost, h.impr_time};
     }
@@ -1535,6 +1541,7 @@ ga_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCostC
                                     nullptr, nullptr, rec);
       int last = 0;
       if (lane == 0) {
+        HPG_DCHECK(run >= 0 && run < c_ga.n_runs && buf * c_ga.max_wave + idx < c_ga.res_per_run);
         c_ga.res[static_cast<int64_t>(run) * c_ga.res_per_run + buf * c_ga.max_wave + idx] = e;
         atomicAdd(&c_ga.ctl[kGaCtlEvals], 1ull);
         atomicAdd(&c_ga.ctl[kGaCtlBytes], static_cast<unsigned long long>(cb));

@@ -123,6 +123,7 @@ sweep_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCo
       const int need = e2e_carve_bytes(z, N, T);
       const bool fits = need <= slab_bytes;
       spilled += fits ? 0 : 1;
+      HPG_DCHECK(fits || need <= gslab_bytes);
       carve_e2e(s, fits ? slab : gbase, z, N, T);
     }
     __syncwarp();

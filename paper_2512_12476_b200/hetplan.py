@@ -30,7 +30,9 @@ from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhpg.so")
+# HPG_LIBRARY selects another build of the engine (diagnostics: the
+# bounds-checked libhpg_checked.so, `make -C paper_2512_12476_b200/csrc checked`)
+LIB_PATH = os.environ.get("HPG_LIBRARY") or os.path.join(_HERE, "libhpg.so")
 
 HPG_OK, HPG_USAGE, HPG_INPUT, HPG_INFEASIBLE, HPG_INTERNAL = 0, 2, 3, 4, 5
 
