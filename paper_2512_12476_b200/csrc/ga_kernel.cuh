@@ -1570,6 +1570,15 @@ cudaError_t ga_launch_team(const DevProblem& P, const DevCostConfig& cfg, Carve 
                            int n_sm, int& grid, cudaStream_t st) {
   auto kern = dev::ga_kernel<kTeam>;
   cv.n_warps = kTeam;
+  // the N x N link-class matrix in each worker's shared memory: small
+  // problems always; up to 128 devices (16 KB) for the helper-warp teams of
+  // the narrow, latency-bound rounds (HPG_GA_CLS_TEAM=0 turns that off)
+  static const int cls_team = [] {
+    const char* v = std::getenv("HPG_GA_CLS_TEAM");
+    return v ? std::atoi(v) : 1;
+  }();
+  const int nn = P.n_dev * P.n_dev;
+  cv.cls_smem = nn <= 4096 || (kTeam > 1 && cls_team && nn <= kClsSmemMax) ? 1 : 0;
   cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave, G.n_dev, G.n_regions,
                                                     G.n_nodes);
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), cv.bytes);
@@ -1592,9 +1601,6 @@ cudaError_t ga_launch_team(const DevProblem& P, const DevCostConfig& cfg, Carve 
 cudaError_t launch_ga_offspring(const DevProblem& P, const DevCostConfig& cfg, Carve cv,
                                 const GaParams& G, double* gscratch, int64_t gscratch_doubles,
                                 int n_sm, int& grid, cudaStream_t st) {
-  // small problems: each persistent worker keeps the N x N link-class matrix
-  // in shared memory (after everything else in its carve)
-  cv.cls_smem = P.n_dev * P.n_dev <= 4096 ? 1 : 0;
   // few live runs (at most one per SM): workers with helper warps, which
   // shorten each evaluation (measured per SHA round on c1-c4: teams of four
   // win whenever runs <= SMs and lose throughput in the wide early rounds)
