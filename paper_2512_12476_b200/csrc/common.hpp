@@ -100,8 +100,6 @@ struct DevProblem {
   const double* bw;    // [n_classes] bytes/s (inf for self)
   RingSlot* ring_cache;       // nullptr = disabled
   unsigned long long ring_mask;  // slots - 1 (power of two)
-  int32_t ring_dp_min;        // exact rings of at least this many vertices by thresholds (ring_small)
-  int32_t pad_;
 };
 
 // ---- packed plan record ----

@@ -410,11 +410,6 @@ void stage_problem(Ctx& ctxr, Problem&& P) {
     constexpr size_t kSlots = size_t(1) << 20;
     D.ring_cache = nullptr;
     D.ring_mask = kSlots - 1;
-    // exact rings from this size up are decided by edge-cost thresholds
-    // (ring_by_thresholds); HPG_RING_DP_MIN overrides for A/B (9 = never)
-    const char* dpm = std::getenv("HPG_RING_DP_MIN");
-    D.ring_dp_min = dpm ? std::atoi(dpm) : 7;
-    D.pad_ = 0;
     if (use_rc) {
       ctx->d_ring.reserve(kSlots * sizeof(RingSlot));
       cuda_check(cudaMemsetAsync(ctx->d_ring.p, 0, kSlots * sizeof(RingSlot), ctx->stream),

@@ -601,52 +601,6 @@ __device__ __noinline__ void ring_insert(const DevProblem& P, const RingKey& k, 
   }
 }
 
-// Exact bottleneck ring by thresholds (n <= 8): the optimum is the smallest
-// directed edge cost t in [lb, ub) for which a Hamiltonian cycle through
-// vertex 0 exists on the edges of cost <= t, or ub when none does (ub is a
-// cycle). Feasibility is monotone in t and the optimum is one of the edge
-// costs, so the minimum feasible candidate is the same double the search
-// below returns. Each lane tests its own candidates with a subset DP:
-// reach[S] = the vertices at which a path 0 -> ... -> v through exactly the
-// vertex set S can end (vertices 1..n-1 as bits 0..n-2).
-__device__ __noinline__ double ring_by_thresholds(const double* rm, int n, double lb, double ub) {
-  const int lane = threadIdx.x & 31;
-  const unsigned full = (1u << (n - 1)) - 1u;
-  double best = ub;
-  for (int e = lane; e < n * n; e += 32) {
-    const int a = e / n, b = e - a * n;
-    if (a == b) continue;
-    const double t = rm[e];
-    if (t < lb || !(t < best)) continue;
-    unsigned out0 = 0, back = 0;
-    uint8_t into[7];
-    for (int u = 1; u < n; ++u) {
-      if (rm[u] <= t) out0 |= 1u << (u - 1);
-      if (rm[u * n] <= t) back |= 1u << (u - 1);
-      unsigned in = 0;
-      for (int v = 1; v < n; ++v)
-        if (v != u && rm[v * n + u] <= t) in |= 1u << (v - 1);
-      into[u - 1] = static_cast<uint8_t>(in);
-    }
-    uint8_t reach[128];
-    for (unsigned S = 1; S <= full; ++S) {
-      unsigned r;
-      if ((S & (S - 1)) == 0) {
-        r = S & out0;
-      } else {
-        r = 0;
-        for (unsigned rest = S; rest; rest &= rest - 1) {
-          const int u = __ffs(rest) - 1;
-          if (reach[S ^ (1u << u)] & into[u]) r |= 1u << u;
-        }
-      }
-      reach[S] = static_cast<uint8_t>(r);
-    }
-    if (reach[full] & back) best = t;
-  }
-  return warp_min(best);
-}
-
 // Exact min-bottleneck Hamiltonian cycle, 3 <= n <= 8 (the reference's
 // RingSearch::dfs regime, cost_model.cpp:94-125, 196-206). The answer is a min
 // of maxes of the same doubles, so any exact method returns identical bits:
@@ -688,12 +642,6 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
     key = ring_key(P, s, devs, n);
     double cached;
     if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
-  }
-  if (n >= P.ring_dp_min) {
-    const double r = ring_by_thresholds(rm, n, lb, ub);
-    double stored;
-    if (P.ring_cache && ring_payload_of(P, s, key, r, stored)) ring_insert(P, key, stored);
-    return r;
   }
   double best = ub;
   const int m = n - 1;
