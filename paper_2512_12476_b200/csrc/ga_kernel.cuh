@@ -1574,11 +1574,11 @@ cudaError_t ga_launch_team(const DevProblem& P, const DevCostConfig& cfg, Carve 
   // problems always; up to 128 devices (16 KB) for the helper-warp teams of
   // the narrow, latency-bound rounds (HPG_GA_CLS_TEAM=0 turns that off)
   static const int cls_team = [] {
-    const char* v = std::getenv("HPG_GA_CLS_TEAM");
+    const char* v = std::getenv("HPG_GA_CLS_TEAM");  // 0: off, 1: teams, 2: every worker
     return v ? std::atoi(v) : 1;
   }();
   const int nn = P.n_dev * P.n_dev;
-  cv.cls_smem = nn <= 4096 || (kTeam > 1 && cls_team && nn <= kClsSmemMax) ? 1 : 0;
+  cv.cls_smem = nn <= 4096 || ((kTeam > 1 ? cls_team >= 1 : cls_team >= 2) && nn <= kClsSmemMax) ? 1 : 0;
   cv.bytes = carve2_bytes(cv) + dev::ga_smem_bytes(G.max_stride, G.max_wave, G.n_dev, G.n_regions,
                                                     G.n_nodes);
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), cv.bytes);
