@@ -199,7 +199,7 @@ HPG_HD int carve_bytes(const Carve& c) {
   b += 7 * carve_round(8 * N) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
        carve_round(8 * T * 7);
   b += 2 * carve_round(4 * c.max_sl) + carve_round(4 * c.max_dpk) + carve_round(4 * N);
-  b += carve_round(c.max_slots) + carve_round(T * N) + carve_round(N > 64 ? N : 64) + carve_round(N);
+  b += carve_round(c.max_slots) + carve_round(T * N) + 2 * carve_round(N);
   return b;
 }
 
@@ -214,7 +214,7 @@ constexpr int kClsSmemMax = 16384;
 HPG_HD int team_scratch_bytes(const Carve& c) {
   const int N = c.n_dev;
   return 5 * carve_round(8 * N) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
-         carve_round(N > 64 ? N : 64) + carve_round(N);
+         2 * carve_round(N);
 }
 
 HPG_HD int carve2_bytes(const Carve& c) {
@@ -269,8 +269,7 @@ HPG_HD int e2e_carve_bytes(const E2ESizes& z, int N, int T) {
          carve_round(4 * z.dpk) + carve_round(8 * N) + 4 * carve_round(8 * z.cell_max) +
          carve_round(8 * z.ring_max) + carve_round(8 * kMaxClasses) + carve_round(8 * 64) +
          carve_round(8 * T * 7) + carve_round(4 * z.sl) + 2 * carve_round(8 * z.sl) +
-         carve_round(z.slots) + carve_round(T * N) + carve_round(z.ring_max > 64 ? z.ring_max : 64) +
-         carve_round(z.ring_max);
+         carve_round(z.slots) + carve_round(T * N) + 2 * carve_round(z.ring_max);
 }
 
 }  // namespace hpg

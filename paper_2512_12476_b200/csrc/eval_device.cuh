@@ -169,7 +169,7 @@ __device__ inline uint8_t* carve(Ws& s, uint8_t* base, const Carve& c) {
   s.split_best = reinterpret_cast<int32_t*>(carve_ptr(p, 4 * N));
   s.dev = carve_ptr(p, c.max_slots);
   s.dstage = carve_ptr(p, T * N);
-  s.tour = carve_ptr(p, N > 64 ? N : 64);  // also ring_small's 8 x 8 neighbour order
+  s.tour = carve_ptr(p, N);
   s.peers = carve_ptr(p, N);
   s.cmin = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_cells));
   s.mmt = reinterpret_cast<double*>(carve_ptr(p, 8 * c.max_sl));
@@ -191,7 +191,7 @@ __device__ inline uint8_t* carve_team_scratch(Ws& s, uint8_t* p, const Carve& c)
   s.edge = reinterpret_cast<double*>(carve_ptr(p, 8 * N));
   s.cc = reinterpret_cast<double*>(carve_ptr(p, 8 * kMaxClasses));
   s.rm = reinterpret_cast<double*>(carve_ptr(p, 8 * 64));
-  s.tour = carve_ptr(p, N > 64 ? N : 64);  // also ring_small's 8 x 8 neighbour order
+  s.tour = carve_ptr(p, N);
   s.peers = carve_ptr(p, N);
   return p;
 }
@@ -643,25 +643,6 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
     double cached;
     if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
   }
-  // every vertex's neighbours by increasing edge cost (ties by index), in
-  // the tour scratch: the search tries cheaper edges first, so at each depth
-  // the first edge whose running maximum reaches the best cycle ends that
-  // level (every later sibling costs at least as much). Exact either way.
-  uint8_t* ord = s.tour;
-  __syncwarp();
-  if (lane < n) {
-    const double* row = rm + lane * n;
-    for (int k = 0, w = 0; k < n; ++k) {
-      if (k == lane) continue;
-      // rank of k among the row's other vertices
-      int r = 0;
-      for (int u = 0; u < n; ++u)
-        if (u != lane && u != k && (row[u] < row[k] || (row[u] == row[k] && u < k))) ++r;
-      ord[lane * 8 + r] = static_cast<uint8_t>(k);
-      ++w;
-    }
-  }
-  __syncwarp();
   double best = ub;
   const int m = n - 1;
   const int nprefix = m * (m - 1);
@@ -684,7 +665,7 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
     cmx[2] = c2;
     unsigned used = 1u | (1u << a) | (1u << b);
     int d = 3;
-    nxt[3] = 0;
+    nxt[3] = 1;
     while (d >= 3) {
       if (d == n) {
         best = smin(best, smax(cmx[n - 1], rm[path[n - 1] * n]));
@@ -692,27 +673,21 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
         used &= ~(1u << path[d]);
         continue;
       }
-      const uint8_t* o = ord + path[d - 1] * 8;
-      int k = nxt[d];
-      while (k < n - 1 && ((used >> o[k]) & 1u)) ++k;
-      if (k >= n - 1) {
+      int v = nxt[d];
+      while (v < n && ((used >> v) & 1u)) ++v;
+      if (v >= n) {
         --d;
         if (d >= 3) used &= ~(1u << path[d]);
         continue;
       }
-      const int v = o[k];
+      nxt[d] = v + 1;
       const double c = smax(cmx[d - 1], rm[path[d - 1] * n + v]);
-      if (c >= best) {
-        // the remaining candidates of this level cost at least as much
-        nxt[d] = n - 1;
-        continue;
-      }
-      nxt[d] = k + 1;
+      if (c >= best) continue;
       path[d] = v;
       cmx[d] = c;
       used |= 1u << v;
       ++d;
-      nxt[d] = 0;
+      nxt[d] = 1;
     }
   }
   best = warp_min(best);

@@ -42,7 +42,7 @@ __device__ __forceinline__ void carve_e2e(Ws& s, uint8_t* base, const E2ESizes& 
   s.wmt = reinterpret_cast<double*>(carve_ptr(p, 8 * z.sl));
   s.dev = carve_ptr(p, z.slots);
   s.dstage = carve_ptr(p, T * N);
-  s.tour = carve_ptr(p, z.ring_max > 64 ? z.ring_max : 64);  // + ring_small's neighbour order
+  s.tour = carve_ptr(p, z.ring_max);
   s.peers = carve_ptr(p, z.ring_max);
   // balancer state: never touched by end_to_end_cost
   s.wnew = s.wsave = nullptr;
