@@ -706,8 +706,7 @@ __device__ __forceinline__ EvalResult eval_one(const DevProblem& P, const DevCos
   for (int i = lane; i < s.o.dpk[P.n_tasks]; i += 32) s.dpr_sl[i] = -1;
   __syncwarp();
   if (s.n_warps > 1 && P.n_tasks > 1 && mode != kModeMemcheck) {
-    // per task, spread over the team: micro-batches, memory tables and
-    // the geometry memo every later phase needs
+    // per task, spread over the team: micro-batches and memory tables
     team_job(P, cfg, s, kJobStage, (1 << P.n_tasks) - 1);
   } else {
     for (int t = 0; t < P.n_tasks; ++t) {

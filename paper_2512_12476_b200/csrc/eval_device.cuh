@@ -1302,9 +1302,11 @@ __device__ __forceinline__ void team_share(const DevProblem& P, const DevCostCon
       if (kind == kJobTasks) {
         task_cost(P, cfg, s, t, true, s.agg + 7 * t);
       } else if (kind == kJobStage) {
+        // micro-batches and memory tables only: the geometry memo waits for
+        // the memory gate (evaluate skips infeasible candidates) and is then
+        // spread over the team by team_geometry or built inside task_cost
         apportion(P, s, t);
         mem_tables(P, cfg, s, t);
-        ensure_geometry(P, s, t);
       } else {
         ensure_geometry(P, s, t);
       }
