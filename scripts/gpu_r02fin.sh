@@ -1,5 +1,5 @@
 #!/usr/bin/env bash
-# round 2 final (after the GA link-class staging): full GPU suite, smoke, bench + reference arm, launch list, ncu captures
+# round 2 final (geometry after the memory gate): full GPU suite, smoke, bench + reference arm, launch list, ncu captures
 cd "$(dirname "$0")/.."
 O=gpurun_out
 timeout 2400 python -m pytest tests -m gpu -q -rs > $O/r02fin_pytest.txt 2>&1; echo "pytest rc=$?" >> $O/r02fin_pytest.txt
