@@ -74,7 +74,7 @@ struct RingSlot {
   unsigned long long k1, k2, k3;
   double value;
   unsigned long long state;
-  unsigned long long pad;
+  unsigned long long seq;  // n > 8: arena byte offset << 16 | n of the stored device sequence
 };
 static_assert(sizeof(RingSlot) == 48, "ring slot layout");
 
@@ -100,6 +100,10 @@ struct DevProblem {
   const double* bw;    // [n_classes] bytes/s (inf for self)
   RingSlot* ring_cache;       // nullptr = disabled
   unsigned long long ring_mask;  // slots - 1 (power of two)
+  // device sequences of the memoised rings with n > 8 (their keys are
+  // hashes: a hit is confirmed byte for byte); word 0 = bytes used
+  uint8_t* ring_arena;
+  unsigned long long ring_arena_cap;
 };
 
 // ---- packed plan record ----

@@ -410,14 +410,37 @@ void stage_problem(Ctx& ctxr, Problem&& P) {
     constexpr size_t kSlots = size_t(1) << 20;
     D.ring_cache = nullptr;
     D.ring_mask = kSlots - 1;
+    D.ring_arena = nullptr;
+    D.ring_arena_cap = 0;
     if (use_rc) {
-      ctx->d_ring.reserve(kSlots * sizeof(RingSlot));
-      cuda_check(cudaMemsetAsync(ctx->d_ring.p, 0, kSlots * sizeof(RingSlot), ctx->stream),
-                 "ring cache clear");
+      // slots, then the sequence arena (64 MiB; its first word counts the
+      // bytes handed out, starting after itself)
+      constexpr size_t kArena = size_t(64) << 20;
+      const size_t slot_bytes = kSlots * sizeof(RingSlot);
+      ctx->d_ring.reserve(slot_bytes + kArena);
+      cuda_check(cudaMemsetAsync(ctx->d_ring.p, 0, slot_bytes, ctx->stream), "ring cache clear");
+      const unsigned long long start = 16;
+      cuda_check(cudaMemcpyAsync(ctx->d_ring.p + slot_bytes, &start, 8, cudaMemcpyHostToDevice,
+                                 ctx->stream), "ring arena reset");
       cuda_check(cudaStreamSynchronize(ctx->stream), "ring cache clear");
       D.ring_cache = reinterpret_cast<RingSlot*>(ctx->d_ring.p);
+      D.ring_arena = ctx->d_ring.p + slot_bytes;
+      D.ring_arena_cap = kArena;
     }
   }
+}
+
+// Empties the device-wide ring memo and its sequence arena (on the context's
+// stream): every search starts cold, so no ring value is carried from one
+// search to the next (the memo is a within-search cache).
+void reset_ring_memo(Ctx& ctx) {
+  const DevProblem& D = ctx.dprob;
+  if (!D.ring_cache) return;
+  cuda_check(cudaMemsetAsync(D.ring_cache, 0, (D.ring_mask + 1) * sizeof(RingSlot), ctx.stream),
+             "ring memo reset");
+  static const unsigned long long start = 16;
+  cuda_check(cudaMemcpyAsync(D.ring_arena, &start, 8, cudaMemcpyHostToDevice, ctx.stream),
+             "ring arena reset");
 }
 
 namespace {

@@ -254,6 +254,7 @@ struct Ctx {
 Ctx* create_ctx(const hpg_problem& p, int device);
 void stage_problem(Ctx& ctx, Problem&& P);
 void restage(Ctx& ctx, const hpg_problem& p);
+void reset_ring_memo(Ctx& ctx);
 
 // Packs `b`, runs eval_kernel, returns per-plan results (and balanced records).
 // writes a wave's [generation weights | stage layers] section into the record

@@ -556,11 +556,16 @@ __device__ __forceinline__ bool ring_payload_of(const DevProblem& P, const Ws& s
   return true;
 }
 
-// lane 0 probes; result broadcast. Returns true and sets v on a hit.
-__device__ __noinline__ bool ring_lookup(const DevProblem& P, const RingKey& k, double& v) {
+// lane 0 probes; result broadcast. Returns true and sets v on a hit. Keys of
+// rings with n > 8 are hashes: a hit is confirmed against the device
+// sequence stored with the slot, byte for byte (warp-collective), so a hash
+// collision reads as a miss and never changes a ring's value.
+__device__ __noinline__ bool ring_lookup(const DevProblem& P, const RingKey& k, double& v,
+                                         const uint8_t* devs, int n) {
   const int lane = threadIdx.x & 31;
   int hit = 0;
   double val = 0.0;
+  unsigned long long seq = 0;
   if (lane == 0 && P.ring_cache) {
     const unsigned long long h = (k.k1 ^ mix64d(k.k2 ^ k.k3)) & P.ring_mask;
     for (int pr = 0; pr < 8; ++pr) {
@@ -572,18 +577,44 @@ __device__ __noinline__ bool ring_lookup(const DevProblem& P, const RingKey& k, 
       __threadfence();
       if (sl->k2 == k.k2 && sl->k3 == k.k3) {
         val = sl->value;
+        seq = sl->seq;
         hit = 1;
         break;
       }
     }
   }
   hit = __shfl_sync(kFull, hit, 0);
+  if (hit && n > 8) {
+    seq = __shfl_sync(kFull, seq, 0);
+    const uint8_t* stored = P.ring_arena + (seq >> 16);
+    bool diff = static_cast<int>(seq & 0xffffull) != n;
+    if (!diff)
+      for (int i = lane; i < n; i += 32) diff |= __ldcg(stored + i) != devs[i];
+    if (__any_sync(kFull, diff)) hit = 0;
+  }
   v = __shfl_sync(kFull, val, 0);
   return hit != 0;
 }
 
-__device__ __noinline__ void ring_insert(const DevProblem& P, const RingKey& k, double v) {
-  if ((threadIdx.x & 31) != 0 || !P.ring_cache) return;
+__device__ __noinline__ void ring_insert(const DevProblem& P, const RingKey& k, double v,
+                                         const uint8_t* devs, int n) {
+  if (!P.ring_cache) return;
+  const int lane = threadIdx.x & 31;
+  // n > 8: the sequence goes to the arena first (no room: not memoised)
+  unsigned long long off = 0;
+  if (n > 8) {
+    if (lane == 0) {
+      off = atomicAdd(reinterpret_cast<unsigned long long*>(P.ring_arena),
+                      static_cast<unsigned long long>(n));
+      if (off + n > P.ring_arena_cap) off = 0;
+    }
+    off = __shfl_sync(kFull, off, 0);
+    if (off == 0) return;
+    for (int i = lane; i < n; i += 32) P.ring_arena[off + i] = devs[i];
+    __threadfence();
+    __syncwarp();
+  }
+  if (lane != 0) return;
   const unsigned long long h = (k.k1 ^ mix64d(k.k2 ^ k.k3)) & P.ring_mask;
   for (int pr = 0; pr < 8; ++pr) {
     RingSlot* sl = P.ring_cache + ((h + pr) & P.ring_mask);
@@ -593,6 +624,7 @@ __device__ __noinline__ void ring_insert(const DevProblem& P, const RingKey& k, 
       vs->k2 = k.k2;
       vs->k3 = k.k3;
       vs->value = v;
+      vs->seq = (off << 16) | static_cast<unsigned long long>(n);
       __threadfence();
       vs->state = 1;
       return;
@@ -641,7 +673,7 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
   if (P.ring_cache) {
     key = ring_key(P, s, devs, n);
     double cached;
-    if (ring_lookup(P, key, cached)) return ring_payload_value(s, key, cached);
+    if (ring_lookup(P, key, cached, devs, n)) return ring_payload_value(s, key, cached);
   }
   double best = ub;
   const int m = n - 1;
@@ -692,7 +724,7 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
   }
   best = warp_min(best);
   double stored;
-  if (P.ring_cache && ring_payload_of(P, s, key, best, stored)) ring_insert(P, key, stored);
+  if (P.ring_cache && ring_payload_of(P, s, key, best, stored)) ring_insert(P, key, stored, devs, n);
   return best;
 }
 
@@ -925,10 +957,10 @@ __device__ inline double ring_bottleneck_impl(const DevProblem& P, Ws& s, const 
   if (!P.ring_cache) return ring_heuristic(P, s, devs, n);
   const RingKey key = ring_key(P, s, devs, n);
   double v;
-  if (ring_lookup(P, key, v)) return ring_payload_value(s, key, v);
+  if (ring_lookup(P, key, v, devs, n)) return ring_payload_value(s, key, v);
   v = ring_heuristic(P, s, devs, n);
   double stored;
-  if (ring_payload_of(P, s, key, v, stored)) ring_insert(P, key, stored);
+  if (ring_payload_of(P, s, key, v, stored)) ring_insert(P, key, stored, devs, n);
   return v;
 }
 

@@ -81,6 +81,7 @@ double exhaustive_space_estimate(const Problem& P, const Knobs& K) {
 }
 
 SearchOut exhaustive_search(Ctx& ctx, const Knobs& K) {
+  reset_ring_memo(ctx);
   const Problem& P = ctx.prob;
   const double t0 = now_s();
   const int64_t launches0 = ctx.launches, plans0 = ctx.plans_evaluated;

@@ -1514,6 +1514,7 @@ void exchange_runs(Ctx& ctx, Dist& d, std::vector<ArmRun*>& all, double now) {
 SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
   (void)dist;
   if (K.budget < 1) throw UsageError("search budget must be >= 1");
+  reset_ring_memo(ctx);
   const Problem& P = ctx.prob;
   const double t0 = now_s();
   const int64_t launches0 = ctx.launches, plans0 = ctx.plans_evaluated;
@@ -1866,6 +1867,7 @@ SearchOut nested_sha_search(Ctx& ctx, const Knobs& K, Dist* dist) {
 SearchOut ga_search(Ctx& ctx, const Grouping& tg, const std::vector<int>& counts, int64_t slice,
                     uint64_t seed, const Knobs& K) {
   if (slice < 1) throw UsageError("ga_search needs a budget of at least 1 evaluation");
+  reset_ring_memo(ctx);
   const Problem& P = ctx.prob;
   if (counts.size() != tg.size()) throw InputError("gpu grouping must list one count per task group");
   const double t0 = now_s();
