@@ -728,6 +728,162 @@ __device__ __noinline__ double ring_small(const DevProblem& P, Ws& s, const uint
   return best;
 }
 
+// Open TP cells of one 32-cell block (LB < UB after the bounds pass), rings
+// of 3 <= n <= 8 devices, batched over the warp instead of one ring_small per
+// cell: memo probes and inserts one lane per cell (the n <= 8 keys are
+// exact), then the exact DFS over (cell, 2-vertex prefix) items dealt
+// round-robin to the lanes. Each cell's incumbent (its identity-tour UB to
+// start) is shared through a 64-bit atomicMin on its bit pattern in ubb
+// (costs >= 0 order like their bits), so a cycle found by any lane prunes the
+// others. The result is the min over all cycles of the max edge, the same
+// double ring_small returns.
+__device__ __forceinline__ int nth_set_bit(unsigned m, int k) {
+  for (int i = 0; i < k; ++i) m &= m - 1;
+  return __ffs(m) - 1;
+}
+
+__device__ __noinline__ void open_rings(const DevProblem& P, Ws& s, const uint8_t* dv, int n,
+                                        int c0, unsigned open, unsigned long long* ubb,
+                                        double* out) {
+  const int lane = threadIdx.x & 31;
+  const bool memo = P.ring_cache != nullptr;
+  const bool sig = P.n_classes <= 16;
+  unsigned long long k2 = 0;
+  if (memo) k2 = sig ? cc_signature(P, s) : static_cast<unsigned long long>(__double_as_longlong(s.cc_vol));
+  const unsigned long long k3 = static_cast<unsigned long long>(n) | (sig ? kSigMode : 0ull);
+  const int nopen = __popc(open);
+  int my_c = -1;
+  unsigned long long my_k1 = 0, h = 0;
+  bool hit = false;
+  if (lane < nopen) {
+    my_c = c0 + nth_set_bit(open, lane);
+    const uint8_t* r = dv + my_c * n;
+    unsigned long long pk = 0;
+    for (int i = 0; i < n; ++i) pk |= static_cast<unsigned long long>(r[i]) << (8 * i);
+    my_k1 = pk == 0 ? 1 : pk;
+    if (memo) {
+      // ring_lookup's probe (n <= 8: the key is the ring itself)
+      h = (my_k1 ^ mix64d(k2 ^ k3)) & P.ring_mask;
+      for (int pr = 0; pr < 8; ++pr) {
+        volatile RingSlot* sl = P.ring_cache + ((h + pr) & P.ring_mask);
+        const unsigned long long a = sl->k1;
+        if (a == 0) break;
+        if (a != my_k1) continue;
+        if (sl->state != 1) break;
+        __threadfence();
+        if (sl->k2 == k2 && sl->k3 == k3) {
+          const double val = sl->value;
+          out[my_c] = sig ? s.cc[__double_as_longlong(val)] : val;
+          hit = true;
+          break;
+        }
+      }
+    }
+  }
+  const unsigned miss = __ballot_sync(kFull, lane < nopen && !hit);
+  if (miss) {
+    const int N = P.n_dev;
+    const int m = n - 1, npre = m * (m - 1);
+    const int items = __popc(miss) * npre;
+    for (int it = lane; it < items; it += 32) {
+      const int k = it / npre, p = it - k * npre;
+      const int c = c0 + nth_set_bit(open, nth_set_bit(miss, k));
+      const uint8_t* r = dv + c * n;
+      unsigned long long dw = 0;
+      for (int i = 0; i < n; ++i) dw |= static_cast<unsigned long long>(r[i]) << (8 * i);
+      // rm[i * n + j] of ring_small = ecost(devs[i], devs[j])
+      auto E = [&](int i, int j) {
+        return s.cc[s.cls[static_cast<int>((dw >> (8 * i)) & 255u) * N +
+                          static_cast<int>((dw >> (8 * j)) & 255u)]];
+      };
+      const int a = 1 + p / (m - 1);
+      const int bi = p % (m - 1);
+      const int b = 1 + bi + ((1 + bi) >= a ? 1 : 0);
+      double best = __longlong_as_double(static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&ubb[c - c0])));
+      const double start = best;
+      const double c2 = smax(E(0, a), E(a, b));
+      if (c2 >= best) continue;
+      if (n == 3) {
+        best = smin(best, smax(c2, E(b, 0)));
+      } else {
+        int path[8];
+        double cmx[8];
+        int nxt[9];
+        path[0] = 0;
+        path[1] = a;
+        path[2] = b;
+        cmx[2] = c2;
+        unsigned used = 1u | (1u << a) | (1u << b);
+        int d = 3;
+        nxt[3] = 1;
+        while (d >= 3) {
+          if (d == n) {
+            best = smin(best, smax(cmx[n - 1], E(path[n - 1], 0)));
+            --d;
+            used &= ~(1u << path[d]);
+            continue;
+          }
+          int v = nxt[d];
+          while (v < n && ((used >> v) & 1u)) ++v;
+          if (v >= n) {
+            --d;
+            if (d >= 3) used &= ~(1u << path[d]);
+            continue;
+          }
+          nxt[d] = v + 1;
+          const double cc = smax(cmx[d - 1], E(path[d - 1], v));
+          if (cc >= best) continue;
+          path[d] = v;
+          cmx[d] = cc;
+          used |= 1u << v;
+          ++d;
+          nxt[d] = 1;
+        }
+      }
+      if (best < start)
+        atomicMin(&ubb[c - c0], static_cast<unsigned long long>(__double_as_longlong(best)));
+    }
+    __syncwarp();
+    if ((miss >> lane) & 1u) {
+      const double v = __longlong_as_double(
+          static_cast<long long>(*reinterpret_cast<volatile unsigned long long*>(&ubb[my_c - c0])));
+      out[my_c] = v;
+      if (memo) {
+        // ring_payload_of + ring_insert (n <= 8: no arena), one lane per cell
+        double stored = v;
+        bool ok = true;
+        if (sig) {
+          ok = false;
+          for (int j = 0; j < P.n_classes; ++j)
+            if (s.cc[j] == v) {
+              stored = __longlong_as_double(static_cast<long long>(j));
+              ok = true;
+              break;
+            }
+        }
+        if (ok) {
+          for (int pr = 0; pr < 8; ++pr) {
+            RingSlot* sl = P.ring_cache + ((h + pr) & P.ring_mask);
+            const unsigned long long prev = atomicCAS(&sl->k1, 0ULL, my_k1);
+            if (prev == 0) {
+              volatile RingSlot* vs = sl;
+              vs->k2 = k2;
+              vs->k3 = k3;
+              vs->value = stored;
+              vs->seq = static_cast<unsigned long long>(n);
+              __threadfence();
+              vs->state = 1;
+              break;
+            }
+            if (prev == my_k1) break;
+          }
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
 // Top-2 (value, position) among edges, excluding positions ex0/ex1.
 __device__ __forceinline__ void top2_merge(double& v1, int& p1, double& v2, int& p2, double ov1,
                                            int op1, double ov2, int op2) {
@@ -1069,6 +1225,7 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
         atomicMax(&lbb[c], static_cast<unsigned long long>(__double_as_longlong(m2)));
       }
       __syncwarp();
+      HPG_PH_COUNT(30, ncell);
       unsigned open = 0;  // cells left to the exact search (rare)
       for (int c0 = 0; c0 < ncell; c0 += 32) {
         const int c = c0 + lane;
@@ -1081,12 +1238,11 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
           }
         }
         open = __ballot_sync(kFull, o);
-        while (open) {
-          const int cc = c0 + __ffs(open) - 1;
-          open &= open - 1;
-          const double ub = __longlong_as_double(static_cast<long long>(ubb[cc]));
-          const double r = ring_small(P, s, dv + cc * tp, tp, ub);
-          if (lane == 0) s.rtp[cell0 + cc] = r;
+        if (open) {
+          HPG_PH_BEGIN(28);
+          open_rings(P, s, dv, tp, c0, open, ubb + c0, s.rtp + cell0);
+          HPG_PH_END(28);
+          HPG_PH_COUNT(29, __popc(open));
         }
       }
     } else {
@@ -1113,14 +1269,23 @@ __device__ __noinline__ void ensure_geometry(const DevProblem& P, Ws& s, int t) 
         s.ppp[cell0 + c] = best;
       }
     } else {
-      // cheapest pair per (cell, next stage): the warp over the tp x tp pairs
-      for (int c = 0; c < ncell; ++c) {
-        if (c % pp + 1 >= pp) continue;
+      // cheapest pair per (cell, next stage): groups of g lanes per cell, g
+      // the largest power of two that keeps every lane on one pass over the
+      // cells (g = 1: a lane per cell), each group over the tp x tp pairs and
+      // a min across the group (a min of the same doubles in any order)
+      const int nq = dp * (pp - 1);
+      int g = 1;
+      while (2 * g <= 32 && 2 * g <= tt && 2 * g * nq <= 32) g *= 2;
+      const int per = 32 / g, sub = lane & (g - 1), grp = lane / g;
+      for (int q0 = 0; q0 < nq; q0 += per) {
+        const int q = q0 + grp;
+        const int c = q < nq ? (q / (pp - 1)) * pp + q % (pp - 1) : 0;
         double best = kInf;
-        for (int xy = lane; xy < tt; xy += 32)
-          best = smin(best, ecost(P, s, dv[c * tp + xy / tp], dv[(c + 1) * tp + xy % tp]));
-        best = warp_min(best);
-        if (lane == 0) s.ppp[cell0 + c] = best;
+        if (q < nq)
+          for (int xy = sub; xy < tt; xy += g)
+            best = smin(best, ecost(P, s, dv[c * tp + xy / tp], dv[(c + 1) * tp + xy % tp]));
+        for (int o = g >> 1; o > 0; o >>= 1) best = smin(best, __shfl_xor_sync(kFull, best, o));
+        if (q < nq && sub == 0) s.ppp[cell0 + c] = best;
       }
     }
     __syncwarp();

@@ -1463,7 +1463,7 @@ ga_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevCostC
     uint8_t* p = carve(l, smem, cv);
     l.dtab = gscratch + static_cast<int64_t>(blockIdx.x) * gscratch_doubles;
     l.dtab_stride = 0;
-    l.prof = nullptr;
+    l.prof = g_plan_prof;  // diagnostics only (HPG_GA_LOG): a shared dummy slot block
     l.team = team;
     l.n_warps = kTeam;
     l.job_words[0] = l.job_words[1] = 0;

@@ -1077,6 +1077,13 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   const double t_launch = now_s();
   cuda_check(cudaEventRecord(ctx.ev0, st), "event");
   int grid = 0;
+  // diagnostics (HPG_GA_LOG): the evaluation phase accumulators run inside
+  // the GA kernel too (one shared dummy per-plan slot block)
+  static long long* d_prof_dummy = nullptr;
+  if (ga_log) {
+    if (!d_prof_dummy) cuda_check(cudaMalloc(&d_prof_dummy, sizeof(long long) * 64), "profile alloc");
+    cuda_check(eval_set_plan_profile(d_prof_dummy), "profile symbol");
+  }
   cuda_check(launch_ga_offspring(ctx.dprob, cfg, cv, G, ctx.d_scratch.p, scratch, ctx.n_sm, grid, st),
              "ga_kernel launch");
   if (grid > max_workers) throw InternalError("ga_kernel grid exceeds its scratch");
@@ -1158,6 +1165,17 @@ void device_ga(Ctx& ctx, const Knobs& K, const std::vector<ArmRun*>& runs, doubl
   waves += mx;
   clock = now_s();
   if (ga_log) {
+    cuda_check(eval_set_plan_profile(nullptr), "profile symbol");
+    unsigned long long acc[32];
+    cuda_check(eval_phase_acc(acc), "phase acc");
+    if (FILE* f = std::fopen(ga_log, "a")) {
+      // cumulative evaluation phases (kcycles): geometry, TP rings, PP pairs,
+      // exact searches of open TP cells (kcycles, count), TP cells with 3-8
+      // vertices
+      std::fprintf(f, "  phases: geometry %.1f tp %.1f pp %.1f open %.1f n_open %llu cells %llu\n",
+                   1e-3 * acc[12], 1e-3 * acc[13], 1e-3 * acc[14], 1e-3 * acc[28], acc[29], acc[30]);
+      std::fclose(f);
+    }
     if (FILE* f = std::fopen(ga_log, "a")) {
       // runs grid stride evals impr max_waves prep_ms kernel_ms total_ms |
       // step_kcycles_avg steps eval_kcycles_avg evals
